@@ -1,0 +1,172 @@
+/*
+ * mtgp_b200.h -- C-ABI of the B200-native MTGP32 bulk generator (libmtgp_b200.so).
+ *
+ * This is the drop-in boundary under the reference's generation path. The reference binds
+ * its generation path through C++, not an FFI:
+ *
+ *   class WordSource { virtual void fill(std::span<std::uint32_t> out) = 0; }
+ *        proj/include/twistsieve/word_source.hpp:21-25
+ *   std::unique_ptr<WordSource> make_word_source(const ParameterizedStatus&, std::uint32_t seed)
+ *        proj/include/twistsieve/word_source.hpp:75-76, proj/src/word_source.cpp:5-16
+ *   Generator(ParameterizedStatus, seed) / next_u32 / next_f64_01 / from_state
+ *        proj/include/twistsieve/generator.hpp:23-52, proj/src/generator.cpp:37-66
+ *
+ * Each entry point below names the reference interface it replaces. The C++ layer
+ * (include/twistsieve_b200/ headers: GpuWordSource : WordSource, make_word_source for
+ * Engine::mtgp32) sits on top of these calls; INTEGRATION.md shows the binding.
+ *
+ * Conventions (mirroring the reference's error behaviour without exceptions across the ABI):
+ *   - every function returns MTGP_OK (0) or a positive MTGP_E* code;
+ *   - MTGP_EINVAL is what the reference reports as std::invalid_argument
+ *     (ParameterizedStatus::validate, proj/src/params.cpp:23-39; generator.cpp:40-41,57-59);
+ *   - mtgp_last_error() returns a thread-local message for the last failure on this thread;
+ *   - a context is not thread-safe (one per host thread, like one Generator per worker,
+ *     SPEC.md:104-105); it owns one CUDA stream and all its device memory.
+ *   - There is no CPU fallback: without a usable sm_100 device, mtgp_ctx_create fails with
+ *     MTGP_ECUDA.
+ *
+ * Output layout: per-stream contiguous. A call with words_per_stream = L writes stream s
+ * (parameter set s with seed s) at out[s*L, (s+1)*L) and advances every stream by L words,
+ * exactly as L successive WordSource::fill() words would (word_source.hpp:31-33).
+ */
+#ifndef MTGP_B200_H
+#define MTGP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MTGP_ABI_VERSION 1
+
+/* status codes */
+#define MTGP_OK 0
+#define MTGP_EINVAL 1   /* invalid parameter set / argument  (reference: std::invalid_argument) */
+#define MTGP_ECUDA 2    /* CUDA runtime failure or no usable device                           */
+#define MTGP_ENOMEM 3   /* device or pinned-host allocation failed                            */
+#define MTGP_ESTATE 4   /* call not valid in the context's current state                      */
+
+/* output kinds */
+#define MTGP_U32 0      /* tempered 32-bit word                                  */
+#define MTGP_F32_12 1   /* single float in [1,2): bits (u32 >> 9) | 0x3F800000   */
+#define MTGP_F32_01OC 2 /* single float in (0,1]: 2.0f - [1,2) value (exact)     */
+
+/*
+ * One MTGP32 parameter set. Field meaning follows mtgp32_params_fast
+ * (/usr/local/cuda/include/curand_mtgp32.h:140-152); poly_sha1 is not needed on the device.
+ * Replaces: the recurrence fields of ParameterizedStatus (proj/include/twistsieve/params.hpp:21-42)
+ * for Engine::mtgp32.
+ */
+typedef struct mtgp_params {
+    uint32_t mexp;           /* Mersenne exponent; N = mexp/32 + 1 words of state */
+    uint32_t pos;            /* pick-up position, 3 <= pos, N - pos >= 32         */
+    uint32_t sh1, sh2;       /* shifts, 1..31                                      */
+    uint32_t tbl[16];        /* recursion table (GF(2)-linear in its 4-bit index)  */
+    uint32_t tmp_tbl[16];    /* tempering table                                    */
+    uint32_t flt_tmp_tbl[16];/* tempering+float table: must equal (tmp>>9)|0x3F800000 */
+    uint32_t mask;           /* 0xFFFFFFFF << (32N - mexp)                         */
+} mtgp_params;
+
+/* Per-stream checksum accumulated by the generation kernels (order independent). */
+typedef struct mtgp_cksum {
+    uint64_t sum64;          /* sum of the emitted 32-bit words (float kinds: bit patterns), mod 2^64 */
+    uint64_t words;          /* words emitted                                                        */
+    uint32_t xor32;          /* XOR of the emitted words                                             */
+    uint32_t pad;
+} mtgp_cksum;
+
+typedef struct mtgp_ctx mtgp_ctx;
+
+/* Options for mtgp_set_option */
+#define MTGP_OPT_CHECKSUM 1        /* 0/1: accumulate mtgp_cksum in-kernel (default 1)              */
+#define MTGP_OPT_KERNEL 2          /* 0 = auto, 1 = reference-shaped v1 (one CTA per set), 2 = v2  */
+#define MTGP_OPT_MAX_PIECES 3      /* cap on jump-ahead pieces per call (0 = auto)                  */
+#define MTGP_OPT_MIN_PIECE_WORDS 4 /* minimum words per jump-ahead piece (default 1<<21)            */
+#define MTGP_OPT_TIMING 5          /* 0/1: record CUDA events around every generation kernel        */
+#define MTGP_OPT_HOST_CHUNK 6      /* words per stream per device chunk when out is host memory     */
+
+/* Library / device info. */
+int mtgp_abi_version(void);
+const char* mtgp_last_error(void);
+
+/*
+ * Validate one parameter set (replaces ParameterizedStatus::validate for Engine::mtgp32,
+ * proj/src/params.cpp:23-39): supported shape, mask, shifts, pos window, table linearity,
+ * float table identity. MTGP_EINVAL with a message on failure.
+ */
+int mtgp_validate_params(const mtgp_params* p);
+
+/*
+ * Create a context holding n_sets independent streams; stream s uses sets[s] seeded with
+ * seeds[s] (MTGP seed expansion, curand_mtgp32_host.h:155-172).
+ * Replaces: Generator::Generator(params, seed) (generator.cpp:37-52) and
+ * make_word_source(params, seed) (word_source.cpp:5-16), batched over n_sets streams.
+ * All sets of one context must share mexp. `stream` is a cudaStream_t to run on, or NULL for
+ * a context-owned stream.
+ */
+int mtgp_ctx_create(mtgp_ctx** out, int device, const mtgp_params* sets, uint32_t n_sets,
+                    const uint32_t* seeds, void* stream);
+int mtgp_ctx_destroy(mtgp_ctx* ctx);
+
+/* Number of streams, state words per stream (N), current position (words emitted) of stream s. */
+int mtgp_ctx_info(const mtgp_ctx* ctx, uint32_t* n_sets, uint32_t* state_words, uint32_t* mexp);
+int mtgp_position(const mtgp_ctx* ctx, uint32_t s, uint64_t* words_emitted);
+/* The cudaStream_t all of this context's work is enqueued on. */
+int mtgp_ctx_stream(const mtgp_ctx* ctx, void** stream);
+
+int mtgp_set_option(mtgp_ctx* ctx, int option, int64_t value);
+
+/*
+ * Bulk generation. Writes words_per_stream outputs of every stream, per-stream contiguous,
+ * and advances every stream. out_is_device = 1: `out` is device memory on the context's
+ * device (the call is asynchronous on the context stream); 0: `out` is host memory (pageable
+ * or pinned; the call returns when the data is in `out`).
+ * Replaces: WordSource::fill(std::span<uint32_t>) (word_source.hpp:21-25,31-33) for n_sets
+ * streams at once; the float kinds extend next_f64_01 (generator.hpp:39-41) with the
+ * single-float [1,2) / (0,1] conversions north_star names.
+ */
+int mtgp_generate(mtgp_ctx* ctx, int kind, void* out, uint64_t words_per_stream, int out_is_device);
+int mtgp_generate_u32(mtgp_ctx* ctx, uint32_t* out, uint64_t words_per_stream, int out_is_device);
+int mtgp_generate_f32_12(mtgp_ctx* ctx, float* out, uint64_t words_per_stream, int out_is_device);
+int mtgp_generate_f32_01oc(mtgp_ctx* ctx, float* out, uint64_t words_per_stream, int out_is_device);
+
+/*
+ * Advance every stream by `words` without writing output (GF(2) jump-ahead; cost independent
+ * of `words`). No reference equivalent: the reference can only step.
+ */
+int mtgp_skip(mtgp_ctx* ctx, uint64_t words);
+
+/*
+ * State save / restore: the N-word window x[i..i+N-1] of every stream (oldest first; the low
+ * 32N-mexp bits of the oldest word are dead) plus its position i.
+ * Replaces: SeedStatus {seed, state, index} / Generator::from_state (generator.hpp:11-15,
+ * generator.cpp:54-66). windows: n_sets*N words; positions: n_sets (may be NULL on save).
+ */
+int mtgp_state_save(mtgp_ctx* ctx, uint32_t* windows, uint64_t* positions);
+int mtgp_state_restore(mtgp_ctx* ctx, const uint32_t* windows, const uint64_t* positions);
+
+/* Per-stream checksums accumulated since create / reset (n_sets entries). */
+int mtgp_checksums(mtgp_ctx* ctx, mtgp_cksum* out);
+int mtgp_checksums_reset(mtgp_ctx* ctx);
+
+/* Wait for all work on the context stream. */
+int mtgp_sync(mtgp_ctx* ctx);
+
+/*
+ * Timing of the generation kernels (MTGP_OPT_TIMING = 1): total device milliseconds and launch
+ * count of the main generation kernel, and of the jump-ahead kernels, since the last reset.
+ */
+int mtgp_kernel_timing(mtgp_ctx* ctx, double* gen_ms, uint64_t* gen_launches, double* jump_ms,
+                       uint64_t* jump_launches);
+int mtgp_kernel_timing_reset(mtgp_ctx* ctx);
+
+/* Launch plan of the last generation call: pieces (jump-ahead segments) and warps per piece. */
+int mtgp_last_plan(const mtgp_ctx* ctx, uint32_t* pieces, uint32_t* warps_per_piece,
+                   uint32_t* kernel_version);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MTGP_B200_H */

@@ -1,0 +1,469 @@
+// mtgp_capi.cu -- the C-ABI (include/mtgp_b200.h): contexts, validation, seeding, state
+// save/restore, host<->device staging, and dispatch to the generation kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "mtgp_internal.cuh"
+#include "mtgp_plan.h"
+
+using namespace mtgpb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(e == cudaErrorMemoryAllocation ? MTGP_ENOMEM : MTGP_ECUDA, "%s: %s", what,
+                cudaGetErrorString(e));
+}
+
+#define CK(call, what)                                    \
+    do {                                                  \
+        cudaError_t e_ = (call);                          \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+    } while (0)
+
+// MTGP32 exponents whose state shape we support (the MTGP32 family, Saito & Matsumoto).
+const uint32_t kMtgpMexp[] = {3217, 4253, 4423, 9689, 9941, 11213, 19937, 21701, 23209, 44497};
+
+bool supported_mexp(uint32_t m) {
+    for (uint32_t e : kMtgpMexp)
+        if (e == m) return true;
+    return false;
+}
+
+// Appendix A "Init(seed)"; external pin curand_mtgp32_host.h:155-172.
+void seed_window(const mtgp_params& p, uint32_t seed, uint32_t* x) {
+    const uint32_t n = state_words(p.mexp);
+    const uint32_t hidden = p.tbl[4] ^ (p.tbl[8] << 16);
+    uint32_t c = hidden;
+    c += c >> 16;
+    c += c >> 8;
+    const uint32_t fillw = (c & 0xffu) * 0x01010101u;
+    for (uint32_t i = 0; i < n; ++i) x[i] = fillw;
+    x[0] = seed;
+    x[1] = hidden;
+    for (uint32_t i = 1; i < n; ++i) x[i] ^= 1812433253u * (x[i - 1] ^ (x[i - 1] >> 30)) + i;
+}
+
+}  // namespace
+
+struct mtgp_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    bool own_stream = false;
+    uint32_t n_sets = 0, N = 0, mexp = 0;
+    std::vector<mtgp_params> sets;
+    std::vector<uint64_t> position;
+
+    DevParams* d_params = nullptr;
+    uint32_t* d_win = nullptr;
+    DevCksum* d_ck = nullptr;
+
+    // options
+    bool cksum = true;
+    int kernel = 0;
+    uint32_t max_pieces = 0;
+    uint64_t min_piece_words = 1ull << 21;
+    bool timing = false;
+    uint64_t host_chunk = 1ull << 20;
+
+    // host-output staging
+    void* d_stage = nullptr;
+    size_t stage_bytes = 0;
+    cudaEvent_t ev_gen[2] = {nullptr, nullptr};
+    cudaEvent_t ev_copy[2] = {nullptr, nullptr};
+
+    // timing
+    cudaEvent_t t0 = nullptr, t1 = nullptr, j0 = nullptr, j1 = nullptr;
+    double gen_ms = 0, jump_ms = 0;
+    uint64_t gen_launches = 0, jump_launches = 0;
+
+    // v2 planner / jump-ahead state
+    std::unique_ptr<Planner> planner;
+    uint32_t last_pieces = 0, last_warps = 0, last_kernel = 0;
+};
+
+extern "C" {
+
+int mtgp_abi_version(void) { return MTGP_ABI_VERSION; }
+const char* mtgp_last_error(void) { return g_err.c_str(); }
+
+int mtgp_validate_params(const mtgp_params* p) {
+    if (!p) return fail(MTGP_EINVAL, "null parameter set");
+    if (!supported_mexp(p->mexp)) return fail(MTGP_EINVAL, "unsupported period exponent %u", p->mexp);
+    const uint32_t n = state_words(p->mexp);
+    const uint32_t r = 32 * n - p->mexp;
+    const uint32_t mask = r ? (0xFFFFFFFFu << r) : 0xFFFFFFFFu;
+    if (p->mask != mask) return fail(MTGP_EINVAL, "mask must be 0x%08x for mexp %u", mask, p->mexp);
+    if (p->sh1 < 1 || p->sh1 > 31 || p->sh2 < 1 || p->sh2 > 31)
+        return fail(MTGP_EINVAL, "shifts must be in [1, 31]");
+    if (p->pos < 2 || p->pos + 32 > n)
+        return fail(MTGP_EINVAL, "pick-up position must satisfy 2 <= pos <= N - 32 (N=%u)", n);
+    for (int i = 0; i < 16; ++i) {
+        uint32_t t = 0, m = 0;
+        for (int b = 0; b < 4; ++b)
+            if (i & (1 << b)) {
+                t ^= p->tbl[1 << b];
+                m ^= p->tmp_tbl[1 << b];
+            }
+        if (p->tbl[i] != t || p->tmp_tbl[i] != m)
+            return fail(MTGP_EINVAL, "tables must be GF(2)-linear in their index (entry %d)", i);
+        if (p->flt_tmp_tbl[i] != ((p->tmp_tbl[i] >> 9) | 0x3F800000u))
+            return fail(MTGP_EINVAL, "flt_tmp_tbl[%d] must equal (tmp_tbl>>9)|0x3F800000", i);
+    }
+    return MTGP_OK;
+}
+
+int mtgp_ctx_create(mtgp_ctx** out, int device, const mtgp_params* sets, uint32_t n_sets,
+                    const uint32_t* seeds, void* stream) {
+    if (!out || !sets || !seeds || n_sets == 0) return fail(MTGP_EINVAL, "null argument or n_sets == 0");
+    *out = nullptr;
+    for (uint32_t s = 0; s < n_sets; ++s) {
+        int rc = mtgp_validate_params(&sets[s]);
+        if (rc) return fail(rc, "set %u: %s", s, g_err.c_str());
+        if (sets[s].mexp != sets[0].mexp) return fail(MTGP_EINVAL, "all sets of a context must share mexp");
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(MTGP_ECUDA, "no CUDA device (there is no CPU fallback)");
+    if (device < 0 || device >= ndev) return fail(MTGP_EINVAL, "device %d out of range", device);
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major < 10) return fail(MTGP_ECUDA, "device %d is sm_%d%d; this library is built for sm_100a", device, prop.major, prop.minor);
+    CK(cudaSetDevice(device), "cudaSetDevice");
+
+    auto ctx = std::make_unique<mtgp_ctx>();
+    ctx->device = device;
+    ctx->n_sets = n_sets;
+    ctx->mexp = sets[0].mexp;
+    ctx->N = state_words(ctx->mexp);
+    ctx->sets.assign(sets, sets + n_sets);
+    ctx->position.assign(n_sets, 0);
+    if (stream) {
+        ctx->stream = static_cast<cudaStream_t>(stream);
+    } else {
+        CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        ctx->own_stream = true;
+    }
+    CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (int i = 0; i < 2; ++i) {
+        CK(cudaEventCreateWithFlags(&ctx->ev_gen[i], cudaEventDisableTiming), "cudaEventCreate");
+        CK(cudaEventCreateWithFlags(&ctx->ev_copy[i], cudaEventDisableTiming), "cudaEventCreate");
+    }
+    CK(cudaEventCreate(&ctx->t0), "cudaEventCreate");
+    CK(cudaEventCreate(&ctx->t1), "cudaEventCreate");
+    CK(cudaEventCreate(&ctx->j0), "cudaEventCreate");
+    CK(cudaEventCreate(&ctx->j1), "cudaEventCreate");
+
+    std::vector<DevParams> dp(n_sets);
+    for (uint32_t s = 0; s < n_sets; ++s) {
+        dp[s].pos = sets[s].pos;
+        dp[s].sh1 = sets[s].sh1;
+        dp[s].sh2 = sets[s].sh2;
+        dp[s].mask = sets[s].mask;
+        std::memcpy(dp[s].tbl, sets[s].tbl, sizeof(dp[s].tbl));
+        std::memcpy(dp[s].tmp, sets[s].tmp_tbl, sizeof(dp[s].tmp));
+    }
+    std::vector<uint32_t> win((size_t)n_sets * ctx->N);
+    for (uint32_t s = 0; s < n_sets; ++s) seed_window(sets[s], seeds[s], win.data() + (size_t)s * ctx->N);
+
+    CK(cudaMalloc(&ctx->d_params, sizeof(DevParams) * n_sets), "cudaMalloc params");
+    CK(cudaMalloc(&ctx->d_win, sizeof(uint32_t) * win.size()), "cudaMalloc state");
+    CK(cudaMalloc(&ctx->d_ck, sizeof(DevCksum) * n_sets), "cudaMalloc checksums");
+    CK(cudaMemcpyAsync(ctx->d_params, dp.data(), sizeof(DevParams) * n_sets, cudaMemcpyHostToDevice, ctx->stream), "upload params");
+    CK(cudaMemcpyAsync(ctx->d_win, win.data(), sizeof(uint32_t) * win.size(), cudaMemcpyHostToDevice, ctx->stream), "upload state");
+    CK(cudaMemsetAsync(ctx->d_ck, 0, sizeof(DevCksum) * n_sets, ctx->stream), "memset checksums");
+    CK(cudaStreamSynchronize(ctx->stream), "sync");
+    ctx->planner = std::make_unique<Planner>(ctx->sets, prop.multiProcessorCount);
+    *out = ctx.release();
+    return MTGP_OK;
+}
+
+int mtgp_ctx_destroy(mtgp_ctx* ctx) {
+    if (!ctx) return MTGP_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->copy_stream);
+    ctx->planner.reset();
+    cudaFree(ctx->d_params);
+    cudaFree(ctx->d_win);
+    cudaFree(ctx->d_ck);
+    cudaFree(ctx->d_stage);
+    for (int i = 0; i < 2; ++i) {
+        cudaEventDestroy(ctx->ev_gen[i]);
+        cudaEventDestroy(ctx->ev_copy[i]);
+    }
+    cudaEventDestroy(ctx->t0);
+    cudaEventDestroy(ctx->t1);
+    cudaEventDestroy(ctx->j0);
+    cudaEventDestroy(ctx->j1);
+    cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return MTGP_OK;
+}
+
+int mtgp_ctx_info(const mtgp_ctx* ctx, uint32_t* n_sets, uint32_t* state_words_out, uint32_t* mexp) {
+    if (!ctx) return fail(MTGP_EINVAL, "null context");
+    if (n_sets) *n_sets = ctx->n_sets;
+    if (state_words_out) *state_words_out = ctx->N;
+    if (mexp) *mexp = ctx->mexp;
+    return MTGP_OK;
+}
+
+int mtgp_position(const mtgp_ctx* ctx, uint32_t s, uint64_t* words) {
+    if (!ctx || !words) return fail(MTGP_EINVAL, "null argument");
+    if (s >= ctx->n_sets) return fail(MTGP_EINVAL, "stream %u out of range", s);
+    *words = ctx->position[s];
+    return MTGP_OK;
+}
+
+int mtgp_ctx_stream(const mtgp_ctx* ctx, void** stream) {
+    if (!ctx || !stream) return fail(MTGP_EINVAL, "null argument");
+    *stream = ctx->stream;
+    return MTGP_OK;
+}
+
+int mtgp_set_option(mtgp_ctx* ctx, int option, int64_t value) {
+    if (!ctx) return fail(MTGP_EINVAL, "null context");
+    switch (option) {
+        case MTGP_OPT_CHECKSUM: ctx->cksum = value != 0; return MTGP_OK;
+        case MTGP_OPT_KERNEL:
+            if (value < 0 || value > 2) return fail(MTGP_EINVAL, "kernel must be 0, 1 or 2");
+            ctx->kernel = (int)value;
+            return MTGP_OK;
+        case MTGP_OPT_MAX_PIECES:
+            if (value < 0) return fail(MTGP_EINVAL, "max_pieces must be >= 0");
+            ctx->max_pieces = (uint32_t)value;
+            return MTGP_OK;
+        case MTGP_OPT_MIN_PIECE_WORDS:
+            if (value < 1) return fail(MTGP_EINVAL, "min_piece_words must be >= 1");
+            ctx->min_piece_words = (uint64_t)value;
+            return MTGP_OK;
+        case MTGP_OPT_TIMING: ctx->timing = value != 0; return MTGP_OK;
+        case MTGP_OPT_HOST_CHUNK:
+            if (value < 1) return fail(MTGP_EINVAL, "host chunk must be >= 1");
+            ctx->host_chunk = (uint64_t)value;
+            return MTGP_OK;
+    }
+    return fail(MTGP_EINVAL, "unknown option %d", option);
+}
+
+}  // extern "C"
+
+namespace {
+
+// One device-side generation of L words per stream into device memory `out`.
+int generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
+    if (L == 0) return MTGP_OK;
+    const bool use_v1 = ctx->kernel == 1 || !ctx->planner->v2_supported();
+    if (use_v1) {
+        if (ctx->timing) CK(cudaEventRecord(ctx->t0, ctx->stream), "event");
+        cudaError_t e = launch_v1(kind, ctx->cksum, ctx->d_params, ctx->d_win, ctx->n_sets, ctx->N, out, L,
+                                  ctx->d_ck, ctx->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "v1 generation kernel");
+        if (ctx->timing) {
+            CK(cudaEventRecord(ctx->t1, ctx->stream), "event");
+            CK(cudaEventSynchronize(ctx->t1), "event sync");
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, ctx->t0, ctx->t1), "event time");
+            ctx->gen_ms += ms;
+            ctx->gen_launches++;
+        }
+        ctx->last_pieces = ctx->n_sets;
+        ctx->last_warps = 8;
+        ctx->last_kernel = 1;
+    } else {
+        PlanRun run;
+        run.kind = kind;
+        run.cksum = ctx->cksum;
+        run.params = ctx->d_params;
+        run.win = ctx->d_win;
+        run.ck = ctx->d_ck;
+        run.out = out;
+        run.L = L;
+        run.stream = ctx->stream;
+        run.max_pieces = ctx->max_pieces;
+        run.min_piece_words = ctx->min_piece_words;
+        run.timing = ctx->timing;
+        run.ev[0] = ctx->t0;
+        run.ev[1] = ctx->t1;
+        run.ev[2] = ctx->j0;
+        run.ev[3] = ctx->j1;
+        std::string err;
+        cudaError_t e = ctx->planner->run(run, err);
+        if (e != cudaSuccess) return fail(e == cudaErrorMemoryAllocation ? MTGP_ENOMEM : MTGP_ECUDA, "v2 generation: %s (%s)", err.c_str(), cudaGetErrorString(e));
+        if (!err.empty()) return fail(MTGP_EINVAL, "v2 generation: %s", err.c_str());
+        ctx->gen_ms += run.gen_ms;
+        ctx->jump_ms += run.jump_ms;
+        ctx->gen_launches += run.gen_launches;
+        ctx->jump_launches += run.jump_launches;
+        ctx->last_pieces = run.pieces;
+        ctx->last_warps = run.warps_per_piece;
+        ctx->last_kernel = 2;
+    }
+    for (auto& p : ctx->position) p += L;
+    return MTGP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mtgp_generate(mtgp_ctx* ctx, int kind, void* out, uint64_t L, int out_is_device) {
+    if (!ctx) return fail(MTGP_EINVAL, "null context");
+    if (kind < MTGP_U32 || kind > MTGP_F32_01OC) return fail(MTGP_EINVAL, "unknown output kind %d", kind);
+    if (!out && L) return fail(MTGP_EINVAL, "null output");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (out_is_device) return generate_device(ctx, kind, out, L);
+
+    // Host output: generate chunks of Lc words per stream into a double-buffered device stage
+    // and copy each chunk out with one strided 2-D copy, overlapping generation of chunk c+1
+    // with the copy of chunk c.
+    const uint64_t Lc = std::min<uint64_t>(L, ctx->host_chunk);
+    const size_t chunk_bytes = (size_t)Lc * ctx->n_sets * 4;
+    if (ctx->stage_bytes < 2 * chunk_bytes) {
+        CK(cudaStreamSynchronize(ctx->copy_stream), "sync");
+        cudaFree(ctx->d_stage);
+        ctx->d_stage = nullptr;
+        ctx->stage_bytes = 0;
+        CK(cudaMalloc(&ctx->d_stage, 2 * chunk_bytes), "cudaMalloc stage");
+        ctx->stage_bytes = 2 * chunk_bytes;
+    }
+    char* host = static_cast<char*>(out);
+    int c = 0;
+    for (uint64_t done = 0; done < L; done += Lc, ++c) {
+        const uint64_t len = std::min<uint64_t>(Lc, L - done);
+        const int b = c & 1;
+        char* stage = static_cast<char*>(ctx->d_stage) + b * chunk_bytes;
+        // buffer b is free once its previous copy finished
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_copy[b], 0), "wait");
+        int rc = generate_device(ctx, kind, stage, len);
+        if (rc) return rc;
+        CK(cudaEventRecord(ctx->ev_gen[b], ctx->stream), "event");
+        CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_gen[b], 0), "wait");
+        CK(cudaMemcpy2DAsync(host + done * 4, (size_t)L * 4, stage, (size_t)len * 4, (size_t)len * 4,
+                             ctx->n_sets, cudaMemcpyDeviceToHost, ctx->copy_stream),
+           "D2H copy");
+        CK(cudaEventRecord(ctx->ev_copy[b], ctx->copy_stream), "event");
+    }
+    CK(cudaStreamSynchronize(ctx->copy_stream), "sync");
+    return MTGP_OK;
+}
+
+int mtgp_generate_u32(mtgp_ctx* ctx, uint32_t* out, uint64_t L, int out_is_device) {
+    return mtgp_generate(ctx, MTGP_U32, out, L, out_is_device);
+}
+int mtgp_generate_f32_12(mtgp_ctx* ctx, float* out, uint64_t L, int out_is_device) {
+    return mtgp_generate(ctx, MTGP_F32_12, out, L, out_is_device);
+}
+int mtgp_generate_f32_01oc(mtgp_ctx* ctx, float* out, uint64_t L, int out_is_device) {
+    return mtgp_generate(ctx, MTGP_F32_01OC, out, L, out_is_device);
+}
+
+int mtgp_skip(mtgp_ctx* ctx, uint64_t words) {
+    if (!ctx) return fail(MTGP_EINVAL, "null context");
+    if (words == 0) return MTGP_OK;
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    std::string err;
+    cudaError_t e = ctx->planner->skip(ctx->d_params, ctx->d_win, words, ctx->stream, err);
+    if (e != cudaSuccess) return fail(MTGP_ECUDA, "skip: %s (%s)", err.c_str(), cudaGetErrorString(e));
+    if (!err.empty()) return fail(MTGP_EINVAL, "skip: %s", err.c_str());
+    for (auto& p : ctx->position) p += words;
+    return MTGP_OK;
+}
+
+int mtgp_state_save(mtgp_ctx* ctx, uint32_t* windows, uint64_t* positions) {
+    if (!ctx || !windows) return fail(MTGP_EINVAL, "null argument");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CK(cudaMemcpyAsync(windows, ctx->d_win, (size_t)ctx->n_sets * ctx->N * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H state");
+    CK(cudaStreamSynchronize(ctx->stream), "sync");
+    if (positions) std::copy(ctx->position.begin(), ctx->position.end(), positions);
+    return MTGP_OK;
+}
+
+int mtgp_state_restore(mtgp_ctx* ctx, const uint32_t* windows, const uint64_t* positions) {
+    if (!ctx || !windows) return fail(MTGP_EINVAL, "null argument");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CK(cudaMemcpyAsync(ctx->d_win, windows, (size_t)ctx->n_sets * ctx->N * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D state");
+    CK(cudaStreamSynchronize(ctx->stream), "sync");
+    if (positions) std::copy(positions, positions + ctx->n_sets, ctx->position.begin());
+    return MTGP_OK;
+}
+
+int mtgp_checksums(mtgp_ctx* ctx, mtgp_cksum* out) {
+    if (!ctx || !out) return fail(MTGP_EINVAL, "null argument");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    std::vector<DevCksum> h(ctx->n_sets);
+    CK(cudaMemcpyAsync(h.data(), ctx->d_ck, sizeof(DevCksum) * ctx->n_sets, cudaMemcpyDeviceToHost, ctx->stream), "D2H checksums");
+    CK(cudaStreamSynchronize(ctx->stream), "sync");
+    for (uint32_t s = 0; s < ctx->n_sets; ++s) {
+        out[s].sum64 = h[s].sum64;
+        out[s].words = h[s].words;
+        out[s].xor32 = h[s].xor32;
+        out[s].pad = 0;
+    }
+    return MTGP_OK;
+}
+
+int mtgp_checksums_reset(mtgp_ctx* ctx) {
+    if (!ctx) return fail(MTGP_EINVAL, "null context");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CK(cudaMemsetAsync(ctx->d_ck, 0, sizeof(DevCksum) * ctx->n_sets, ctx->stream), "memset");
+    return MTGP_OK;
+}
+
+int mtgp_sync(mtgp_ctx* ctx) {
+    if (!ctx) return fail(MTGP_EINVAL, "null context");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CK(cudaStreamSynchronize(ctx->stream), "sync");
+    CK(cudaStreamSynchronize(ctx->copy_stream), "sync");
+    return MTGP_OK;
+}
+
+int mtgp_kernel_timing(mtgp_ctx* ctx, double* gen_ms, uint64_t* gen_launches, double* jump_ms,
+                       uint64_t* jump_launches) {
+    if (!ctx) return fail(MTGP_EINVAL, "null context");
+    if (gen_ms) *gen_ms = ctx->gen_ms;
+    if (gen_launches) *gen_launches = ctx->gen_launches;
+    if (jump_ms) *jump_ms = ctx->jump_ms;
+    if (jump_launches) *jump_launches = ctx->jump_launches;
+    return MTGP_OK;
+}
+
+int mtgp_kernel_timing_reset(mtgp_ctx* ctx) {
+    if (!ctx) return fail(MTGP_EINVAL, "null context");
+    ctx->gen_ms = ctx->jump_ms = 0;
+    ctx->gen_launches = ctx->jump_launches = 0;
+    return MTGP_OK;
+}
+
+int mtgp_last_plan(const mtgp_ctx* ctx, uint32_t* pieces, uint32_t* warps, uint32_t* kernel_version) {
+    if (!ctx) return fail(MTGP_EINVAL, "null context");
+    if (pieces) *pieces = ctx->last_pieces;
+    if (warps) *warps = ctx->last_warps;
+    if (kernel_version) *kernel_version = ctx->last_kernel;
+    return MTGP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,56 @@
+// mtgp_internal.cuh -- shared definitions of the B200 MTGP32 generator (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "mtgp_b200.h"
+
+namespace mtgpb {
+
+// Device copy of one parameter set. Tables are stored so a warp can hold them in registers
+// (lane l keeps tbl[l & 15], tmp[l & 15]) and look them up with one shfl.
+struct alignas(16) DevParams {
+    uint32_t pos, sh1, sh2, mask;
+    uint32_t tbl[16];
+    uint32_t tmp[16];
+};
+
+struct DevCksum {
+    unsigned long long sum64;
+    unsigned long long words;
+    unsigned int xor32;
+    unsigned int pad;
+};
+
+// One jump-ahead piece of the v2 kernel: `len` words of stream `set` starting `offset` words
+// after the set's position at the start of the call. jump_idx < 0: offset == 0, no jump.
+struct Piece {
+    uint32_t set;
+    int32_t jump_idx;
+    uint64_t offset;
+    uint64_t len;
+};
+
+// A team (one or more warps sharing a ring) processes pieces [first, first+count).
+struct TeamWork {
+    uint32_t first;
+    uint32_t count;
+};
+
+inline uint32_t state_words(uint32_t mexp) { return mexp / 32 + 1; }
+
+inline uint32_t next_pow2(uint32_t v) {
+    uint32_t r = 1;
+    while (r < v) r <<= 1;
+    return r;
+}
+
+// ---- kernel launchers (mtgp_kernels.cu) ----
+cudaError_t launch_v1(int kind, bool cksum, const DevParams* params, uint32_t* win, uint32_t n_sets,
+                      uint32_t N, void* out, uint64_t L, DevCksum* ck, cudaStream_t st);
+
+}  // namespace mtgpb

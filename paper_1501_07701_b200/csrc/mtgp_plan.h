@@ -1,0 +1,50 @@
+// mtgp_plan.h -- v2 launch planner: splits a call's work into jump-ahead pieces, owns the
+// per-set characteristic polynomials and jump polynomials, and launches the v2 kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "mtgp_b200.h"
+#include "mtgp_internal.cuh"
+
+namespace mtgpb {
+
+struct PlanRun {
+    int kind = 0;
+    bool cksum = true;
+    const DevParams* params = nullptr;
+    uint32_t* win = nullptr;
+    DevCksum* ck = nullptr;
+    void* out = nullptr;
+    uint64_t L = 0;
+    cudaStream_t stream = nullptr;
+    uint32_t max_pieces = 0;
+    uint64_t min_piece_words = 1ull << 21;
+    bool timing = false;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // results
+    double gen_ms = 0, jump_ms = 0;
+    uint64_t gen_launches = 0, jump_launches = 0;
+    uint32_t pieces = 0, warps_per_piece = 0;
+};
+
+struct PlannerImpl;
+
+class Planner {
+public:
+    Planner(const std::vector<mtgp_params>& sets, int num_sms);
+    ~Planner();
+    bool v2_supported() const;
+    cudaError_t run(PlanRun& r, std::string& err);
+    cudaError_t skip(const DevParams* params, uint32_t* win, uint64_t words, cudaStream_t st,
+                     std::string& err);
+
+private:
+    std::unique_ptr<PlannerImpl> impl_;
+};
+
+}  // namespace mtgpb

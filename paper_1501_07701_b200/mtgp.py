@@ -1,0 +1,229 @@
+"""ctypes binding of the C-ABI in include/mtgp_b200.h (libmtgp_b200.so).
+
+This is plumbing for tests and bench.py: every call goes straight into the CUDA library. There
+is no CPU fallback -- if the library or a device is missing, construction raises.
+
+Mirrors the reference's generation API shape (proj/include/twistsieve/word_source.hpp:21-25,
+75-76; generator.hpp:23-52): a context is "n_sets WordSources at once"; ``fill_u32(L)`` is L
+successive ``WordSource::fill`` words of every stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+from typing import Optional, Sequence
+
+import numpy as np
+
+from .tables import MtgpParams, state_words
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libmtgp_b200.so"
+
+MTGP_OK, MTGP_EINVAL, MTGP_ECUDA, MTGP_ENOMEM, MTGP_ESTATE = 0, 1, 2, 3, 4
+U32, F32_12, F32_01OC = 0, 1, 2
+OPT_CHECKSUM, OPT_KERNEL, OPT_MAX_PIECES, OPT_MIN_PIECE_WORDS, OPT_TIMING, OPT_HOST_CHUNK = 1, 2, 3, 4, 5, 6
+
+# Every symbol include/mtgp_b200.h declares (checked by the CPU test suite).
+EXPORTS = (
+    "mtgp_abi_version", "mtgp_last_error", "mtgp_validate_params", "mtgp_ctx_create",
+    "mtgp_ctx_destroy", "mtgp_ctx_info", "mtgp_position", "mtgp_ctx_stream", "mtgp_set_option",
+    "mtgp_generate", "mtgp_generate_u32", "mtgp_generate_f32_12", "mtgp_generate_f32_01oc",
+    "mtgp_skip", "mtgp_state_save", "mtgp_state_restore", "mtgp_checksums",
+    "mtgp_checksums_reset", "mtgp_sync", "mtgp_kernel_timing", "mtgp_kernel_timing_reset",
+    "mtgp_last_plan",
+)
+
+
+class MtgpParamsC(C.Structure):
+    _fields_ = [("mexp", C.c_uint32), ("pos", C.c_uint32), ("sh1", C.c_uint32), ("sh2", C.c_uint32),
+                ("tbl", C.c_uint32 * 16), ("tmp_tbl", C.c_uint32 * 16),
+                ("flt_tmp_tbl", C.c_uint32 * 16), ("mask", C.c_uint32)]
+
+
+class MtgpCksumC(C.Structure):
+    _fields_ = [("sum64", C.c_uint64), ("words", C.c_uint64), ("xor32", C.c_uint32), ("pad", C.c_uint32)]
+
+
+class MtgpError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class MtgpInvalidArgument(MtgpError, ValueError):
+    """What the reference raises as std::invalid_argument (proj/src/params.cpp:23-39)."""
+
+
+_lib = None
+
+
+def load_library(path: Optional[str] = None) -> C.CDLL:
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise ImportError(f"{p} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(str(p))
+    lib.mtgp_last_error.restype = C.c_char_p
+    lib.mtgp_ctx_create.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.POINTER(MtgpParamsC), C.c_uint32,
+                                    C.POINTER(C.c_uint32), C.c_void_p]
+    lib.mtgp_ctx_destroy.argtypes = [C.c_void_p]
+    lib.mtgp_ctx_info.argtypes = [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
+    lib.mtgp_position.argtypes = [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint64)]
+    lib.mtgp_ctx_stream.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+    lib.mtgp_set_option.argtypes = [C.c_void_p, C.c_int, C.c_int64]
+    lib.mtgp_generate.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_int]
+    lib.mtgp_skip.argtypes = [C.c_void_p, C.c_uint64]
+    lib.mtgp_state_save.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.mtgp_state_restore.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.mtgp_checksums.argtypes = [C.c_void_p, C.POINTER(MtgpCksumC)]
+    lib.mtgp_checksums_reset.argtypes = [C.c_void_p]
+    lib.mtgp_sync.argtypes = [C.c_void_p]
+    lib.mtgp_kernel_timing.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64),
+                                       C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+    lib.mtgp_kernel_timing_reset.argtypes = [C.c_void_p]
+    lib.mtgp_last_plan.argtypes = [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
+    lib.mtgp_validate_params.argtypes = [C.POINTER(MtgpParamsC)]
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def _check(lib, rc: int) -> None:
+    if rc != MTGP_OK:
+        msg = lib.mtgp_last_error().decode()
+        if rc == MTGP_EINVAL:
+            raise MtgpInvalidArgument(rc, msg)
+        raise MtgpError(rc, msg)
+
+
+def to_c_params(sets: Sequence[MtgpParams]):
+    arr = (MtgpParamsC * len(sets))()
+    for i, p in enumerate(sets):
+        a = arr[i]
+        a.mexp, a.pos, a.sh1, a.sh2, a.mask = p.mexp, p.pos, p.sh1, p.sh2, p.mask
+        for j in range(16):
+            a.tbl[j] = p.tbl[j]
+            a.tmp_tbl[j] = p.tmp_tbl[j]
+            a.flt_tmp_tbl[j] = p.flt_tmp_tbl[j]
+    return arr
+
+
+def validate(p: MtgpParams) -> None:
+    lib = load_library()
+    arr = to_c_params([p])
+    _check(lib, lib.mtgp_validate_params(arr))
+
+
+class MtgpContext:
+    """n_sets independent MTGP32 streams on one GPU (C-ABI mtgp_ctx)."""
+
+    def __init__(self, sets: Sequence[MtgpParams], seeds: Sequence[int], device: int = 0,
+                 stream: Optional[int] = None):
+        self.lib = load_library()
+        if len(seeds) != len(sets):
+            raise ValueError("one seed per parameter set")
+        self.sets = list(sets)
+        self.n_sets = len(sets)
+        self.N = state_words(sets[0].mexp)
+        self._params = to_c_params(sets)
+        self._seeds = (C.c_uint32 * len(seeds))(*[int(s) & 0xFFFFFFFF for s in seeds])
+        h = C.c_void_p()
+        _check(self.lib, self.lib.mtgp_ctx_create(C.byref(h), device, self._params, self.n_sets,
+                                                  self._seeds, C.c_void_p(stream or 0)))
+        self.h = h
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.mtgp_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- options / info
+    def set_option(self, opt: int, value: int) -> None:
+        _check(self.lib, self.lib.mtgp_set_option(self.h, opt, int(value)))
+
+    def stream_handle(self) -> int:
+        s = C.c_void_p()
+        _check(self.lib, self.lib.mtgp_ctx_stream(self.h, C.byref(s)))
+        return s.value or 0
+
+    def position(self, s: int = 0) -> int:
+        v = C.c_uint64()
+        _check(self.lib, self.lib.mtgp_position(self.h, s, C.byref(v)))
+        return v.value
+
+    def last_plan(self):
+        a, b, c = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        _check(self.lib, self.lib.mtgp_last_plan(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    # -- generation
+    def generate_device(self, kind: int, ptr: int, words_per_stream: int) -> None:
+        """Asynchronous generation into device memory at `ptr` (int address)."""
+        _check(self.lib, self.lib.mtgp_generate(self.h, kind, C.c_void_p(ptr), words_per_stream, 1))
+
+    def generate_host(self, kind: int, words_per_stream: int, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """Synchronous generation into host memory; returns an (n_sets, L) uint32 array."""
+        if out is None:
+            out = np.empty((self.n_sets, words_per_stream), dtype=np.uint32)
+        assert out.dtype == np.uint32 and out.flags.c_contiguous and out.size == self.n_sets * words_per_stream
+        _check(self.lib, self.lib.mtgp_generate(self.h, kind, out.ctypes.data_as(C.c_void_p),
+                                                words_per_stream, 0))
+        return out
+
+    def fill_u32(self, L: int) -> np.ndarray:
+        return self.generate_host(U32, L)
+
+    def skip(self, words: int) -> None:
+        _check(self.lib, self.lib.mtgp_skip(self.h, words))
+
+    def sync(self) -> None:
+        _check(self.lib, self.lib.mtgp_sync(self.h))
+
+    # -- state
+    def state_save(self):
+        win = np.empty((self.n_sets, self.N), dtype=np.uint32)
+        pos = np.empty(self.n_sets, dtype=np.uint64)
+        _check(self.lib, self.lib.mtgp_state_save(self.h, win.ctypes.data_as(C.c_void_p),
+                                                  pos.ctypes.data_as(C.c_void_p)))
+        return win, pos
+
+    def state_restore(self, win: np.ndarray, pos: Optional[np.ndarray] = None) -> None:
+        win = np.ascontiguousarray(win, dtype=np.uint32)
+        assert win.size == self.n_sets * self.N
+        pp = None
+        if pos is not None:
+            pos = np.ascontiguousarray(pos, dtype=np.uint64)
+            pp = pos.ctypes.data_as(C.c_void_p)
+        _check(self.lib, self.lib.mtgp_state_restore(self.h, win.ctypes.data_as(C.c_void_p), pp))
+
+    def checksums(self):
+        arr = (MtgpCksumC * self.n_sets)()
+        _check(self.lib, self.lib.mtgp_checksums(self.h, arr))
+        return [(a.sum64, a.xor32, a.words) for a in arr]
+
+    def checksums_reset(self) -> None:
+        _check(self.lib, self.lib.mtgp_checksums_reset(self.h))
+
+    def kernel_timing(self):
+        g, gl, j, jl = C.c_double(), C.c_uint64(), C.c_double(), C.c_uint64()
+        _check(self.lib, self.lib.mtgp_kernel_timing(self.h, C.byref(g), C.byref(gl), C.byref(j), C.byref(jl)))
+        return g.value, gl.value, j.value, jl.value
+
+    def kernel_timing_reset(self) -> None:
+        _check(self.lib, self.lib.mtgp_kernel_timing_reset(self.h))

@@ -1,0 +1,144 @@
+"""CPU: pin the oracle before trusting it.
+
+MTGP32: oracle/mtgp32_oracle.c vs the cuRAND host-compiled known answers
+(tests/golden/mtgp32_11213_curand.json).
+Engine::mt: oracle/mt_oracle.c vs the reference's own goldens (proj/tests/test_generator.cpp:
+11-25, 46-48, 52-57, 67, 90-103) and vs the reference compiled from its sources (oracle/_ref).
+"""
+import numpy as np
+import pytest
+
+import oracle_py
+from paper_1501_07701_b200 import tables
+
+
+def test_curand_table_import(curand_sets):
+    assert len(curand_sets) == 200
+    assert all(p.mexp == 11213 and p.mask == 0xFFF80000 for p in curand_sets)
+    assert min(p.pos for p in curand_sets) == 3 and max(p.pos for p in curand_sets) == 93
+    for p in curand_sets:
+        p.validate()  # linear tables, flt identity
+
+
+def test_init_state_golden(curand_sets, curand_golden):
+    g = oracle_py.MtgpOracle(curand_sets[0], 1)
+    w = g.window()
+    want = curand_golden["init_set0_seed1"]
+    assert [w[0], w[1], w[2], w[3], w[350]] == [want["x0"], want["x1"], want["x2"], want["x3"], want["x350"]]
+
+
+def test_first32_all_cases(curand_sets, curand_golden):
+    for case in curand_golden["first32"]:
+        g = oracle_py.MtgpOracle(curand_sets[case["set"]], case["seed"])
+        assert g.fill(32).tolist() == case["u32"], (case["set"], case["seed"])
+
+
+def test_appendix_b_first8(curand_sets):
+    g = oracle_py.MtgpOracle(curand_sets[0], 1)
+    assert g.fill(8).tolist() == [360948779, 1200908298, 2313932395, 2218157478, 3754595429,
+                                  1713953624, 1821568161, 2144555324]
+
+
+def test_single_float_matches_curand_temper_single(curand_sets, curand_golden):
+    for case in curand_golden["single12"]:
+        g = oracle_py.MtgpOracle(curand_sets[case["set"]], case["seed"])
+        assert g.fill(32, kind=1).tolist() == case["bits"]
+
+
+def test_float_01oc_goldens(curand_sets):
+    g = oracle_py.MtgpOracle(curand_sets[0], 1)
+    assert [hex(v) for v in g.fill(4, kind=2)] == ["0x3f6a7c5c", "0x3f386b98", "0x3eec2864", "0x3ef79338"]
+    g = oracle_py.MtgpOracle(curand_sets[0], 1)
+    f = g.fill(1 << 14, kind=2).view(np.float32)
+    assert f.min() > 0.0 and f.max() <= 1.0
+
+
+def test_checksums(curand_sets, curand_golden):
+    for case in curand_golden["checksums"]:
+        g = oracle_py.MtgpOracle(curand_sets[case["set"]], case["seed"])
+        if case["skip"]:
+            g.skip(case["skip"])
+        c = oracle_py.cksum(g.fill(case["n"]))
+        assert (c["sum64"], c["xor32"], c["last"], c["poly31"]) == (
+            case["sum64"], case["xor32"], case["last"], case["poly31"]), case
+
+
+def test_all200_weighted(curand_sets, curand_golden):
+    out, _ = oracle_py.mtgp_bulk(curand_sets, [1] * 200, 1 << 16, threads=8)
+    sums = out.astype(np.uint64).sum(axis=1)
+    assert sums.tolist() == curand_golden["all200_seed1_n65536_sum64"]
+    w = 0
+    for s, v in enumerate(sums.tolist()):
+        w = (w + (s + 1) * v) % (1 << 64)
+    assert w == curand_golden["all200_seed1_n65536_weighted"] == 2829222411326737783
+
+
+def test_window_roundtrip(curand_sets):
+    g = oracle_py.MtgpOracle(curand_sets[3], 99)
+    g.skip(12345)
+    h = oracle_py.MtgpOracle.from_window(curand_sets[3], g.window())
+    assert np.array_equal(g.fill(5000), h.fill(5000))
+
+
+def test_synthetic_sets_run(curand_sets):
+    for mexp in (23209, 44497):
+        for p in tables.synthetic_sets(mexp, 3):
+            g = oracle_py.MtgpOracle(p, 1)
+            w = g.fill(4096)
+            assert len(set(w.tolist())) > 4000  # not degenerate
+
+
+# ---------------- Engine::mt (the reference's own recurrence) ----------------
+
+def test_mt19937_reference_goldens(mt_golden):
+    # proj/tests/test_generator.cpp:11-15
+    g = oracle_py.MtOracle(None, 5489)
+    assert g.fill(3).tolist() == [3499211612, 581869302, 3890346734]
+    g = oracle_py.MtOracle(None, 5489)
+    c = oracle_py.cksum(g.fill(1 << 20))
+    want = mt_golden["mt19937_seed5489_n1048576"]
+    assert (c["sum64"], c["xor32"], c["last"]) == (want["sum64"], want["xor32"], want["last"]) == (
+        2252191846071920, 0x612DA44E, 1092562784)
+
+
+def test_mt19937_temper_golden():
+    p = oracle_py.mt19937_params()
+    L = oracle_py.lib()
+    assert L.oracle_mt_temper(0, p) == 0
+    assert L.oracle_mt_temper(0xFFFFFFFF, p) == 0x6FE01BF8  # test_generator.cpp:67
+    rng = np.random.default_rng(7)
+    for w in rng.integers(0, 1 << 32, 2000, dtype=np.uint64).tolist():
+        assert L.oracle_mt_untemper(L.oracle_mt_temper(w, p), p) == w
+
+
+def test_mt_seed_state_recurrence():
+    g = oracle_py.MtOracle(None, 5489)
+    assert g.g.st[0] == 5489
+    assert g.g.st[1] == (1812433253 * (5489 ^ (5489 >> 30)) + 1) & 0xFFFFFFFF
+
+
+def test_mt_oracle_vs_compiled_reference(mt_golden):
+    pytest.importorskip("ctypes")
+    try:
+        oracle_py.ref_lib()
+    except ImportError:
+        pytest.skip("oracle/_ref not built")
+    for seed in (0, 1, 5489, 12345, 0xFFFFFFFF):
+        a = oracle_py.MtOracle(None, seed).fill(5000)
+        b = oracle_py.ref_fill(5000, seed)
+        assert np.array_equal(a, b)
+    for name in ("dc521_id7", "dc3217_id7"):
+        d = mt_golden[name]
+        st = d["status12"]
+        p = oracle_py.OracleMtParams(st[1], st[2], st[3], st[4], st[5], st[6], st[7], st[8], st[9], st[10], st[11])
+        w = oracle_py.MtOracle(p, d["seed"]).fill(d["n"])
+        c = oracle_py.cksum(w)
+        assert (c["sum64"], c["xor32"], c["last"]) == (d["sum64"], d["xor32"], d["last"])
+        assert np.array_equal(w, oracle_py.ref_fill(d["n"], d["seed"], st))
+
+
+def test_derive_seed_matches_reference_formula():
+    L = oracle_py.lib()
+    # splitmix64(0) is the published first output of the splitmix64 sequence
+    assert L.oracle_splitmix64(0) == 0xE220A8397B1DCDAF
+    assert L.oracle_derive_seed(10, 3) == L.oracle_splitmix64(13) & 0xFFFFFFFF
