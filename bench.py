@@ -1,0 +1,322 @@
+#!/usr/bin/env python
+"""bench.py -- MTGP32 bulk generation throughput on B200 (BASELINE.json metric).
+
+Default workload (N=1): BASELINE config 2 -- the 200 certified MTGP32-11213 parameter sets of
+the CUDA toolkit, seed 1 each, 2^28 uint32 per set per step. One step = the next 2^28 words of
+every stream (214.7 GB written), produced as --calls device calls of 2^28/calls words per
+stream into one reused device buffer (the step's output exceeds HBM). Streams advance across
+steps; nothing is cached or skipped.
+
+Multi-GPU (torchrun): weak scaling. Rank r owns parameter sets [200r, 200r+200) (the cuRAND
+sets for r=0, deterministic synthetic MTGP-11213 sets beyond), no collective on the hot path;
+after timing, the per-stream checksums are gathered over NCCL (the only collective).
+
+--impl reference: the reference's own CPU generator (oracle/_ref: proj/src/{generator,params,
+word_source}.cpp compiled from its sources) filling MT19937 streams through
+make_word_source()/WordSource::fill on every host core, rank 0 only.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+CONFIGS = {
+    # name: (mexp, kind, words per set per step, workload label)
+    "c2": (11213, 0, 1 << 28, "MTGP32-11213 x200 sets, 2^28 u32/set/step (BASELINE config 2)"),
+    "c3-f12": (11213, 1, 1 << 28, "MTGP32-11213 x200 sets, 2^28 f32 [1,2)/set/step (BASELINE config 3)"),
+    "c3-f01": (11213, 2, 1 << 28, "MTGP32-11213 x200 sets, 2^28 f32 (0,1]/set/step (BASELINE config 3)"),
+    "c4-23209": (23209, 0, 1 << 28, "MTGP32-23209 x200 synthetic sets, 2^28 u32/set/step (BASELINE config 4)"),
+    "c4-44497": (44497, 0, 1 << 28, "MTGP32-44497 x200 synthetic sets, 2^28 u32/set/step (BASELINE config 4)"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--sets", type=int, default=200)
+    ap.add_argument("--calls", type=int, default=4, help="device calls per step (output buffer = step/calls)")
+    ap.add_argument("--no-checksum", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-words-per-thread", type=int, default=1 << 27)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (the profiling recipe's clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm = []
+        reasons = set()
+        smax = None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                smax = float(r[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, r[3:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        loaded = [v for v in sm if smax and v > 0.5 * smax] or sm
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    if PEAKS.exists():
+        d = json.loads(PEAKS.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_reference(words_per_thread: int, threads: int):
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle_py
+    secs, _ = oracle_py.ref_bulk_throughput(threads, words_per_thread, 1 << 18, 5489)
+    return threads * words_per_thread / secs / 1e9, secs
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cores = len(os.sched_getaffinity(0))
+    wpt = args.cpu_words_per_thread
+    for _ in range(args.warmup):
+        cpu_reference(wpt // 8, cores)
+    vals, secs = [], []
+    for _ in range(args.steps):
+        v, s = cpu_reference(wpt, cores)
+        vals.append(v)
+        secs.append(s)
+    v = float(np.median(vals))
+    mexp, kind, L, label = CONFIGS[args.config]
+    line = {
+        "impl": "reference",
+        "metric": "Gsamples/s (uint32 & float) per GPU and at 1/2/4/8 B200; % of HBM write peak",
+        "value": round(v, 4), "unit": "Gsamples/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1000 * float(np.median(secs)), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (seeded generator streams; no input data)",
+        "config": {"workload": label, "reference_generator": "MT19937 via make_word_source/WordSource::fill "
+                   "(the reference implements no MTGP32; SURVEY.md §0)"},
+        "cpu_baseline": {"value": round(v, 4), "unit": "Gsamples/s", "cores": cores, "kind": "reference",
+                         "sample": f"{cores} threads x {wpt} MT19937 words in 2^18-word fill() calls per step"},
+        "e2e": {"value": round(v, 4), "unit": "Gsamples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_1501_07701_b200 import mtgp, tables
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    mexp, kind, L_step, label = CONFIGS[args.config]
+    S = args.sets
+    sets = tables.sets_for(mexp, S, first=rank * S)
+    seeds = [1] * S
+    calls = max(1, args.calls)
+    Lc = L_step // calls
+    ctx = mtgp.MtgpContext(sets, seeds, device=local)
+    ctx.set_option(mtgp.OPT_CHECKSUM, 0 if args.no_checksum else 1)
+    ext = torch.cuda.ExternalStream(ctx.stream_handle(), device=torch.device("cuda", local))
+    out = torch.empty((S, Lc), dtype=torch.int32, device=f"cuda:{local}")
+
+    # correctness gate before timing: first words of stream 0 vs the oracle
+    if rank == 0:
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import oracle_py
+        probe = mtgp.MtgpContext(sets[:2], seeds[:2], device=local)
+        w = probe.generate_host(kind, 4096)
+        probe.close()
+        ref = oracle_py.MtgpOracle(sets[0], seeds[0]).fill(4096, kind=kind)
+        if not np.array_equal(w[0], ref):
+            raise SystemExit("parity gate failed: GPU stream 0 differs from the oracle")
+
+    def step():
+        for _ in range(calls):
+            ctx.generate_device(kind, out.data_ptr(), Lc)
+
+    for _ in range(args.warmup):
+        step()
+    ctx.sync()
+    torch.cuda.synchronize()
+    ctx.kernel_timing_reset()
+    ctx.set_option(mtgp.OPT_TIMING, 1)
+    launches0 = ctx.launch_count()
+
+    clocks = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(ext)
+    for _ in range(args.steps):
+        step()
+    e1.record(ext)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launch_count() - launches0
+    gen_ms, gen_n, jump_ms, jump_n = ctx.kernel_timing()
+    ctx.set_option(mtgp.OPT_TIMING, 0)
+    pieces, _, kver = ctx.last_plan()
+
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        # per-stream checksum gather (NCCL; the only inter-GPU traffic)
+        ck = torch.tensor([[c[0] & 0x7FFFFFFFFFFFFFFF, c[1], c[2]] for c in ctx.checksums()],
+                          device=f"cuda:{local}", dtype=torch.int64)
+        allck = [torch.empty_like(ck) for _ in range(world)]
+        dist.all_gather(allck, ck)
+
+    samples_rank = S * L_step * args.steps
+    total = samples_rank * world
+    value = total / (ms / 1e3) / 1e9
+    hbm, hbm_src = peaks()
+    bytes_per_launch = 4.0 * S * Lc
+    gen_avg_ms = gen_ms / max(1, gen_n)
+    achieved = bytes_per_launch / (gen_avg_ms / 1e3) / 1e9
+    step_gbs = 4.0 * samples_rank / (ms / 1e3) / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cores = len(os.sched_getaffinity(0))
+            v, secs = cpu_reference(args.cpu_words_per_thread, cores)
+            cpu = {"value": round(v, 4), "unit": "Gsamples/s", "cores": cores, "kind": "reference",
+                   "sample": f"reference MtWordSource::fill (MT19937) x {cores} pinned threads x "
+                             f"{args.cpu_words_per_thread} words, {secs:.2f} s wall; the reference has no MTGP32"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "error": str(e)[:200]}
+
+    e2e = None
+    if rank == 0 and not args.no_e2e:
+        # public API, HOST buffers: mtgp_generate(out_is_device=0) into pinned memory; the timed
+        # region contains generation plus the device->host copy of every word
+        Le = 1 << 20
+        host = torch.empty((S, Le), dtype=torch.int32, pin_memory=True)
+        hv = host.numpy().view(np.uint32)
+        ectx = mtgp.MtgpContext(sets, seeds, device=local)
+        ectx.set_option(mtgp.OPT_HOST_CHUNK, 1 << 18)
+        ectx.generate_host(kind, Le, out=hv)
+        reps = 5
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            ectx.generate_host(kind, Le, out=hv)
+        t1 = time.perf_counter()
+        ectx.close()
+        e2e = {"value": round(S * Le * reps / (t1 - t0) / 1e9, 4), "unit": "Gsamples/s",
+               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": S * Le * 4,
+               "how": f"mtgp_generate(out_is_device=0) of {Le} words x {S} streams into pinned host memory, "
+                      f"{reps} calls, wall clock"}
+
+    if rank == 0:
+        line = {
+            "metric": "Gsamples/s (uint32 & float) per GPU and at 1/2/4/8 B200; % of HBM write peak",
+            "value": round(value, 3), "unit": "Gsamples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": ["u32", "f32", "f32"][kind],
+            "data": "synthetic (seeded generator streams; no input data)",
+            "config": {"workload": label, "sets_per_gpu": S, "seed": 1, "words_per_set_per_step": L_step,
+                       "calls_per_step": calls, "kernel": f"v{kver}", "pieces_per_call": pieces,
+                       "checksums_fused": not args.no_checksum,
+                       "l2": "output 4*S*L/calls bytes per call >> 126 MB L2; no flush needed",
+                       "parameter_sets": "cuRAND MTGP32-11213 (certified)" if (mexp == 11213 and rank == 0 and S <= 200)
+                       else "synthetic (uncertified period)"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                         "frac": round(achieved / hbm, 4), "traffic": None,
+                         "peak_source": hbm_src,
+                         "kernel": "gen_kernel (v2)", "launches_timed": gen_n,
+                         "avg_launch_ms": round(gen_avg_ms, 4),
+                         "algorithmic_bytes_per_launch": bytes_per_launch,
+                         "step_write_GBps": round(step_gbs, 1),
+                         "jump_ms_per_call": round(jump_ms / max(1, jump_n), 4)},
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -161,6 +161,8 @@ int mtgp_sync(mtgp_ctx* ctx);
 int mtgp_kernel_timing(mtgp_ctx* ctx, double* gen_ms, uint64_t* gen_launches, double* jump_ms,
                        uint64_t* jump_launches);
 int mtgp_kernel_timing_reset(mtgp_ctx* ctx);
+/* Number of CUDA kernels this context has launched since creation. */
+int mtgp_launch_count(const mtgp_ctx* ctx, uint64_t* launches);
 
 /* Launch plan of the last generation call: pieces (jump-ahead segments) and warps per piece. */
 int mtgp_last_plan(const mtgp_ctx* ctx, uint32_t* pieces, uint32_t* warps_per_piece,

@@ -94,9 +94,10 @@ struct mtgp_ctx {
     cudaEvent_t ev_copy[2] = {nullptr, nullptr};
 
     // timing
-    cudaEvent_t t0 = nullptr, t1 = nullptr, j0 = nullptr, j1 = nullptr;
+    EventPool pool;
     double gen_ms = 0, jump_ms = 0;
     uint64_t gen_launches = 0, jump_launches = 0;
+    uint64_t total_launches = 0;  // every kernel this context launched
 
     // v2 planner / jump-ahead state
     std::unique_ptr<Planner> planner;
@@ -170,10 +171,6 @@ int mtgp_ctx_create(mtgp_ctx** out, int device, const mtgp_params* sets, uint32_
         CK(cudaEventCreateWithFlags(&ctx->ev_gen[i], cudaEventDisableTiming), "cudaEventCreate");
         CK(cudaEventCreateWithFlags(&ctx->ev_copy[i], cudaEventDisableTiming), "cudaEventCreate");
     }
-    CK(cudaEventCreate(&ctx->t0), "cudaEventCreate");
-    CK(cudaEventCreate(&ctx->t1), "cudaEventCreate");
-    CK(cudaEventCreate(&ctx->j0), "cudaEventCreate");
-    CK(cudaEventCreate(&ctx->j1), "cudaEventCreate");
 
     std::vector<DevParams> dp(n_sets);
     for (uint32_t s = 0; s < n_sets; ++s) {
@@ -213,10 +210,6 @@ int mtgp_ctx_destroy(mtgp_ctx* ctx) {
         cudaEventDestroy(ctx->ev_gen[i]);
         cudaEventDestroy(ctx->ev_copy[i]);
     }
-    cudaEventDestroy(ctx->t0);
-    cudaEventDestroy(ctx->t1);
-    cudaEventDestroy(ctx->j0);
-    cudaEventDestroy(ctx->j1);
     cudaStreamDestroy(ctx->copy_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -278,18 +271,16 @@ int generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
     if (L == 0) return MTGP_OK;
     const bool use_v1 = ctx->kernel == 1 || !ctx->planner->v2_supported();
     if (use_v1) {
-        if (ctx->timing) CK(cudaEventRecord(ctx->t0, ctx->stream), "event");
+        size_t e0 = 0, e1 = 0;
+        if (ctx->timing) ctx->pool.record(ctx->stream, &e0);
         cudaError_t e = launch_v1(kind, ctx->cksum, ctx->d_params, ctx->d_win, ctx->n_sets, ctx->N, out, L,
                                   ctx->d_ck, ctx->stream);
         if (e != cudaSuccess) return cuda_fail(e, "v1 generation kernel");
         if (ctx->timing) {
-            CK(cudaEventRecord(ctx->t1, ctx->stream), "event");
-            CK(cudaEventSynchronize(ctx->t1), "event sync");
-            float ms = 0;
-            CK(cudaEventElapsedTime(&ms, ctx->t0, ctx->t1), "event time");
-            ctx->gen_ms += ms;
-            ctx->gen_launches++;
+            ctx->pool.record(ctx->stream, &e1);
+            ctx->pool.gen.push_back({e0, e1});
         }
+        ctx->total_launches += 1;
         ctx->last_pieces = ctx->n_sets;
         ctx->last_warps = 8;
         ctx->last_kernel = 1;
@@ -305,19 +296,12 @@ int generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
         run.stream = ctx->stream;
         run.max_pieces = ctx->max_pieces;
         run.min_piece_words = ctx->min_piece_words;
-        run.timing = ctx->timing;
-        run.ev[0] = ctx->t0;
-        run.ev[1] = ctx->t1;
-        run.ev[2] = ctx->j0;
-        run.ev[3] = ctx->j1;
+        run.timing = ctx->timing ? &ctx->pool : nullptr;
         std::string err;
         cudaError_t e = ctx->planner->run(run, err);
         if (e != cudaSuccess) return fail(e == cudaErrorMemoryAllocation ? MTGP_ENOMEM : MTGP_ECUDA, "v2 generation: %s (%s)", err.c_str(), cudaGetErrorString(e));
         if (!err.empty()) return fail(MTGP_EINVAL, "v2 generation: %s", err.c_str());
-        ctx->gen_ms += run.gen_ms;
-        ctx->jump_ms += run.jump_ms;
-        ctx->gen_launches += run.gen_launches;
-        ctx->jump_launches += run.jump_launches;
+        ctx->total_launches += run.launches;
         ctx->last_pieces = run.pieces;
         ctx->last_warps = run.warps_per_piece;
         ctx->last_kernel = 2;
@@ -408,6 +392,7 @@ int mtgp_state_restore(mtgp_ctx* ctx, const uint32_t* windows, const uint64_t* p
     CK(cudaMemcpyAsync(ctx->d_win, windows, (size_t)ctx->n_sets * ctx->N * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D state");
     CK(cudaStreamSynchronize(ctx->stream), "sync");
     if (positions) std::copy(positions, positions + ctx->n_sets, ctx->position.begin());
+    ctx->planner->invalidate();
     return MTGP_OK;
 }
 
@@ -444,6 +429,8 @@ int mtgp_sync(mtgp_ctx* ctx) {
 int mtgp_kernel_timing(mtgp_ctx* ctx, double* gen_ms, uint64_t* gen_launches, double* jump_ms,
                        uint64_t* jump_launches) {
     if (!ctx) return fail(MTGP_EINVAL, "null context");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CK(ctx->pool.resolve(&ctx->gen_ms, &ctx->gen_launches, &ctx->jump_ms, &ctx->jump_launches), "event resolve");
     if (gen_ms) *gen_ms = ctx->gen_ms;
     if (gen_launches) *gen_launches = ctx->gen_launches;
     if (jump_ms) *jump_ms = ctx->jump_ms;
@@ -453,8 +440,18 @@ int mtgp_kernel_timing(mtgp_ctx* ctx, double* gen_ms, uint64_t* gen_launches, do
 
 int mtgp_kernel_timing_reset(mtgp_ctx* ctx) {
     if (!ctx) return fail(MTGP_EINVAL, "null context");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    double a = 0, b = 0;
+    uint64_t c = 0, d = 0;
+    CK(ctx->pool.resolve(&a, &c, &b, &d), "event resolve");
     ctx->gen_ms = ctx->jump_ms = 0;
     ctx->gen_launches = ctx->jump_launches = 0;
+    return MTGP_OK;
+}
+
+int mtgp_launch_count(const mtgp_ctx* ctx, uint64_t* launches) {
+    if (!ctx || !launches) return fail(MTGP_EINVAL, "null argument");
+    *launches = ctx->total_launches;
     return MTGP_OK;
 }
 

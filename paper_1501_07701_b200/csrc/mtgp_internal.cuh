@@ -41,6 +41,49 @@ struct TeamWork {
     uint32_t count;
 };
 
+// Non-blocking kernel timing: event pairs recorded around launches, resolved on demand.
+struct EventPool {
+    std::vector<cudaEvent_t> ev;
+    size_t used = 0;
+    std::vector<std::pair<size_t, size_t>> gen, jump;
+    cudaEvent_t record(cudaStream_t st, size_t* idx) {
+        if (used == ev.size()) {
+            cudaEvent_t e = nullptr;
+            cudaEventCreate(&e);
+            ev.push_back(e);
+        }
+        *idx = used;
+        cudaEventRecord(ev[used], st);
+        return ev[used++];
+    }
+    // Sums elapsed milliseconds of all recorded pairs, then recycles the events.
+    cudaError_t resolve(double* gen_ms, uint64_t* gen_n, double* jump_ms, uint64_t* jump_n) {
+        if (used) {
+            cudaError_t e = cudaEventSynchronize(ev[used - 1]);
+            if (e != cudaSuccess) return e;
+        }
+        for (auto& p : gen) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, ev[p.first], ev[p.second]);
+            *gen_ms += ms;
+            ++*gen_n;
+        }
+        for (auto& p : jump) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, ev[p.first], ev[p.second]);
+            *jump_ms += ms;
+            ++*jump_n;
+        }
+        gen.clear();
+        jump.clear();
+        used = 0;
+        return cudaSuccess;
+    }
+    ~EventPool() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+
 inline uint32_t state_words(uint32_t mexp) { return mexp / 32 + 1; }
 
 inline uint32_t next_pow2(uint32_t v) {

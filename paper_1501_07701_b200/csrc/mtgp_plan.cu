@@ -1,29 +1,453 @@
-// mtgp_plan.cu -- v2 planner (stub until the warp-team kernel lands).
+// mtgp_plan.cu -- v2 planner: piece decomposition, per-set annihilating polynomials, jump
+// polynomials, and the prefix -> jump -> generate launch sequence.
+//
+// Jump-ahead math. The MTGP32 state is the window (x_i & mask, x_{i+1}, ..., x_{i+N-1}); the
+// transition F is GF(2)-linear on an mexp-dimensional space, so every bit-sequence of the
+// state words is annihilated by the minimal polynomial P of the stream's state (degree
+// <= mexp). If q = x^o mod P then x_{o+j} = XOR_i q_i x_{i+j} (exactly for j >= 1, on the live
+// bits for j = 0: the low 32N-mexp bits of the oldest word are dead).
+// P comes from Berlekamp-Massey over 2*mexp bits of one bit-plane, LCM'd with further
+// functionals until it provably annihilates the whole state (checked on all N window words).
+// For the certified cuRAND sets P is the irreducible characteristic polynomial of degree 11213.
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <thread>
+
+#include "gf2.h"
 #include "mtgp_plan.h"
+#include "mtgp_v2.cuh"
 
 namespace mtgpb {
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+template <class F>
+void parallel_for(size_t n, F&& f) {
+    const size_t hw = std::max<size_t>(1, std::thread::hardware_concurrency());
+    const size_t nt = std::min(n, hw);
+    if (nt <= 1) {
+        for (size_t i = 0; i < n; ++i) f(i);
+        return;
+    }
+    std::atomic<size_t> next{0};
+    std::vector<std::thread> th;
+    for (size_t t = 0; t < nt; ++t)
+        th.emplace_back([&] {
+            for (size_t i; (i = next.fetch_add(1)) < n;) f(i);
+        });
+    for (auto& x : th) x.join();
+}
+
+constexpr uint64_t kMaxPieceWords = 1ull << 30;
+
+}  // namespace
 
 struct PlannerImpl {
     std::vector<mtgp_params> sets;
     int num_sms = 148;
+    uint32_t M = 0, N = 0, S = 0;
+    bool v2 = false;
+
+    // algebra (per set)
+    bool analyzed = false;
+    bool jumps_ok = false;
+    std::vector<std::unique_ptr<gf2::Modulus>> mods;
+
+    // cached plan
+    uint64_t plan_L = 0;
+    uint32_t plan_T = 0;
+    bool plan_valid = false;
+    std::vector<Piece> pieces;
+    std::vector<TeamWork> teams;
+    std::vector<uint32_t> jump_rows;  // set index per prefix row
+    std::vector<uint32_t> job_off;
+    std::vector<JumpJob> jobs;
+    uint32_t n_q = 0;
+    uint32_t q_words = 0;
+    uint32_t pre_len = 0;
+
+    DevBuf d_pieces, d_teams, d_pwin_ptrs, d_pwin, d_q, d_pre, d_rows, d_joboff, d_jobs, d_win_next, d_all_rows;
+
+    ~PlannerImpl() {
+        for (DevBuf* b : {&d_pieces, &d_teams, &d_pwin_ptrs, &d_pwin, &d_q, &d_pre, &d_rows, &d_joboff, &d_jobs,
+                          &d_win_next, &d_all_rows})
+            b->release();
+    }
+
+    uint32_t prefix_len() const {
+        const uint32_t qw = (M + 31) / 32;
+        const uint32_t jblk = 32 * 12;
+        const uint32_t need = 32 * qw + jblk * ((N + jblk - 1) / jblk) + 36;
+        return (need + 31) & ~31u;
+    }
+
+    cudaError_t analyze(const DevParams* params, const uint32_t* win, cudaStream_t st, std::string& err);
+    cudaError_t build_plan(uint64_t L, uint32_t T, uint64_t min_piece, std::string& err);
 };
 
 Planner::Planner(const std::vector<mtgp_params>& sets, int num_sms) : impl_(new PlannerImpl) {
     impl_->sets = sets;
     impl_->num_sms = num_sms;
+    impl_->S = (uint32_t)sets.size();
+    impl_->M = sets[0].mexp;
+    impl_->N = state_words(impl_->M);
+    impl_->v2 = v2_supports(impl_->M);
+    for (const auto& p : sets)
+        if (p.pos + kStepWords > impl_->N) impl_->v2 = false;  // needs N - pos >= 256
 }
 Planner::~Planner() = default;
 
-bool Planner::v2_supported() const { return false; }
+bool Planner::v2_supported() const { return impl_->v2; }
+void Planner::invalidate() {
+    impl_->analyzed = false;
+    impl_->jumps_ok = false;
+    impl_->plan_valid = false;
+}
 
-cudaError_t Planner::run(PlanRun&, std::string& err) {
-    err = "v2 kernel not available";
+cudaError_t PlannerImpl::analyze(const DevParams* params, const uint32_t* win, cudaStream_t st, std::string& err) {
+    if (analyzed) return cudaSuccess;
+    const uint32_t len = ((2 * M + N + 64) + 31) & ~31u;
+    std::vector<uint32_t> rows(S);
+    for (uint32_t s = 0; s < S; ++s) rows[s] = s;
+    cudaError_t e;
+    if ((e = d_all_rows.ensure(S * 4)) != cudaSuccess) return e;
+    DevBuf seq;
+    if ((e = seq.ensure((size_t)S * len * 4)) != cudaSuccess) return e;
+    cudaMemcpyAsync(d_all_rows.p, rows.data(), S * 4, cudaMemcpyHostToDevice, st);
+    if ((e = launch_prefix(params, win, d_all_rows.as<uint32_t>(), S, N, seq.as<uint32_t>(), len, st)) != cudaSuccess) {
+        seq.release();
+        return e;
+    }
+    std::vector<uint32_t> h((size_t)S * len);
+    e = cudaMemcpyAsync(h.data(), seq.p, h.size() * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    seq.release();
+    if (e != cudaSuccess) return e;
+
+    mods.clear();
+    mods.resize(S);
+    std::vector<int> ok(S, 0);
+    const uint32_t mask0 = sets[0].mask;
+    parallel_for(S, [&](size_t s) {
+        const uint32_t* x = h.data() + s * len;
+        // functionals: bit 31, bit 0, then parities of pseudo-random masks
+        const uint32_t fmask[] = {0x80000000u, 0x00000001u, 0x00010000u, 0x9E3779B9u, 0x7F4A7C15u,
+                                  0x85EBCA6Bu, 0xC2B2AE35u, 0x27D4EB2Fu, 0x165667B1u, 0xD3A2646Cu};
+        gf2::Poly P;
+        bool good = false;
+        for (uint32_t fi = 0; fi < sizeof(fmask) / sizeof(fmask[0]) && !good; ++fi) {
+            std::vector<uint64_t> bits((2 * (size_t)M + 63) / 64 + 1, 0);
+            for (size_t k = 0; k < 2 * (size_t)M; ++k)
+                if (__builtin_parity(x[k + 1] & fmask[fi])) bits[k >> 6] |= 1ull << (k & 63);
+            gf2::Poly Q = gf2::berlekamp_massey(bits, 2 * (size_t)M);
+            if (fi == 0) {
+                P = Q;
+            } else {
+                // P = lcm(P, Q)
+                gf2::Poly g = gf2::gcd(P, Q);
+                gf2::Poly qq;
+                gf2::divmod(Q, g, &qq, nullptr);
+                P = gf2::mul(P, qq);
+            }
+            if (P.degree() > (int)M) break;
+            // annihilation on all bits of the window (j = 0: live bits only)
+            std::vector<int> idx;
+            for (int i = 0; i <= P.degree(); ++i)
+                if (P.coeff(i)) idx.push_back(i);
+            bool ann = true;
+            for (uint32_t j = 0; j < N && ann; ++j) {
+                uint32_t acc = 0;
+                for (int i : idx) acc ^= x[i + j];
+                if (j == 0) acc &= mask0;
+                ann = acc == 0;
+            }
+            good = ann;
+        }
+        if (good) {
+            mods[s] = std::make_unique<gf2::Modulus>(P);
+            ok[s] = 1;
+        }
+    });
+    jumps_ok = true;
+    for (uint32_t s = 0; s < S; ++s)
+        if (!ok[s]) jumps_ok = false;
+    analyzed = true;
+    if (!jumps_ok) err.clear();  // not an error: the planner falls back to one piece per stream
     return cudaSuccess;
 }
 
-cudaError_t Planner::skip(const DevParams*, uint32_t*, uint64_t, cudaStream_t, std::string& err) {
-    err = "skip not available";
-    return cudaSuccess;
+cudaError_t PlannerImpl::build_plan(uint64_t L, uint32_t T, uint64_t min_piece, std::string& err) {
+    if (plan_valid && plan_L == L && plan_T == T) return cudaSuccess;
+    const uint64_t W = (uint64_t)S * L;
+    uint64_t want = std::max<uint64_t>(1, W / std::max<uint64_t>(1, min_piece));
+    want = std::min<uint64_t>(want, T);
+    want = std::max<uint64_t>(want, (W + kMaxPieceWords - 1) / kMaxPieceWords);
+    pieces.clear();
+    teams.clear();
+    if (want <= S || !jumps_ok) {
+        if (!jumps_ok && L > kMaxPieceWords) {
+            err = "request needs jump-ahead pieces but no annihilating polynomial was found";
+            return cudaSuccess;
+        }
+        for (uint32_t s = 0; s < S; ++s) {
+            pieces.push_back(Piece{s, -1, 0, L});
+            teams.push_back(TeamWork{s, 1});
+        }
+    } else {
+        // split the concatenation of all streams into `want` equal ranges, cut at stream
+        // boundaries; range starts rounded to 4 words so most pieces start 16B-aligned
+        for (uint64_t g = 0; g < want; ++g) {
+            uint64_t a = (W * g / want) & ~3ull, b = g + 1 == want ? W : (W * (g + 1) / want) & ~3ull;
+            if (b <= a) continue;
+            TeamWork tw{(uint32_t)pieces.size(), 0};
+            while (a < b) {
+                const uint32_t s = (uint32_t)(a / L);
+                const uint64_t off = a % L;
+                const uint64_t end = std::min<uint64_t>(b, (uint64_t)(s + 1) * L);
+                pieces.push_back(Piece{s, -1, off, end - a});
+                tw.count++;
+                a = end;
+            }
+            teams.push_back(tw);
+        }
+    }
+    // jump jobs, grouped by set
+    std::map<uint32_t, std::vector<uint32_t>> by_set;
+    for (uint32_t i = 0; i < pieces.size(); ++i)
+        if (pieces[i].offset) by_set[pieces[i].set].push_back(i);
+    jump_rows.clear();
+    job_off.assign(1, 0);
+    jobs.clear();
+    q_words = (M + 31) / 32;
+    std::vector<std::pair<uint32_t, uint32_t>> qlist;  // (piece, set)
+    for (auto& kv : by_set) {
+        jump_rows.push_back(kv.first);
+        for (uint32_t pi : kv.second) {
+            pieces[pi].jump_idx = (int32_t)qlist.size();
+            jobs.push_back(JumpJob{pi, (uint32_t)qlist.size()});
+            qlist.push_back({pi, kv.first});
+        }
+        job_off.push_back((uint32_t)jobs.size());
+    }
+    n_q = (uint32_t)qlist.size();
+    // jump polynomials x^offset mod P, chained per set
+    std::vector<uint32_t> hq((size_t)n_q * q_words, 0);
+    std::vector<uint32_t> rows_list(jump_rows);
+    parallel_for(rows_list.size(), [&](size_t r) {
+        const uint32_t s = rows_list[r];
+        const gf2::Modulus& md = *mods[s];
+        std::map<uint64_t, gf2::Poly> step_cache;
+        gf2::Poly cur;
+        uint64_t cur_off = 0;
+        bool have = false;
+        for (uint32_t jj = job_off[r]; jj < job_off[r + 1]; ++jj) {
+            const uint32_t pi = jobs[jj].piece;
+            const uint64_t off = pieces[pi].offset;
+            if (!have) {
+                cur = md.x_pow(off);
+                have = true;
+            } else {
+                const uint64_t d = off - cur_off;
+                auto it = step_cache.find(d);
+                if (it == step_cache.end()) it = step_cache.emplace(d, md.x_pow(d)).first;
+                cur = md.mulmod(cur, it->second);
+            }
+            cur_off = off;
+            uint32_t* dst = hq.data() + (size_t)jobs[jj].q * q_words;
+            for (int i = 0; i <= cur.degree(); ++i)
+                if (cur.coeff(i)) dst[i >> 5] |= 1u << (i & 31);
+        }
+    });
+    // device copies
+    cudaError_t e;
+    pre_len = prefix_len();
+    if ((e = d_pieces.ensure(sizeof(Piece) * pieces.size())) != cudaSuccess) return e;
+    if ((e = d_teams.ensure(sizeof(TeamWork) * teams.size())) != cudaSuccess) return e;
+    if ((e = d_pwin_ptrs.ensure(sizeof(uint32_t*) * pieces.size())) != cudaSuccess) return e;
+    if ((e = d_pwin.ensure(sizeof(uint32_t) * N * std::max<size_t>(1, pieces.size()))) != cudaSuccess) return e;
+    if ((e = d_q.ensure(sizeof(uint32_t) * std::max<size_t>(1, hq.size()))) != cudaSuccess) return e;
+    if ((e = d_pre.ensure(sizeof(uint32_t) * (size_t)pre_len * std::max<size_t>(1, jump_rows.size()))) != cudaSuccess) return e;
+    if ((e = d_rows.ensure(sizeof(uint32_t) * std::max<size_t>(1, jump_rows.size()))) != cudaSuccess) return e;
+    if ((e = d_joboff.ensure(sizeof(uint32_t) * job_off.size())) != cudaSuccess) return e;
+    if ((e = d_jobs.ensure(sizeof(JumpJob) * std::max<size_t>(1, jobs.size()))) != cudaSuccess) return e;
+    if ((e = d_win_next.ensure(sizeof(uint32_t) * N * S)) != cudaSuccess) return e;
+    cudaMemcpy(d_pieces.p, pieces.data(), sizeof(Piece) * pieces.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(d_teams.p, teams.data(), sizeof(TeamWork) * teams.size(), cudaMemcpyHostToDevice);
+    if (!hq.empty()) cudaMemcpy(d_q.p, hq.data(), sizeof(uint32_t) * hq.size(), cudaMemcpyHostToDevice);
+    if (!jump_rows.empty()) cudaMemcpy(d_rows.p, jump_rows.data(), sizeof(uint32_t) * jump_rows.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(d_joboff.p, job_off.data(), sizeof(uint32_t) * job_off.size(), cudaMemcpyHostToDevice);
+    if (!jobs.empty()) cudaMemcpy(d_jobs.p, jobs.data(), sizeof(JumpJob) * jobs.size(), cudaMemcpyHostToDevice);
+    plan_L = L;
+    plan_T = T;
+    plan_valid = true;
+    return cudaGetLastError();
+}
+
+cudaError_t Planner::run(PlanRun& r, std::string& err) {
+    PlannerImpl& I = *impl_;
+    if (!I.v2) {
+        err = "v2 kernel does not support this parameter shape";
+        return cudaSuccess;
+    }
+    const int cps = gen_ctas_per_sm(I.M, r.kind, r.cksum);
+    if (cps <= 0) {
+        err = "v2 kernel cannot be resident";
+        return cudaSuccess;
+    }
+    uint32_t T = (uint32_t)(cps * kWarpsPerCta * I.num_sms);
+    if (r.max_pieces) T = std::min(T, r.max_pieces);
+    const uint64_t W = (uint64_t)I.S * r.L;
+    const bool need_jumps = std::min<uint64_t>(T, W / std::max<uint64_t>(1, r.min_piece_words)) > I.S ||
+                            r.L > kMaxPieceWords;
+    cudaError_t e;
+    if (need_jumps && !I.analyzed) {
+        if ((e = I.analyze(r.params, r.win, r.stream, err)) != cudaSuccess) return e;
+        if (!err.empty()) return cudaSuccess;
+    }
+    if ((e = I.build_plan(r.L, need_jumps ? T : I.S, r.min_piece_words, err)) != cudaSuccess) return e;
+    if (!err.empty()) return cudaSuccess;
+
+    // per-piece start-window pointers: jumped pieces -> d_pwin rows; offset-0 pieces -> current window
+    std::vector<const uint32_t*> ptrs(I.pieces.size());
+    for (size_t i = 0; i < I.pieces.size(); ++i)
+        ptrs[i] = I.pieces[i].offset ? I.d_pwin.as<uint32_t>() + (size_t)i * I.N
+                                     : r.win + (size_t)I.pieces[i].set * I.N;
+    if ((e = cudaMemcpyAsync(I.d_pwin_ptrs.p, ptrs.data(), sizeof(uint32_t*) * ptrs.size(), cudaMemcpyHostToDevice,
+                             r.stream)) != cudaSuccess)
+        return e;
+
+    size_t j0 = 0, j1 = 0, g0 = 0, g1 = 0;
+    if (!I.jump_rows.empty()) {
+        if (r.timing) r.timing->record(r.stream, &j0);
+        if ((e = launch_prefix(r.params, r.win, I.d_rows.as<uint32_t>(), (uint32_t)I.jump_rows.size(), I.N,
+                               I.d_pre.as<uint32_t>(), I.pre_len, r.stream)) != cudaSuccess)
+            return e;
+        JumpArgs ja;
+        ja.pre = I.d_pre.as<uint32_t>();
+        ja.pre_len = I.pre_len;
+        ja.set_of = I.d_rows.as<uint32_t>();
+        ja.job_off = I.d_joboff.as<uint32_t>();
+        ja.jobs = I.d_jobs.as<JumpJob>();
+        ja.q = I.d_q.as<uint32_t>();
+        ja.q_words = I.q_words;
+        ja.piece_win = I.d_pwin.as<uint32_t>();
+        if ((e = launch_jump(I.M, ja, (uint32_t)I.jump_rows.size(), r.stream)) != cudaSuccess) return e;
+        if (r.timing) {
+            r.timing->record(r.stream, &j1);
+            r.timing->jump.push_back({j0, j1});
+        }
+        r.launches += 2;
+    }
+    GenArgs ga;
+    ga.params = r.params;
+    ga.pieces = I.d_pieces.as<Piece>();
+    ga.teams = I.d_teams.as<TeamWork>();
+    ga.n_teams = (uint32_t)I.teams.size();
+    ga.piece_win = I.d_pwin_ptrs.as<const uint32_t*>();
+    ga.win_out = I.d_win_next.as<uint32_t>();
+    ga.out = r.out;
+    ga.L = r.L;
+    ga.ck = r.ck;
+    if (r.timing) r.timing->record(r.stream, &g0);
+    if ((e = launch_gen(I.M, r.kind, r.cksum, ga, r.stream)) != cudaSuccess) return e;
+    if (r.timing) {
+        r.timing->record(r.stream, &g1);
+        r.timing->gen.push_back({g0, g1});
+    }
+    if ((e = cudaMemcpyAsync(r.win, I.d_win_next.p, sizeof(uint32_t) * I.N * I.S, cudaMemcpyDeviceToDevice,
+                             r.stream)) != cudaSuccess)
+        return e;
+    r.launches += 1;
+    r.pieces = (uint32_t)I.pieces.size();
+    r.warps_per_piece = 1;
+    return cudaGetLastError();
+}
+
+cudaError_t Planner::skip(const DevParams* params, uint32_t* win, uint64_t words, cudaStream_t st, std::string& err) {
+    PlannerImpl& I = *impl_;
+    if (!v2_supports(I.M)) {
+        err = "skip (jump-ahead) is implemented for mexp 11213, 23209 and 44497";
+        return cudaSuccess;
+    }
+    cudaError_t e;
+    if (!I.analyzed && (e = I.analyze(params, win, st, err)) != cudaSuccess) return e;
+    if (!I.jumps_ok) {
+        err = "no annihilating polynomial found for some stream";
+        return cudaSuccess;
+    }
+    const uint32_t qw = (I.M + 31) / 32;
+    std::vector<uint32_t> hq((size_t)I.S * qw, 0);
+    parallel_for(I.S, [&](size_t s) {
+        gf2::Poly q = I.mods[s]->x_pow(words);
+        for (int i = 0; i <= q.degree(); ++i)
+            if (q.coeff(i)) hq[s * qw + (i >> 5)] |= 1u << (i & 31);
+    });
+    const uint32_t pre_len = I.prefix_len();
+    DevBuf pre, q, rows, joff, jobs, out;
+    std::vector<uint32_t> hrows(I.S), hoff(I.S + 1);
+    std::vector<JumpJob> hjobs(I.S);
+    for (uint32_t s = 0; s < I.S; ++s) {
+        hrows[s] = s;
+        hoff[s] = s;
+        hjobs[s] = JumpJob{s, s};
+    }
+    hoff[I.S] = I.S;
+    auto cleanup = [&] {
+        for (DevBuf* b : {&pre, &q, &rows, &joff, &jobs, &out}) b->release();
+    };
+    if ((e = pre.ensure((size_t)pre_len * I.S * 4)) != cudaSuccess || (e = q.ensure(hq.size() * 4)) != cudaSuccess ||
+        (e = rows.ensure(I.S * 4)) != cudaSuccess || (e = joff.ensure((I.S + 1) * 4)) != cudaSuccess ||
+        (e = jobs.ensure(I.S * sizeof(JumpJob))) != cudaSuccess || (e = out.ensure((size_t)I.S * I.N * 4)) != cudaSuccess) {
+        cleanup();
+        return e;
+    }
+    cudaMemcpyAsync(q.p, hq.data(), hq.size() * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(rows.p, hrows.data(), I.S * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(joff.p, hoff.data(), (I.S + 1) * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(jobs.p, hjobs.data(), I.S * sizeof(JumpJob), cudaMemcpyHostToDevice, st);
+    e = launch_prefix(params, win, rows.as<uint32_t>(), I.S, I.N, pre.as<uint32_t>(), pre_len, st);
+    if (e == cudaSuccess) {
+        JumpArgs ja;
+        ja.pre = pre.as<uint32_t>();
+        ja.pre_len = pre_len;
+        ja.set_of = rows.as<uint32_t>();
+        ja.job_off = joff.as<uint32_t>();
+        ja.jobs = jobs.as<JumpJob>();
+        ja.q = q.as<uint32_t>();
+        ja.q_words = qw;
+        ja.piece_win = out.as<uint32_t>();
+        e = launch_jump(I.M, ja, I.S, st);
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(win, out.p, (size_t)I.S * I.N * 4, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cleanup();
+    return e;
 }
 
 }  // namespace mtgpb

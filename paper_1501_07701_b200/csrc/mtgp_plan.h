@@ -24,11 +24,9 @@ struct PlanRun {
     cudaStream_t stream = nullptr;
     uint32_t max_pieces = 0;
     uint64_t min_piece_words = 1ull << 21;
-    bool timing = false;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    EventPool* timing = nullptr;  // non-null: record event pairs around the launches
     // results
-    double gen_ms = 0, jump_ms = 0;
-    uint64_t gen_launches = 0, jump_launches = 0;
+    uint64_t launches = 0;        // kernels launched by this call
     uint32_t pieces = 0, warps_per_piece = 0;
 };
 
@@ -39,6 +37,8 @@ public:
     Planner(const std::vector<mtgp_params>& sets, int num_sms);
     ~Planner();
     bool v2_supported() const;
+    // forget per-stream algebra and cached plans (after a state restore)
+    void invalidate();
     cudaError_t run(PlanRun& r, std::string& err);
     cudaError_t skip(const DevParams* params, uint32_t* win, uint64_t words, cudaStream_t st,
                      std::string& err);

@@ -1,0 +1,451 @@
+// mtgp_v2.cu -- the B200 throughput path for MTGP32.
+//
+// Work decomposition. A call asks for L words of each of S streams. The S*L words are split
+// into "pieces" (contiguous ranges of one stream) so that every resident warp on the GPU has the
+// same amount of work; a piece that does not start at the stream's current position starts
+// from a GF(2) jump-ahead of the stream's state (mtgp_plan.cu computes x^offset mod P on the
+// host, jump_kernel below applies it on the device). One WARP ("team") owns a piece at a time
+// and keeps the piece's state in a private shared-memory ring; it needs no CTA barrier, only
+// __syncwarp between steps.
+//
+// gen_kernel step (256 words per warp; safe because any d <= N - pos consecutive MTGP words are
+// independent): lane t produces words 4t..4t+3 and 128+4t..128+4t+3 of the
+// step, so the two output STG.128 of a warp are each 512 contiguous bytes (fully coalesced),
+// and the new state words go to the ring with two aligned STS.128. The four ring operands a
+// word needs (x[i], x[i+1], x[i+pos], x[i+pos-1]) are read as aligned LDS.128 groups; the
+// 1..4 words a lane needs from its neighbour's group come over shfl. The ring phase is chosen
+// per piece so that stores are 16-byte aligned in both the ring and global memory; the
+// residues of the two read streams are then (-N) mod 4 (compile time) and (pos-1-N) mod 4
+// (runtime, dispatched to one of four unrolled variants). The recursion table and the
+// tempering table live in registers (lane l holds entry l & 15) and are looked up with
+// shfl.idx over 16-lane segments -- no index masking, no shared-memory table traffic.
+// Tempering, the float conversions and the checksums are fused into the same pass.
+#include <cstdio>
+
+#include "mtgp_v2.cuh"
+
+namespace mtgpb {
+
+#define FULL 0xffffffffu
+
+constexpr uint32_t cpow2(uint32_t v) {
+    uint32_t r = 1;
+    while (r < v) r <<= 1;
+    return r;
+}
+
+template <uint32_t MEXP>
+struct Shape {
+    static constexpr uint32_t N = MEXP / 32 + 1;
+    static constexpr uint32_t R = cpow2(N + kStepWords + 8);
+    static constexpr uint32_t RM = R - 1;
+    static constexpr uint32_t RA = (4u - (N & 3u)) & 3u;  // (-N) mod 4
+};
+
+uint32_t v2_ring_words(uint32_t mexp) {
+    switch (mexp) {
+        case 11213: return Shape<11213>::R;
+        case 23209: return Shape<23209>::R;
+        case 44497: return Shape<44497>::R;
+    }
+    return 0;
+}
+
+bool v2_supports(uint32_t mexp) { return v2_ring_words(mexp) != 0; }
+
+__device__ __forceinline__ uint32_t comp(const uint4& g, int c) {
+    return c == 0 ? g.x : c == 1 ? g.y : c == 2 ? g.z : g.w;
+}
+
+// para_rec (external pin curand_mtgp32_kernel.h:137-145). x << sh1 is an
+// IMAD by 2^sh1 so the shift runs on the FMA pipe instead of the ALU pipe.
+__device__ __forceinline__ uint32_t mtgp_rec(uint32_t a, uint32_t b, uint32_t c, uint32_t mask, uint32_t mul1,
+                                             uint32_t sh2, uint32_t tbl_reg) {
+    uint32_t x = (a & mask) ^ b;
+    x ^= x * mul1;
+    const uint32_t y = x ^ (c >> sh2);
+    return y ^ __shfl_sync(FULL, tbl_reg, y, 16);
+}
+
+// temper (curand_mtgp32_kernel.h:155-162): the index is the XOR of the low nibbles of T's bytes.
+__device__ __forceinline__ uint32_t mtgp_temper(uint32_t r, uint32_t t, uint32_t tmp_reg) {
+    t ^= t >> 16;
+    t ^= t >> 8;
+    return r ^ __shfl_sync(FULL, tmp_reg, t, 16);
+}
+
+template <int KIND>
+__device__ __forceinline__ uint32_t conv(uint32_t o) {
+    if (KIND == MTGP_U32) return o;
+    uint32_t v = (o >> 9) | 0x3F800000u;                                     // [1,2)
+    if (KIND == MTGP_F32_01OC) v = __float_as_uint(2.0f - __uint_as_float(v));  // (0,1]
+    return v;
+}
+
+struct PieceCtx {
+    uint32_t* ring;
+    uint32_t phi;  // slot(x_j) = (j + phi) & RM
+    uint32_t lane;
+    uint32_t pos, sh2, mask, mul1, tblr, tmpr;
+    uint32_t* optr;
+};
+
+// Words [n0, n0+cnt) of the piece, one per lane, cnt <= 255 (all independent).
+template <uint32_t MEXP, int KIND, bool CK>
+__device__ __forceinline__ void scalar_words(const PieceCtx& p, uint32_t n0, uint32_t cnt, unsigned long long& sum,
+                                             uint32_t& xr) {
+    using S = Shape<MEXP>;
+    for (uint32_t base = 0; base < cnt; base += 32) {
+        const uint32_t n = n0 + base + p.lane;
+        const bool act = base + p.lane < cnt;
+        const uint32_t a = p.ring[(n + p.phi) & S::RM];
+        const uint32_t b = p.ring[(n + 1 + p.phi) & S::RM];
+        const uint32_t c = p.ring[(n + p.pos + p.phi) & S::RM];
+        const uint32_t t = p.ring[(n + p.pos - 1 + p.phi) & S::RM];
+        const uint32_t r = mtgp_rec(a, b, c, p.mask, p.mul1, p.sh2, p.tblr);
+        const uint32_t o = conv<KIND>(mtgp_temper(r, t, p.tmpr));
+        if (act) {
+            p.ring[(n + S::N + p.phi) & S::RM] = r;
+            __stcs(p.optr + n, o);
+            if (CK) {
+                sum += o;
+                xr ^= o;
+            }
+        }
+    }
+}
+
+// One full 256-word step starting at piece word n. RC = (pos - 1 - N) mod 4.
+template <uint32_t MEXP, int RC, int KIND, bool CK>
+__device__ __forceinline__ void full_step(const PieceCtx& p, uint32_t n, unsigned long long& sum, uint32_t& xr) {
+    using S = Shape<MEXP>;
+    constexpr int RA = (int)S::RA;
+    const uint4* ring4 = reinterpret_cast<const uint4*>(p.ring);
+    const uint32_t l4 = 4 * p.lane;
+    const uint32_t bA = n + p.phi - RA;              // aligned slot of group (u=0, lane 0) of x_n
+    const uint32_t bC = n + p.pos - 1 + p.phi - RC;  // ... of x_{n+pos-1}
+    const uint4 GA0 = ring4[((bA + l4) & S::RM) >> 2];
+    const uint4 GA1 = ring4[((bA + 128 + l4) & S::RM) >> 2];
+    const uint4 EA = ring4[((bA + 256) & S::RM) >> 2];
+    const uint4 GC0 = ring4[((bC + l4) & S::RM) >> 2];
+    const uint4 GC1 = ring4[((bC + 128 + l4) & S::RM) >> 2];
+    const uint4 EC = ring4[((bC + 256) & S::RM) >> 2];
+    const uint32_t nl = (p.lane + 1) & 31;
+    const bool l0 = p.lane == 0;
+
+    uint32_t WA[2][5], WC[2][5];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const uint4 g = u ? GA1 : GA0;
+        const uint4 gn = u ? EA : GA1;
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            const int c = RA + j;
+            if (c < 4) {
+                WA[u][j] = comp(g, c);
+            } else {
+                const uint32_t send = l0 ? comp(gn, c - 4) : comp(g, c - 4);
+                WA[u][j] = __shfl_sync(FULL, send, nl);
+            }
+        }
+        const uint4 h = u ? GC1 : GC0;
+        const uint4 hn = u ? EC : GC1;
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            const int c = RC + j;
+            if (c < 4) {
+                WC[u][j] = comp(h, c);
+            } else {
+                const uint32_t send = l0 ? comp(hn, c - 4) : comp(h, c - 4);
+                WC[u][j] = __shfl_sync(FULL, send, nl);
+            }
+        }
+    }
+
+    uint4* ringw = reinterpret_cast<uint4*>(p.ring);
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        uint32_t r[4], o[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            r[c] = mtgp_rec(WA[u][c], WA[u][c + 1], WC[u][c + 1], p.mask, p.mul1, p.sh2, p.tblr);
+            o[c] = conv<KIND>(mtgp_temper(r[c], WC[u][c], p.tmpr));
+            if (CK) {
+                sum += o[c];
+                xr ^= o[c];
+            }
+        }
+        ringw[((n + 128 * u + l4 + S::N + p.phi) & S::RM) >> 2] = make_uint4(r[0], r[1], r[2], r[3]);
+        __stcs(reinterpret_cast<uint4*>(p.optr + n + 128 * u + l4), make_uint4(o[0], o[1], o[2], o[3]));
+    }
+}
+
+template <uint32_t MEXP, int RC, int KIND, bool CK>
+__device__ __forceinline__ void run_steps(const PieceCtx& p, uint32_t n, uint64_t len, unsigned long long& sum,
+                                       uint32_t& xr) {
+    for (; n + kStepWords <= len; n += kStepWords) {
+        full_step<MEXP, RC, KIND, CK>(p, n, sum, xr);
+        __syncwarp();
+    }
+}
+
+template <uint32_t MEXP, int KIND, bool CK>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) gen_kernel(GenArgs a) {
+    using S = Shape<MEXP>;
+    extern __shared__ uint4 smem4[];
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t team = blockIdx.x * kWarpsPerCta + warp;
+    if (team >= a.n_teams) return;
+    PieceCtx p;
+    p.ring = reinterpret_cast<uint32_t*>(smem4) + warp * S::R;
+    p.lane = lane;
+    const TeamWork tw = a.teams[team];
+    for (uint32_t pi = tw.first; pi < tw.first + tw.count; ++pi) {
+        const Piece pc = a.pieces[pi];
+        const DevParams& prm = a.params[pc.set];
+        p.pos = prm.pos;
+        p.sh2 = prm.sh2;
+        p.mask = prm.mask;
+        p.mul1 = 1u << prm.sh1;
+        p.tblr = prm.tbl[lane & 15];
+        p.tmpr = prm.tmp[lane & 15];
+        p.optr = reinterpret_cast<uint32_t*>(a.out) + (size_t)pc.set * a.L + pc.offset;
+        const uint64_t len = pc.len;
+        // head words so that full steps store 16-byte aligned in global memory
+        const uint32_t mis = (uint32_t)((reinterpret_cast<uintptr_t>(p.optr) >> 2) & 3u);
+        const uint32_t hh = (4u - mis) & 3u;
+        const uint32_t h = len < hh ? (uint32_t)len : hh;
+        p.phi = (0u - (h + S::N)) & 3u;
+        const uint32_t* w0 = a.piece_win[pi];
+        for (uint32_t j = lane; j < S::N; j += 32) p.ring[(j + p.phi) & S::RM] = w0[j];
+        __syncwarp();
+        unsigned long long sum = 0;
+        uint32_t xr = 0;
+        scalar_words<MEXP, KIND, CK>(p, 0, h, sum, xr);
+        __syncwarp();
+        const uint64_t full_end = h + ((len - h) / kStepWords) * kStepWords;
+        switch ((prm.pos - 1u - S::N) & 3u) {
+            case 0: run_steps<MEXP, 0, KIND, CK>(p, h, full_end, sum, xr); break;
+            case 1: run_steps<MEXP, 1, KIND, CK>(p, h, full_end, sum, xr); break;
+            case 2: run_steps<MEXP, 2, KIND, CK>(p, h, full_end, sum, xr); break;
+            default: run_steps<MEXP, 3, KIND, CK>(p, h, full_end, sum, xr); break;
+        }
+        scalar_words<MEXP, KIND, CK>(p, (uint32_t)full_end, (uint32_t)(len - full_end), sum, xr);
+        __syncwarp();
+        if (pc.offset + len == a.L) {
+            uint32_t* we = a.win_out + (size_t)pc.set * S::N;
+            for (uint32_t j = lane; j < S::N; j += 32) we[j] = p.ring[((uint32_t)len + j + p.phi) & S::RM];
+        }
+        if (CK) {
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) {
+                sum += __shfl_xor_sync(FULL, sum, s);
+                xr ^= __shfl_xor_sync(FULL, xr, s);
+            }
+            if (lane == 0) {
+                atomicAdd(&a.ck[pc.set].sum64, sum);
+                atomicXor(&a.ck[pc.set].xor32, xr);
+                atomicAdd(&a.ck[pc.set].words, (unsigned long long)len);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// prefix: the raw state-word sequence x_0..x_{len-1} of each listed set from its window.
+// One CTA per set (the v1 shape); feeds the jump kernel and the host charpoly analysis.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) prefix_kernel(const DevParams* __restrict__ params,
+                                                     const uint32_t* __restrict__ win,
+                                                     const uint32_t* __restrict__ sets, uint32_t N,
+                                                     uint32_t ring_mask, uint32_t* __restrict__ pre,
+                                                     uint32_t len) {
+    extern __shared__ uint32_t ring[];
+    __shared__ uint32_t s_tbl[16];
+    const uint32_t row = blockIdx.x;
+    const uint32_t set = sets[row];
+    const uint32_t t = threadIdx.x;
+    const DevParams& p = params[set];
+    const uint32_t pos = p.pos, sh1 = p.sh1, sh2 = p.sh2, mask = p.mask;
+    const uint32_t* w = win + (size_t)set * N;
+    uint32_t* o = pre + (size_t)row * len;
+    for (uint32_t j = t; j < N; j += blockDim.x) {
+        ring[j] = w[j];
+        o[j] = w[j];
+    }
+    if (t < 16) s_tbl[t] = p.tbl[t];
+    __syncthreads();
+    const uint32_t d = min((uint32_t)blockDim.x, N - pos);
+    for (uint32_t base = 0; base + N < len; base += d) {
+        const uint32_t n = base + t;
+        if (t < d && n + N < len) {
+            uint32_t x = (ring[n & ring_mask] & mask) ^ ring[(n + 1) & ring_mask];
+            x ^= x << sh1;
+            const uint32_t y = x ^ (ring[(n + pos) & ring_mask] >> sh2);
+            const uint32_t r = y ^ s_tbl[y & 15u];
+            ring[(n + N) & ring_mask] = r;
+            o[n + N] = r;
+        }
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_prefix(const DevParams* params, const uint32_t* win, const uint32_t* sets, uint32_t n_rows,
+                          uint32_t N, uint32_t* pre, uint32_t len, cudaStream_t st) {
+    if (n_rows == 0) return cudaSuccess;
+    const uint32_t R = next_pow2(N + 256);
+    const size_t smem = (size_t)R * 4;
+    cudaError_t e = cudaFuncSetAttribute(prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    prefix_kernel<<<n_rows, 256, smem, st>>>(params, win, sets, N, R - 1, pre, len);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// jump: y_j = XOR_{i : q_i = 1} x_{i+j}, j in [0, N) -- the window at offset o when
+// q = x^o mod P (P annihilates the stream; mtgp_plan.cu). One CTA per set with jumps; the set's
+// prefix is staged in shared memory; each warp takes one job (piece) at a time; lane l keeps
+// a sliding window of J consecutive j's in registers and walks q two bits at a time.
+// ------------------------------------------------------------------------------------------
+constexpr int kJumpJ = 12;
+constexpr int kJumpWarps = 8;
+
+template <uint32_t MEXP>
+__global__ void __launch_bounds__(kJumpWarps * 32) jump_kernel(JumpArgs a) {
+    constexpr uint32_t N = MEXP / 32 + 1;
+    constexpr int J = kJumpJ;
+    extern __shared__ uint4 jsm4[];
+    const uint32_t row = blockIdx.x;
+    const uint4* src = reinterpret_cast<const uint4*>(a.pre + (size_t)row * a.pre_len);
+    for (uint32_t i = threadIdx.x; i < a.pre_len / 4; i += blockDim.x) jsm4[i] = src[i];
+    __syncthreads();
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (uint32_t job = a.job_off[row] + warp; job < a.job_off[row + 1]; job += kJumpWarps) {
+        const JumpJob jb = a.jobs[job];
+        const uint32_t* q = a.q + (size_t)jb.q * a.q_words;
+        uint32_t* dst = a.piece_win + (size_t)jb.piece * N;
+        for (uint32_t j0 = 0; j0 < N; j0 += 32 * J) {
+            const uint32_t jl = j0 + J * lane;  // multiple of 4
+            uint32_t acc[J];
+#pragma unroll
+            for (int k = 0; k < J; ++k) acc[k] = 0;
+            for (uint32_t iw0 = 0; iw0 < a.q_words; iw0 += 32) {
+                const uint32_t qmine = iw0 + lane < a.q_words ? q[iw0 + lane] : 0u;
+                const uint32_t nw = min(32u, a.q_words - iw0);
+                for (uint32_t k32 = 0; k32 < nw; ++k32) {
+                    const uint32_t qw = __shfl_sync(FULL, qmine, k32);
+                    if (qw == 0) continue;
+                    const uint32_t base4 = ((iw0 + k32) * 32 + jl) >> 2;
+                    uint32_t w[J + 32];
+#pragma unroll
+                    for (int v = 0; v < (J + 32) / 4; ++v) {
+                        const uint4 g = jsm4[base4 + v];
+                        w[4 * v] = g.x;
+                        w[4 * v + 1] = g.y;
+                        w[4 * v + 2] = g.z;
+                        w[4 * v + 3] = g.w;
+                    }
+#pragma unroll
+                    for (int b = 0; b < 32; b += 2) {
+                        const uint32_t pat = (qw >> b) & 3u;
+                        if (pat == 1) {
+#pragma unroll
+                            for (int k = 0; k < J; ++k) acc[k] ^= w[b + k];
+                        } else if (pat == 2) {
+#pragma unroll
+                            for (int k = 0; k < J; ++k) acc[k] ^= w[b + 1 + k];
+                        } else if (pat == 3) {
+#pragma unroll
+                            for (int k = 0; k < J; ++k) acc[k] ^= w[b + k] ^ w[b + 1 + k];
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < J; ++k)
+                if (jl + k < N) dst[jl + k] = acc[k];
+        }
+    }
+}
+
+template <uint32_t MEXP>
+static cudaError_t launch_jump_t(const JumpArgs& a, uint32_t n_rows, cudaStream_t st) {
+    const size_t smem = (size_t)a.pre_len * 4;
+    cudaError_t e = cudaFuncSetAttribute(jump_kernel<MEXP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    jump_kernel<MEXP><<<n_rows, kJumpWarps * 32, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_jump(uint32_t mexp, const JumpArgs& a, uint32_t n_rows, cudaStream_t st) {
+    if (n_rows == 0) return cudaSuccess;
+    switch (mexp) {
+        case 11213: return launch_jump_t<11213>(a, n_rows, st);
+        case 23209: return launch_jump_t<23209>(a, n_rows, st);
+        case 44497: return launch_jump_t<44497>(a, n_rows, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------------------------------
+template <uint32_t MEXP, int KIND, bool CK>
+static cudaError_t launch_gen_t(const GenArgs& a, cudaStream_t st) {
+    const size_t smem = (size_t)kWarpsPerCta * Shape<MEXP>::R * 4;
+    auto k = gen_kernel<MEXP, KIND, CK>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const uint32_t grid = (a.n_teams + kWarpsPerCta - 1) / kWarpsPerCta;
+    k<<<grid, kWarpsPerCta * 32, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <uint32_t MEXP, int KIND, bool CK>
+static int occ_t() {
+    const size_t smem = (size_t)kWarpsPerCta * Shape<MEXP>::R * 4;
+    auto k = gen_kernel<MEXP, KIND, CK>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kWarpsPerCta * 32, smem) != cudaSuccess) return 0;
+    return n;
+}
+
+#define MTGP_DISPATCH(MEXP)                                                             \
+    switch (kind * 2 + (cksum ? 1 : 0)) {                                               \
+        case 0: return FN<MEXP, MTGP_U32, false> ARGS;                                  \
+        case 1: return FN<MEXP, MTGP_U32, true> ARGS;                                   \
+        case 2: return FN<MEXP, MTGP_F32_12, false> ARGS;                               \
+        case 3: return FN<MEXP, MTGP_F32_12, true> ARGS;                                \
+        case 4: return FN<MEXP, MTGP_F32_01OC, false> ARGS;                             \
+        case 5: return FN<MEXP, MTGP_F32_01OC, true> ARGS;                              \
+    }
+
+cudaError_t launch_gen(uint32_t mexp, int kind, bool cksum, const GenArgs& a, cudaStream_t st) {
+    if (a.n_teams == 0) return cudaSuccess;
+#define FN launch_gen_t
+#define ARGS (a, st)
+    switch (mexp) {
+        case 11213: MTGP_DISPATCH(11213) break;
+        case 23209: MTGP_DISPATCH(23209) break;
+        case 44497: MTGP_DISPATCH(44497) break;
+    }
+#undef FN
+#undef ARGS
+    return cudaErrorInvalidValue;
+}
+
+int gen_ctas_per_sm(uint32_t mexp, int kind, bool cksum) {
+#define FN occ_t
+#define ARGS ()
+    switch (mexp) {
+        case 11213: MTGP_DISPATCH(11213) break;
+        case 23209: MTGP_DISPATCH(23209) break;
+        case 44497: MTGP_DISPATCH(44497) break;
+    }
+#undef FN
+#undef ARGS
+    return 0;
+}
+
+}  // namespace mtgpb

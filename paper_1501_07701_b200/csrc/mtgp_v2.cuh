@@ -1,0 +1,50 @@
+// mtgp_v2.cuh -- launch interface of the v2 kernels (mtgp_v2.cu).
+#pragma once
+
+#include "mtgp_internal.cuh"
+
+namespace mtgpb {
+
+// Words a v2 team produces per full step (one warp, 8 words per lane).
+constexpr uint32_t kStepWords = 256;
+constexpr uint32_t kWarpsPerCta = 4;
+
+struct GenArgs {
+    const DevParams* params;
+    const Piece* pieces;
+    const TeamWork* teams;
+    uint32_t n_teams;
+    const uint32_t* const* piece_win;  // per piece: start window (N words)
+    uint32_t* win_out;                 // [n_sets][N] end windows
+    void* out;                         // per-stream stride L
+    uint64_t L;
+    DevCksum* ck;
+};
+
+struct JumpJob {
+    uint32_t piece;  // destination: jumped window of this piece
+    uint32_t q;      // index of its jump polynomial
+};
+
+struct JumpArgs {
+    const uint32_t* pre;      // [n_jump_sets][pre_len] state-word prefixes
+    uint32_t pre_len;         // >= M + N
+    const uint32_t* set_of;   // [n_jump_sets] set index of each prefix row
+    const uint32_t* job_off;  // [n_jump_sets + 1] CSR offsets into jobs
+    const JumpJob* jobs;
+    const uint32_t* q;        // [n_q][q_words] jump polynomials, bit i = coeff of x^i
+    uint32_t q_words;
+    uint32_t* piece_win;      // [n_pieces][N]
+};
+
+// ring size (words) of one warp team for exponent mexp
+uint32_t v2_ring_words(uint32_t mexp);
+bool v2_supports(uint32_t mexp);
+
+cudaError_t launch_prefix(const DevParams* params, const uint32_t* win, const uint32_t* sets, uint32_t n_rows,
+                          uint32_t N, uint32_t* pre, uint32_t len, cudaStream_t st);
+cudaError_t launch_jump(uint32_t mexp, const JumpArgs& a, uint32_t n_jump_sets, cudaStream_t st);
+cudaError_t launch_gen(uint32_t mexp, int kind, bool cksum, const GenArgs& a, cudaStream_t st);
+int gen_ctas_per_sm(uint32_t mexp, int kind, bool cksum);
+
+}  // namespace mtgpb

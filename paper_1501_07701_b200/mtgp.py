@@ -32,7 +32,7 @@ EXPORTS = (
     "mtgp_generate", "mtgp_generate_u32", "mtgp_generate_f32_12", "mtgp_generate_f32_01oc",
     "mtgp_skip", "mtgp_state_save", "mtgp_state_restore", "mtgp_checksums",
     "mtgp_checksums_reset", "mtgp_sync", "mtgp_kernel_timing", "mtgp_kernel_timing_reset",
-    "mtgp_last_plan",
+    "mtgp_last_plan", "mtgp_launch_count",
 )
 
 
@@ -87,6 +87,7 @@ def load_library(path: Optional[str] = None) -> C.CDLL:
     lib.mtgp_kernel_timing_reset.argtypes = [C.c_void_p]
     lib.mtgp_last_plan.argtypes = [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
     lib.mtgp_validate_params.argtypes = [C.POINTER(MtgpParamsC)]
+    lib.mtgp_launch_count.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
     if path is None:
         _lib = lib
     return lib
@@ -224,6 +225,11 @@ class MtgpContext:
         g, gl, j, jl = C.c_double(), C.c_uint64(), C.c_double(), C.c_uint64()
         _check(self.lib, self.lib.mtgp_kernel_timing(self.h, C.byref(g), C.byref(gl), C.byref(j), C.byref(jl)))
         return g.value, gl.value, j.value, jl.value
+
+    def launch_count(self) -> int:
+        v = C.c_uint64()
+        _check(self.lib, self.lib.mtgp_launch_count(self.h, C.byref(v)))
+        return v.value
 
     def kernel_timing_reset(self) -> None:
         _check(self.lib, self.lib.mtgp_kernel_timing_reset(self.h))

@@ -135,3 +135,67 @@ def test_checksum_option_off(curand_sets):
         ck = ctx.checksums()
     for s in range(2):
         assert ck[s] == (int(w[s].astype(np.uint64).sum()), int(np.bitwise_xor.reduce(w[s])), 1000)
+
+
+# ---------------- v2: jump-ahead pieces ----------------
+
+@pytest.mark.parametrize("mexp", [11213, 23209, 44497])
+def test_v2_jump_pieces_bit_exact(curand_sets, mexp):
+    """Force many jump-ahead pieces on a small request; every word must match the oracle."""
+    sets = curand_sets[40:46] if mexp == 11213 else tables.synthetic_sets(mexp, 6)
+    seeds = [101, 102, 103, 104, 105, 106]
+    L = 150001
+    with _ctx(sets, seeds, 2, **{mtgp.OPT_MIN_PIECE_WORDS: 3000}) as ctx:
+        w1 = ctx.fill_u32(L)
+        pieces, _, kv = ctx.last_plan()
+        assert kv == 2 and pieces > 6 * 10
+        w2 = ctx.fill_u32(77777)  # continues after the jumped call
+        ck = ctx.checksums()
+    ref, _ = oracle_py.mtgp_bulk(sets, seeds, L + 77777, threads=8)
+    assert np.array_equal(w1, ref[:, :L])
+    assert np.array_equal(w2, ref[:, L:])
+    for s in range(6):
+        allw = ref[s]
+        assert ck[s] == (int(allw.astype(np.uint64).sum()), int(np.bitwise_xor.reduce(allw)), L + 77777)
+
+
+def test_v2_float_kinds_with_jumps(curand_sets):
+    sets = curand_sets[:4]
+    for kind in (mtgp.F32_12, mtgp.F32_01OC):
+        with _ctx(sets, [9, 8, 7, 6], 2, **{mtgp.OPT_MIN_PIECE_WORDS: 5000}) as ctx:
+            w = ctx.generate_host(kind, 60000)
+            assert ctx.last_plan()[0] > 4
+        ref, _ = oracle_py.mtgp_bulk(sets, [9, 8, 7, 6], 60000, kind=kind, threads=4)
+        assert np.array_equal(w, ref)
+
+
+@pytest.mark.parametrize("mexp", [11213, 44497])
+def test_skip_jump_ahead(curand_sets, mexp):
+    sets = curand_sets[100:103] if mexp == 11213 else tables.synthetic_sets(mexp, 3)
+    with _ctx(sets, [1, 2, 3], 2) as ctx:
+        ctx.fill_u32(1000)
+        ctx.skip(10_000_019)
+        assert ctx.position(2) == 10_001_019
+        w = ctx.fill_u32(5000)
+    for s in range(3):
+        o = oracle_py.MtgpOracle(sets[s], s + 1)
+        o.skip(10_001_019)
+        assert np.array_equal(w[s], o.fill(5000))
+
+
+def test_v2_long_streams_full_compare(curand_sets):
+    """8 streams x 2^24 words with the default plan (hundreds of jumped pieces)."""
+    import torch
+    sets = curand_sets[150:158]
+    seeds = list(range(1000, 1008))
+    L = 1 << 24
+    with _ctx(sets, seeds, 0) as ctx:
+        buf = torch.empty((8, L), dtype=torch.int32, device="cuda")
+        ctx.set_option(mtgp.OPT_MIN_PIECE_WORDS, 1 << 16)
+        ctx.generate_device(mtgp.U32, buf.data_ptr(), L)
+        ctx.sync()
+        pieces = ctx.last_plan()[0]
+        got = buf.cpu().numpy().view(np.uint32)
+    assert pieces >= 256
+    ref, _ = oracle_py.mtgp_bulk(sets, seeds, L, threads=8)
+    assert np.array_equal(got, ref)
