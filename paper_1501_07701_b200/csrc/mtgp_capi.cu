@@ -178,6 +178,13 @@ int mtgp_ctx_create(mtgp_ctx** out, int device, const mtgp_params* sets, uint32_
         dp[s].sh1 = sets[s].sh1;
         dp[s].sh2 = sets[s].sh2;
         dp[s].mask = sets[s].mask;
+        dp[s].mul1 = 1u << sets[s].sh1;
+        dp[s].mulhi2 = 1u << (32 - sets[s].sh2);
+        dp[s].m16 = 1u << 16;
+        dp[s].m24 = 1u << 24;
+        dp[s].m23 = 1u << 23;
+        dp[s].one = 1;
+        dp[s].pad0 = dp[s].pad1 = 0;
         std::memcpy(dp[s].tbl, sets[s].tbl, sizeof(dp[s].tbl));
         std::memcpy(dp[s].tmp, sets[s].tmp_tbl, sizeof(dp[s].tmp));
     }

@@ -15,6 +15,10 @@ namespace mtgpb {
 // (lane l keeps tbl[l & 15], tmp[l & 15]) and look them up with one shfl.
 struct alignas(16) DevParams {
     uint32_t pos, sh1, sh2, mask;
+    // Multipliers that move shifts onto the FMA pipe: x << sh1 == x * mul1,
+    // x >> sh2 == umulhi(x, mulhi2), x >> 16 == umulhi(x, m16), x >> 8 == umulhi(x, m24),
+    // x >> 9 == umulhi(x, m23). Loaded from memory so the compiler cannot fold them back to SHF.
+    uint32_t mul1, mulhi2, m16, m24, m23, one, pad0, pad1;
     uint32_t tbl[16];
     uint32_t tmp[16];
 };

@@ -89,6 +89,7 @@ struct PlannerImpl {
     std::vector<uint32_t> job_off;
     std::vector<JumpJob> jobs;
     uint32_t n_q = 0;
+    uint32_t max_jobs_per_row = 0;
     uint32_t q_words = 0;
     uint32_t pre_len = 0;
 
@@ -242,6 +243,7 @@ cudaError_t PlannerImpl::build_plan(uint64_t L, uint32_t T, uint64_t min_piece, 
     for (uint32_t i = 0; i < pieces.size(); ++i)
         if (pieces[i].offset) by_set[pieces[i].set].push_back(i);
     jump_rows.clear();
+    max_jobs_per_row = 0;
     job_off.assign(1, 0);
     jobs.clear();
     q_words = (M + 31) / 32;
@@ -254,6 +256,7 @@ cudaError_t PlannerImpl::build_plan(uint64_t L, uint32_t T, uint64_t min_piece, 
             qlist.push_back({pi, kv.first});
         }
         job_off.push_back((uint32_t)jobs.size());
+        max_jobs_per_row = std::max<uint32_t>(max_jobs_per_row, (uint32_t)kv.second.size());
     }
     n_q = (uint32_t)qlist.size();
     // jump polynomials x^offset mod P, chained per set
@@ -357,6 +360,7 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         ja.q = I.d_q.as<uint32_t>();
         ja.q_words = I.q_words;
         ja.piece_win = I.d_pwin.as<uint32_t>();
+        ja.max_jobs_per_row = I.max_jobs_per_row;
         if ((e = launch_jump(I.M, ja, (uint32_t)I.jump_rows.size(), r.stream)) != cudaSuccess) return e;
         if (r.timing) {
             r.timing->record(r.stream, &j1);

@@ -57,79 +57,105 @@ __device__ __forceinline__ uint32_t comp(const uint4& g, int c) {
     return c == 0 ? g.x : c == 1 ? g.y : c == 2 ? g.z : g.w;
 }
 
-// para_rec (external pin curand_mtgp32_kernel.h:137-145). x << sh1 is an
-// IMAD by 2^sh1 so the shift runs on the FMA pipe instead of the ALU pipe.
-__device__ __forceinline__ uint32_t mtgp_rec(uint32_t a, uint32_t b, uint32_t c, uint32_t mask, uint32_t mul1,
-                                             uint32_t sh2, uint32_t tbl_reg) {
-    uint32_t x = (a & mask) ^ b;
-    x ^= x * mul1;
-    const uint32_t y = x ^ (c >> sh2);
-    return y ^ __shfl_sync(FULL, tbl_reg, y, 16);
+// ---- shared-window helpers: 32-bit shared addresses, explicit vector accesses ----
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t x) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(x) : "memory");
+}
+__device__ __forceinline__ uint32_t umulhi(uint32_t a, uint32_t b) { return __umulhi(a, b); }
+
+struct PieceCtx {
+    uint32_t rb;   // shared-window byte address of the ring (aligned to its size)
+    uint32_t phi;  // slot(x_j) = (j + phi) & RM
+    uint32_t lane;
+    uint32_t pos, mask, mul1, mulhi2, m16, m24, m23, one, tblr, tmpr;
+    uint32_t* optr;
+};
+
+// para_rec (external pin curand_mtgp32_kernel.h:137-145) with both shifts
+// on the FMA pipe (IMAD / IMAD.HI by opaque powers of two) so the ALU pipe only sees LOP3s.
+__device__ __forceinline__ uint32_t rec_f(const PieceCtx& p, uint32_t a, uint32_t b, uint32_t c) {
+    const uint32_t x = (a & p.mask) ^ b;
+    const uint32_t y = x ^ (x * p.mul1) ^ umulhi(c, p.mulhi2);
+    return y ^ __shfl_sync(FULL, p.tblr, y, 16);
 }
 
-// temper (curand_mtgp32_kernel.h:155-162): the index is the XOR of the low nibbles of T's bytes.
-__device__ __forceinline__ uint32_t mtgp_temper(uint32_t r, uint32_t t, uint32_t tmp_reg) {
-    t ^= t >> 16;
-    t ^= t >> 8;
-    return r ^ __shfl_sync(FULL, tmp_reg, t, 16);
+// temper (curand_mtgp32_kernel.h:155-162): the index is the XOR of the low nibbles of T's
+// four bytes; shfl.idx over a 16-lane segment reads only index bits [3:0].
+__device__ __forceinline__ uint32_t temper_f(const PieceCtx& p, uint32_t r, uint32_t t) {
+    t ^= umulhi(t, p.m16);
+    t ^= umulhi(t, p.m24);
+    return r ^ __shfl_sync(FULL, p.tmpr, t, 16);
 }
 
 template <int KIND>
-__device__ __forceinline__ uint32_t conv(uint32_t o) {
+__device__ __forceinline__ uint32_t conv_f(const PieceCtx& p, uint32_t o) {
     if (KIND == MTGP_U32) return o;
-    uint32_t v = (o >> 9) | 0x3F800000u;                                     // [1,2)
+    uint32_t v = umulhi(o, p.m23) | 0x3F800000u;                               // [1,2)
     if (KIND == MTGP_F32_01OC) v = __float_as_uint(2.0f - __uint_as_float(v));  // (0,1]
     return v;
 }
 
-struct PieceCtx {
-    uint32_t* ring;
-    uint32_t phi;  // slot(x_j) = (j + phi) & RM
-    uint32_t lane;
-    uint32_t pos, sh2, mask, mul1, tblr, tmpr;
-    uint32_t* optr;
-};
+template <bool CK>
+__device__ __forceinline__ void ck_add(const PieceCtx& p, unsigned long long& sum, uint32_t v) {
+    if (CK) asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(sum) : "r"(v), "r"(p.one));
+}
 
 // Words [n0, n0+cnt) of the piece, one per lane, cnt <= 255 (all independent).
 template <uint32_t MEXP, int KIND, bool CK>
 __device__ __forceinline__ void scalar_words(const PieceCtx& p, uint32_t n0, uint32_t cnt, unsigned long long& sum,
                                              uint32_t& xr) {
     using S = Shape<MEXP>;
+    constexpr uint32_t RMB = S::R * 4 - 1;
     for (uint32_t base = 0; base < cnt; base += 32) {
         const uint32_t n = n0 + base + p.lane;
         const bool act = base + p.lane < cnt;
-        const uint32_t a = p.ring[(n + p.phi) & S::RM];
-        const uint32_t b = p.ring[(n + 1 + p.phi) & S::RM];
-        const uint32_t c = p.ring[(n + p.pos + p.phi) & S::RM];
-        const uint32_t t = p.ring[(n + p.pos - 1 + p.phi) & S::RM];
-        const uint32_t r = mtgp_rec(a, b, c, p.mask, p.mul1, p.sh2, p.tblr);
-        const uint32_t o = conv<KIND>(mtgp_temper(r, t, p.tmpr));
+        const uint32_t nb = (n + p.phi) * 4;
+        const uint32_t a = lds32(p.rb + (nb & RMB));
+        const uint32_t b = lds32(p.rb + ((nb + 4) & RMB));
+        const uint32_t c = lds32(p.rb + ((nb + 4 * p.pos) & RMB));
+        const uint32_t t = lds32(p.rb + ((nb + 4 * p.pos - 4) & RMB));
+        const uint32_t r = rec_f(p, a, b, c);
+        const uint32_t o = conv_f<KIND>(p, temper_f(p, r, t));
         if (act) {
-            p.ring[(n + S::N + p.phi) & S::RM] = r;
+            sts32(p.rb + ((nb + 4 * S::N) & RMB), r);
             __stcs(p.optr + n, o);
-            if (CK) {
-                sum += o;
-                xr ^= o;
-            }
+            ck_add<CK>(p, sum, o);
+            if (CK) xr ^= o;
         }
     }
 }
 
 // One full 256-word step starting at piece word n. RC = (pos - 1 - N) mod 4.
+// Ring addresses: byte offset (n + phi)*4 plus a lane constant, masked to the ring and OR-ed
+// with the size-aligned ring base (2 ALU ops per vector access).
 template <uint32_t MEXP, int RC, int KIND, bool CK>
 __device__ __forceinline__ void full_step(const PieceCtx& p, uint32_t n, unsigned long long& sum, uint32_t& xr) {
     using S = Shape<MEXP>;
     constexpr int RA = (int)S::RA;
-    const uint4* ring4 = reinterpret_cast<const uint4*>(p.ring);
-    const uint32_t l4 = 4 * p.lane;
-    const uint32_t bA = n + p.phi - RA;              // aligned slot of group (u=0, lane 0) of x_n
-    const uint32_t bC = n + p.pos - 1 + p.phi - RC;  // ... of x_{n+pos-1}
-    const uint4 GA0 = ring4[((bA + l4) & S::RM) >> 2];
-    const uint4 GA1 = ring4[((bA + 128 + l4) & S::RM) >> 2];
-    const uint4 EA = ring4[((bA + 256) & S::RM) >> 2];
-    const uint4 GC0 = ring4[((bC + l4) & S::RM) >> 2];
-    const uint4 GC1 = ring4[((bC + 128 + l4) & S::RM) >> 2];
-    const uint4 EC = ring4[((bC + 256) & S::RM) >> 2];
+    constexpr uint32_t RMB = S::R * 4 - 1;
+    const uint32_t nb = (n + p.phi) * 4;
+    const uint32_t l16 = 16 * p.lane;
+    const uint32_t bA = nb - 4 * RA;
+    const uint32_t bC = nb + 4 * (p.pos - 1) - 4 * RC;
+    const uint4 GA0 = lds128(((bA + l16) & RMB) | p.rb);
+    const uint4 GA1 = lds128(((bA + 512 + l16) & RMB) | p.rb);
+    const uint4 EA = lds128(((bA + 1024) & RMB) | p.rb);
+    const uint4 GC0 = lds128(((bC + l16) & RMB) | p.rb);
+    const uint4 GC1 = lds128(((bC + 512 + l16) & RMB) | p.rb);
+    const uint4 EC = lds128(((bC + 1024) & RMB) | p.rb);
     const uint32_t nl = (p.lane + 1) & 31;
     const bool l0 = p.lane == 0;
 
@@ -162,27 +188,25 @@ __device__ __forceinline__ void full_step(const PieceCtx& p, uint32_t n, unsigne
         }
     }
 
-    uint4* ringw = reinterpret_cast<uint4*>(p.ring);
+    const uint32_t bS = nb + 4 * S::N + l16;
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
         uint32_t r[4], o[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            r[c] = mtgp_rec(WA[u][c], WA[u][c + 1], WC[u][c + 1], p.mask, p.mul1, p.sh2, p.tblr);
-            o[c] = conv<KIND>(mtgp_temper(r[c], WC[u][c], p.tmpr));
-            if (CK) {
-                sum += o[c];
-                xr ^= o[c];
-            }
+            r[c] = rec_f(p, WA[u][c], WA[u][c + 1], WC[u][c + 1]);
+            o[c] = conv_f<KIND>(p, temper_f(p, r[c], WC[u][c]));
+            ck_add<CK>(p, sum, o[c]);
         }
-        ringw[((n + 128 * u + l4 + S::N + p.phi) & S::RM) >> 2] = make_uint4(r[0], r[1], r[2], r[3]);
-        __stcs(reinterpret_cast<uint4*>(p.optr + n + 128 * u + l4), make_uint4(o[0], o[1], o[2], o[3]));
+        if (CK) xr ^= o[0] ^ o[1] ^ o[2] ^ o[3];
+        sts128(((bS + 512 * u) & RMB) | p.rb, r[0], r[1], r[2], r[3]);
+        __stcs(reinterpret_cast<uint4*>(p.optr + n + 128 * u) + p.lane, make_uint4(o[0], o[1], o[2], o[3]));
     }
 }
 
 template <uint32_t MEXP, int RC, int KIND, bool CK>
 __device__ __forceinline__ void run_steps(const PieceCtx& p, uint32_t n, uint64_t len, unsigned long long& sum,
-                                       uint32_t& xr) {
+                                          uint32_t& xr) {
     for (; n + kStepWords <= len; n += kStepWords) {
         full_step<MEXP, RC, KIND, CK>(p, n, sum, xr);
         __syncwarp();
@@ -198,16 +222,25 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) gen_kernel(GenArgs a) {
     const uint32_t team = blockIdx.x * kWarpsPerCta + warp;
     if (team >= a.n_teams) return;
     PieceCtx p;
-    p.ring = reinterpret_cast<uint32_t*>(smem4) + warp * S::R;
+    {
+        // rings are aligned to their size so that (offset & RMB) | base addresses them
+        const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem4);
+        const uint32_t rbytes = S::R * 4;
+        p.rb = ((base + rbytes - 1) & ~(rbytes - 1)) + warp * rbytes;
+    }
     p.lane = lane;
     const TeamWork tw = a.teams[team];
     for (uint32_t pi = tw.first; pi < tw.first + tw.count; ++pi) {
         const Piece pc = a.pieces[pi];
         const DevParams& prm = a.params[pc.set];
         p.pos = prm.pos;
-        p.sh2 = prm.sh2;
         p.mask = prm.mask;
-        p.mul1 = 1u << prm.sh1;
+        p.mul1 = prm.mul1;
+        p.mulhi2 = prm.mulhi2;
+        p.m16 = prm.m16;
+        p.m24 = prm.m24;
+        p.m23 = prm.m23;
+        p.one = prm.one;
         p.tblr = prm.tbl[lane & 15];
         p.tmpr = prm.tmp[lane & 15];
         p.optr = reinterpret_cast<uint32_t*>(a.out) + (size_t)pc.set * a.L + pc.offset;
@@ -218,7 +251,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) gen_kernel(GenArgs a) {
         const uint32_t h = len < hh ? (uint32_t)len : hh;
         p.phi = (0u - (h + S::N)) & 3u;
         const uint32_t* w0 = a.piece_win[pi];
-        for (uint32_t j = lane; j < S::N; j += 32) p.ring[(j + p.phi) & S::RM] = w0[j];
+        for (uint32_t j = lane; j < S::N; j += 32) sts32(p.rb + (((j + p.phi) & S::RM) << 2), w0[j]);
         __syncwarp();
         unsigned long long sum = 0;
         uint32_t xr = 0;
@@ -235,7 +268,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) gen_kernel(GenArgs a) {
         __syncwarp();
         if (pc.offset + len == a.L) {
             uint32_t* we = a.win_out + (size_t)pc.set * S::N;
-            for (uint32_t j = lane; j < S::N; j += 32) we[j] = p.ring[((uint32_t)len + j + p.phi) & S::RM];
+            for (uint32_t j = lane; j < S::N; j += 32)
+                we[j] = lds32(p.rb + ((((uint32_t)len + j + p.phi) & S::RM) << 2));
         }
         if (CK) {
 #pragma unroll
@@ -317,12 +351,16 @@ __global__ void __launch_bounds__(kJumpWarps * 32) jump_kernel(JumpArgs a) {
     constexpr uint32_t N = MEXP / 32 + 1;
     constexpr int J = kJumpJ;
     extern __shared__ uint4 jsm4[];
+    // grid: x = prefix row (set), y = group of kJumpWarps jobs of that set
     const uint32_t row = blockIdx.x;
+    const uint32_t first = a.job_off[row] + blockIdx.y * kJumpWarps;
+    const uint32_t end = a.job_off[row + 1];
+    if (first >= end) return;
     const uint4* src = reinterpret_cast<const uint4*>(a.pre + (size_t)row * a.pre_len);
     for (uint32_t i = threadIdx.x; i < a.pre_len / 4; i += blockDim.x) jsm4[i] = src[i];
     __syncthreads();
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (uint32_t job = a.job_off[row] + warp; job < a.job_off[row + 1]; job += kJumpWarps) {
+    for (uint32_t job = first + warp; job < end && job < first + kJumpWarps; job += kJumpWarps) {
         const JumpJob jb = a.jobs[job];
         const uint32_t* q = a.q + (size_t)jb.q * a.q_words;
         uint32_t* dst = a.piece_win + (size_t)jb.piece * N;
@@ -375,7 +413,8 @@ static cudaError_t launch_jump_t(const JumpArgs& a, uint32_t n_rows, cudaStream_
     const size_t smem = (size_t)a.pre_len * 4;
     cudaError_t e = cudaFuncSetAttribute(jump_kernel<MEXP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    jump_kernel<MEXP><<<n_rows, kJumpWarps * 32, smem, st>>>(a);
+    const dim3 grid(n_rows, (a.max_jobs_per_row + kJumpWarps - 1) / kJumpWarps);
+    jump_kernel<MEXP><<<grid, kJumpWarps * 32, smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -392,7 +431,7 @@ cudaError_t launch_jump(uint32_t mexp, const JumpArgs& a, uint32_t n_rows, cudaS
 // ------------------------------------------------------------------------------------------
 template <uint32_t MEXP, int KIND, bool CK>
 static cudaError_t launch_gen_t(const GenArgs& a, cudaStream_t st) {
-    const size_t smem = (size_t)kWarpsPerCta * Shape<MEXP>::R * 4;
+    const size_t smem = (size_t)(kWarpsPerCta + 1) * Shape<MEXP>::R * 4;
     auto k = gen_kernel<MEXP, KIND, CK>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -403,7 +442,7 @@ static cudaError_t launch_gen_t(const GenArgs& a, cudaStream_t st) {
 
 template <uint32_t MEXP, int KIND, bool CK>
 static int occ_t() {
-    const size_t smem = (size_t)kWarpsPerCta * Shape<MEXP>::R * 4;
+    const size_t smem = (size_t)(kWarpsPerCta + 1) * Shape<MEXP>::R * 4;
     auto k = gen_kernel<MEXP, KIND, CK>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
     int n = 0;

@@ -35,6 +35,7 @@ struct JumpArgs {
     const uint32_t* q;        // [n_q][q_words] jump polynomials, bit i = coeff of x^i
     uint32_t q_words;
     uint32_t* piece_win;      // [n_pieces][N]
+    uint32_t max_jobs_per_row = 1;
 };
 
 // ring size (words) of one warp team for exponent mexp

@@ -13,10 +13,10 @@ pytestmark = pytest.mark.gpu
 KERNELS = [1, 2]
 
 
-def _ctx(sets, seeds, kernel, **opts):
+def _ctx(sets, seeds, kernel, opts=None):
     ctx = mtgp.MtgpContext(sets, seeds)
     ctx.set_option(mtgp.OPT_KERNEL, kernel)
-    for k, v in opts.items():
+    for k, v in (opts or {}).items():
         ctx.set_option(k, v)
     return ctx
 
@@ -145,7 +145,7 @@ def test_v2_jump_pieces_bit_exact(curand_sets, mexp):
     sets = curand_sets[40:46] if mexp == 11213 else tables.synthetic_sets(mexp, 6)
     seeds = [101, 102, 103, 104, 105, 106]
     L = 150001
-    with _ctx(sets, seeds, 2, **{mtgp.OPT_MIN_PIECE_WORDS: 3000}) as ctx:
+    with _ctx(sets, seeds, 2, {mtgp.OPT_MIN_PIECE_WORDS: 3000}) as ctx:
         w1 = ctx.fill_u32(L)
         pieces, _, kv = ctx.last_plan()
         assert kv == 2 and pieces > 6 * 10
@@ -162,7 +162,7 @@ def test_v2_jump_pieces_bit_exact(curand_sets, mexp):
 def test_v2_float_kinds_with_jumps(curand_sets):
     sets = curand_sets[:4]
     for kind in (mtgp.F32_12, mtgp.F32_01OC):
-        with _ctx(sets, [9, 8, 7, 6], 2, **{mtgp.OPT_MIN_PIECE_WORDS: 5000}) as ctx:
+        with _ctx(sets, [9, 8, 7, 6], 2, {mtgp.OPT_MIN_PIECE_WORDS: 5000}) as ctx:
             w = ctx.generate_host(kind, 60000)
             assert ctx.last_plan()[0] > 4
         ref, _ = oracle_py.mtgp_bulk(sets, [9, 8, 7, 6], 60000, kind=kind, threads=4)
