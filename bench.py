@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--sets", type=int, default=200)
-    ap.add_argument("--calls", type=int, default=4, help="device calls per step (output buffer = step/calls)")
+    ap.add_argument("--calls", type=int, default=2, help="device calls per step (output buffer = step/calls)")
     ap.add_argument("--no-checksum", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -208,6 +208,10 @@ cudaError_t PlannerImpl::build_plan(uint64_t L, uint32_t T, uint64_t min_piece, 
     const uint64_t W = (uint64_t)S * L;
     uint64_t want = std::max<uint64_t>(1, W / std::max<uint64_t>(1, min_piece));
     want = std::min<uint64_t>(want, T);
+    // Equal work per SM: team counts are whole multiples of (SMs x warps per CTA), so every SM
+    // holds the same number of CTAs (a 5-vs-6 CTA split costs ~10% of the makespan).
+    const uint64_t quantum = (uint64_t)num_sms * kWarpsPerCta;
+    if (want >= quantum) want -= want % quantum;
     want = std::max<uint64_t>(want, (W + kMaxPieceWords - 1) / kMaxPieceWords);
     pieces.clear();
     teams.clear();

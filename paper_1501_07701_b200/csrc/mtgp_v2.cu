@@ -28,6 +28,25 @@ namespace mtgpb {
 
 #define FULL 0xffffffffu
 
+// Pipe-balance switches (tools/sweep_variants.sh measures them on the B200):
+// move a shift onto the FMA pipe (IMAD / IMAD.HI by an opaque power of two) or keep it on the
+// ALU pipe (SHF); accumulate sum64 with IMAD.WIDE or IADD3 carry chains; CTAs/SM register target.
+#ifndef MTGP_SH1_IMAD
+#define MTGP_SH1_IMAD 1
+#endif
+#ifndef MTGP_SH2_IMAD
+#define MTGP_SH2_IMAD 0
+#endif
+#ifndef MTGP_FOLD_IMAD
+#define MTGP_FOLD_IMAD 0
+#endif
+#ifndef MTGP_CK_WIDE
+#define MTGP_CK_WIDE 0
+#endif
+#ifndef MTGP_MIN_CTAS
+#define MTGP_MIN_CTAS 6
+#endif
+
 constexpr uint32_t cpow2(uint32_t v) {
     uint32_t r = 1;
     while (r < v) r <<= 1;
@@ -80,7 +99,7 @@ struct PieceCtx {
     uint32_t rb;   // shared-window byte address of the ring (aligned to its size)
     uint32_t phi;  // slot(x_j) = (j + phi) & RM
     uint32_t lane;
-    uint32_t pos, mask, mul1, mulhi2, m16, m24, m23, one, tblr, tmpr;
+    uint32_t pos, mask, sh1, sh2, mul1, mulhi2, m16, m24, m23, one, tblr, tmpr;
     uint32_t* optr;
 };
 
@@ -88,15 +107,30 @@ struct PieceCtx {
 // on the FMA pipe (IMAD / IMAD.HI by opaque powers of two) so the ALU pipe only sees LOP3s.
 __device__ __forceinline__ uint32_t rec_f(const PieceCtx& p, uint32_t a, uint32_t b, uint32_t c) {
     const uint32_t x = (a & p.mask) ^ b;
-    const uint32_t y = x ^ (x * p.mul1) ^ umulhi(c, p.mulhi2);
+#if MTGP_SH1_IMAD
+    const uint32_t xs = x * p.mul1;
+#else
+    const uint32_t xs = x << p.sh1;
+#endif
+#if MTGP_SH2_IMAD
+    const uint32_t cs = umulhi(c, p.mulhi2);
+#else
+    const uint32_t cs = c >> p.sh2;
+#endif
+    const uint32_t y = x ^ xs ^ cs;
     return y ^ __shfl_sync(FULL, p.tblr, y, 16);
 }
 
 // temper (curand_mtgp32_kernel.h:155-162): the index is the XOR of the low nibbles of T's
 // four bytes; shfl.idx over a 16-lane segment reads only index bits [3:0].
 __device__ __forceinline__ uint32_t temper_f(const PieceCtx& p, uint32_t r, uint32_t t) {
+#if MTGP_FOLD_IMAD
     t ^= umulhi(t, p.m16);
     t ^= umulhi(t, p.m24);
+#else
+    t ^= t >> 16;
+    t ^= t >> 8;
+#endif
     return r ^ __shfl_sync(FULL, p.tmpr, t, 16);
 }
 
@@ -110,7 +144,11 @@ __device__ __forceinline__ uint32_t conv_f(const PieceCtx& p, uint32_t o) {
 
 template <bool CK>
 __device__ __forceinline__ void ck_add(const PieceCtx& p, unsigned long long& sum, uint32_t v) {
+#if MTGP_CK_WIDE
     if (CK) asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(sum) : "r"(v), "r"(p.one));
+#else
+    if (CK) sum += v;
+#endif
 }
 
 // Words [n0, n0+cnt) of the piece, one per lane, cnt <= 255 (all independent).
@@ -214,7 +252,7 @@ __device__ __forceinline__ void run_steps(const PieceCtx& p, uint32_t n, uint64_
 }
 
 template <uint32_t MEXP, int KIND, bool CK>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) gen_kernel(GenArgs a) {
+__global__ void __launch_bounds__(kWarpsPerCta * 32, MTGP_MIN_CTAS) gen_kernel(GenArgs a) {
     using S = Shape<MEXP>;
     extern __shared__ uint4 smem4[];
     const uint32_t warp = threadIdx.x >> 5;
@@ -235,6 +273,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) gen_kernel(GenArgs a) {
         const DevParams& prm = a.params[pc.set];
         p.pos = prm.pos;
         p.mask = prm.mask;
+        p.sh1 = prm.sh1;
+        p.sh2 = prm.sh2;
         p.mul1 = prm.mul1;
         p.mulhi2 = prm.mulhi2;
         p.m16 = prm.m16;

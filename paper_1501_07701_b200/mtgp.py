@@ -123,8 +123,8 @@ class MtgpContext:
     """n_sets independent MTGP32 streams on one GPU (C-ABI mtgp_ctx)."""
 
     def __init__(self, sets: Sequence[MtgpParams], seeds: Sequence[int], device: int = 0,
-                 stream: Optional[int] = None):
-        self.lib = load_library()
+                 stream: Optional[int] = None, lib: Optional[C.CDLL] = None):
+        self.lib = lib if lib is not None else load_library()
         if len(seeds) != len(sets):
             raise ValueError("one seed per parameter set")
         self.sets = list(sets)
