@@ -176,24 +176,38 @@ __device__ __forceinline__ void scalar_words(const PieceCtx& p, uint32_t n0, uin
     }
 }
 
-// One full 256-word step starting at piece word n. RC = (pos - 1 - N) mod 4.
-// Ring addresses: byte offset (n + phi)*4 plus a lane constant, masked to the ring and OR-ed
-// with the size-aligned ring base (2 ALU ops per vector access).
-template <uint32_t MEXP, int RC, int KIND, bool CK>
+// One full 256-word step starting at piece word n, ring phase Q = step index mod (R/256).
+// RC = (pos - 1 - N) mod 4. The piece's ring phase phi = RA - h puts the aligned x_n group
+// at slot 256*Q, so the A groups, and -- except in the last phase(s) of the ring period --
+// the C groups and the stores, are addressed as (uniform base) + 16*lane + 512*u without any
+// wrap masking; only the uniform E groups and the wrapping phases pay for a mask.
+template <uint32_t MEXP, int RC, int KIND, bool CK, int Q>
 __device__ __forceinline__ void full_step(const PieceCtx& p, uint32_t n, unsigned long long& sum, uint32_t& xr) {
     using S = Shape<MEXP>;
     constexpr int RA = (int)S::RA;
-    constexpr uint32_t RMB = S::R * 4 - 1;
-    const uint32_t nb = (n + p.phi) * 4;
+    constexpr uint32_t RB = S::R * 4;  // ring bytes
+    constexpr uint32_t RMB = RB - 1;
+    constexpr uint32_t qa = 1024u * Q;                       // A group byte base in this phase
+    constexpr uint32_t cS4 = 4u * (S::N + RA);               // store offset from the A base
+    constexpr uint32_t cCmax4 = 4u * (S::N - 257u + RA);     // largest C offset (pos <= N - 256)
+    constexpr bool wrapC = qa + cCmax4 + 1040u > RB;
+    constexpr bool wrapS = qa + cS4 + 1024u > RB;
     const uint32_t l16 = 16 * p.lane;
-    const uint32_t bA = nb - 4 * RA;
-    const uint32_t bC = nb + 4 * (p.pos - 1) - 4 * RC;
-    const uint4 GA0 = lds128(((bA + l16) & RMB) | p.rb);
-    const uint4 GA1 = lds128(((bA + 512 + l16) & RMB) | p.rb);
-    const uint4 EA = lds128(((bA + 1024) & RMB) | p.rb);
-    const uint4 GC0 = lds128(((bC + l16) & RMB) | p.rb);
-    const uint4 GC1 = lds128(((bC + 512 + l16) & RMB) | p.rb);
-    const uint4 EC = lds128(((bC + 1024) & RMB) | p.rb);
+    const uint32_t cC4 = 4u * (p.pos - 1u + RA - RC);
+    const uint32_t aA = p.rb + qa + l16;
+    const uint4 GA0 = lds128(aA);
+    const uint4 GA1 = lds128(aA + 512);
+    const uint4 EA = lds128(p.rb + ((qa + 1024u) & RMB));
+    uint4 GC0, GC1;
+    if (wrapC) {
+        GC0 = lds128(p.rb + ((qa + cC4 + l16) & RMB));
+        GC1 = lds128(p.rb + ((qa + cC4 + 512u + l16) & RMB));
+    } else {
+        const uint32_t aC = p.rb + qa + cC4 + l16;
+        GC0 = lds128(aC);
+        GC1 = lds128(aC + 512);
+    }
+    const uint4 EC = lds128(p.rb + ((qa + cC4 + 1024u) & RMB));
     const uint32_t nl = (p.lane + 1) & 31;
     const bool l0 = p.lane == 0;
 
@@ -226,7 +240,6 @@ __device__ __forceinline__ void full_step(const PieceCtx& p, uint32_t n, unsigne
         }
     }
 
-    const uint32_t bS = nb + 4 * S::N + l16;
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
         uint32_t r[4], o[4];
@@ -237,17 +250,28 @@ __device__ __forceinline__ void full_step(const PieceCtx& p, uint32_t n, unsigne
             ck_add<CK>(p, sum, o[c]);
         }
         if (CK) xr ^= o[0] ^ o[1] ^ o[2] ^ o[3];
-        sts128(((bS + 512 * u) & RMB) | p.rb, r[0], r[1], r[2], r[3]);
+        const uint32_t aS = wrapS ? p.rb + ((qa + cS4 + 512u * u + l16) & RMB) : p.rb + qa + cS4 + 512u * u + l16;
+        sts128(aS, r[0], r[1], r[2], r[3]);
         __stcs(reinterpret_cast<uint4*>(p.optr + n + 128 * u) + p.lane, make_uint4(o[0], o[1], o[2], o[3]));
     }
 }
 
+// Full steps from piece word n (ring phase 0) while a whole step fits before `end`.
 template <uint32_t MEXP, int RC, int KIND, bool CK>
-__device__ __forceinline__ void run_steps(const PieceCtx& p, uint32_t n, uint64_t len, unsigned long long& sum,
+__device__ __forceinline__ void run_steps(const PieceCtx& p, uint32_t n, uint64_t end, unsigned long long& sum,
                                           uint32_t& xr) {
-    for (; n + kStepWords <= len; n += kStepWords) {
-        full_step<MEXP, RC, KIND, CK>(p, n, sum, xr);
-        __syncwarp();
+    constexpr int U = (int)(Shape<MEXP>::R / kStepWords);
+    static_assert(U == 4 || U == 8, "ring period");
+    for (;;) {
+#define MTGP_STEP(Qv)                                               \
+    if (Qv < U) {                                                   \
+        if (n + kStepWords > end) return;                           \
+        full_step<MEXP, RC, KIND, CK, (Qv < U ? Qv : 0)>(p, n, sum, xr); \
+        __syncwarp();                                               \
+        n += kStepWords;                                            \
+    }
+        MTGP_STEP(0) MTGP_STEP(1) MTGP_STEP(2) MTGP_STEP(3) MTGP_STEP(4) MTGP_STEP(5) MTGP_STEP(6) MTGP_STEP(7)
+#undef MTGP_STEP
     }
 }
 
@@ -289,7 +313,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MTGP_MIN_CTAS) gen_kernel(G
         const uint32_t mis = (uint32_t)((reinterpret_cast<uintptr_t>(p.optr) >> 2) & 3u);
         const uint32_t hh = (4u - mis) & 3u;
         const uint32_t h = len < hh ? (uint32_t)len : hh;
-        p.phi = (0u - (h + S::N)) & 3u;
+        // ring phase: slot(x_h) = RA, so the aligned x_n group of every full step sits at a
+        // multiple of 256 slots and STS.128 / STG.128 are both 16-byte aligned
+        p.phi = (S::RA - h) & S::RM;
         const uint32_t* w0 = a.piece_win[pi];
         for (uint32_t j = lane; j < S::N; j += 32) sts32(p.rb + (((j + p.phi) & S::RM) << 2), w0[j]);
         __syncwarp();
