@@ -127,6 +127,14 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def traffic_per_launch(algo_bytes: float):
+    """DRAM read+write bytes of one generation launch, scaled from the committed ncu capture."""
+    f = ROOT / "profiles" / "gen_traffic.json"
+    if not f.exists():
+        return None
+    return round(json.loads(f.read_text())["traffic_over_algorithmic"] * algo_bytes)
+
+
 def cpu_reference(words_per_thread: int, threads: int):
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle_py
@@ -300,7 +308,8 @@ def main():
                        "parameter_sets": "cuRAND MTGP32-11213 (certified)" if (mexp == 11213 and rank == 0 and S <= 200)
                        else "synthetic (uncertified period)"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                         "frac": round(achieved / hbm, 4), "traffic": None,
+                         "frac": round(achieved / hbm, 4), "traffic": traffic_per_launch(bytes_per_launch),
+                         "traffic_source": "profiles/gen_traffic.json (ncu dram__bytes_read+write per algorithmic byte)",
                          "peak_source": hbm_src,
                          "kernel": "gen_kernel (v2)", "launches_timed": gen_n,
                          "avg_launch_ms": round(gen_avg_ms, 4),

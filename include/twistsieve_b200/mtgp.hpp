@@ -1,0 +1,156 @@
+// twistsieve_b200/mtgp.hpp -- C++ drop-in for the reference's generation path, MTGP32 on B200.
+//
+// Mirrors the reference's C++ API shape (the reference binds its generation path in C++, not
+// through an FFI):
+//   ParameterizedStatus + validate()         proj/include/twistsieve/params.hpp:21-42,
+//                                            proj/src/params.cpp:23-39      -> MtgpStatus
+//   WordSource::fill(std::span<uint32_t>)    proj/include/twistsieve/word_source.hpp:21-25
+//                                                                           -> GpuWordSource
+//   make_word_source(params, seed)           word_source.hpp:75-76, word_source.cpp:5-16
+//   Generator::next_u32 / next_f64_01        generator.hpp:33-41             -> GpuWordSource
+//   StatusRecord / read_status_file / status_from_line / status_to_json_line
+//                                            proj/include/twistsieve/status_io.hpp:13-27
+//   splitmix64 / derive_seed                 word_source.cpp:18-27
+// Error behaviour follows the reference: std::invalid_argument for invalid parameters or
+// arguments, std::runtime_error for everything else (CUDA failures, I/O) -- translated from
+// the C-ABI's status codes (include/mtgp_b200.h).
+//
+// WordSource: by default this header declares a WordSource with the reference's exact virtual
+// interface. Define TWISTSIEVE_B200_WITH_REFERENCE before including it (and put the reference's
+// include/ directory on the include path) to derive from twistsieve::WordSource itself, so a
+// GpuWordSource plugs into BufferedStream and the sieve unchanged.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <filesystem>
+#include <memory>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "mtgp_b200.h"
+
+#ifdef TWISTSIEVE_B200_WITH_REFERENCE
+#include "twistsieve/word_source.hpp"
+#endif
+
+namespace twistsieve_b200 {
+
+#ifdef TWISTSIEVE_B200_WITH_REFERENCE
+using WordSource = twistsieve::WordSource;
+#else
+/// Campaign-facing word producer (same virtual interface as proj/include/twistsieve/word_source.hpp:21-25).
+class WordSource {
+public:
+    virtual ~WordSource() = default;
+    virtual void fill(std::span<std::uint32_t> out) = 0;
+};
+#endif
+
+/// Output conversions of one MTGP32 stream.
+enum class OutputKind { u32 = MTGP_U32, f32_12 = MTGP_F32_12, f32_01oc = MTGP_F32_01OC };
+
+/// One MTGP32 parameter set -- the Engine::mtgp32 counterpart of ParameterizedStatus.
+struct MtgpStatus {
+    std::uint32_t id = 0;
+    std::uint32_t mexp = 0;
+    std::uint32_t pos = 0;
+    std::uint32_t sh1 = 0;
+    std::uint32_t sh2 = 0;
+    std::uint32_t mask = 0;
+    std::uint32_t tbl[16] = {};
+    std::uint32_t tmp_tbl[16] = {};
+    std::uint32_t flt_tmp_tbl[16] = {};
+    std::string poly_sha1;  // hex SHA-1 of the characteristic polynomial (cuRAND table), may be empty
+    bool certified = false; // full period certified by the table's authors
+
+    std::uint32_t n() const { return mexp / 32 + 1; }
+    /// Throws std::invalid_argument on any violated invariant (mtgp_validate_params).
+    void validate() const;
+    mtgp_params to_c() const;
+    bool operator==(const MtgpStatus&) const = default;
+};
+
+/// Stable identifier for reports, e.g. "mtgp11213-id7" (cf. status_display_id, params.hpp:45).
+std::string status_display_id(const MtgpStatus& p);
+
+/// The 200 certified MTGP32-11213 sets shipped with the CUDA toolkit
+/// (curand_mtgp32dc_p_11213.h), read from `header` or from $CUDA_HOME/include.
+std::vector<MtgpStatus> curand_mtgp32_11213(const std::string& header = "");
+
+/// Deterministic MTGP-shaped set #idx for `mexp` with UNCERTIFIED period;
+/// identical to paper_1501_07701_b200.tables.synthetic_set.
+MtgpStatus synthetic_status(std::uint32_t mexp, std::uint32_t idx, std::uint64_t family_seed = 0x4D544750ull);
+
+// ---- parameter-set table file (extends proj/src/status_io.cpp:15-141) ----
+struct StatusRecord {
+    MtgpStatus status;
+    std::optional<std::uint32_t> seed;
+};
+std::string status_to_json_line(const StatusRecord& rec);
+StatusRecord status_from_line(const std::string& line);  // JSON or key=value; validates
+std::vector<StatusRecord> read_status_file(const std::filesystem::path& path);
+void write_status_file(const std::filesystem::path& path, const std::vector<StatusRecord>& records);
+
+// ---- seeds (proj/src/word_source.cpp:18-27) ----
+std::uint64_t splitmix64(std::uint64_t x);
+std::uint32_t derive_seed(std::uint64_t source, std::uint32_t j);
+
+/// RAII owner of a C-ABI context: many independent streams on one GPU.
+class StreamBatch {
+public:
+    StreamBatch(const std::vector<MtgpStatus>& sets, const std::vector<std::uint32_t>& seeds, int device = 0);
+    ~StreamBatch();
+    StreamBatch(const StreamBatch&) = delete;
+    StreamBatch& operator=(const StreamBatch&) = delete;
+    StreamBatch(StreamBatch&&) noexcept;
+    StreamBatch& operator=(StreamBatch&&) noexcept;
+
+    std::uint32_t size() const { return n_sets_; }
+    std::uint32_t state_words() const { return n_; }
+    /// words_per_stream outputs of every stream into host memory out[s*L + j] (s-major).
+    void generate_host(OutputKind kind, void* out, std::uint64_t words_per_stream);
+    /// same into device memory (asynchronous on the context stream).
+    void generate_device(OutputKind kind, void* device_out, std::uint64_t words_per_stream);
+    void skip(std::uint64_t words);
+    std::uint64_t position(std::uint32_t s) const;
+    std::vector<mtgp_cksum> checksums() const;
+    void set_option(int option, std::int64_t value);
+    void synchronize();
+    mtgp_ctx* handle() { return ctx_; }
+
+private:
+    mtgp_ctx* ctx_ = nullptr;
+    std::uint32_t n_sets_ = 0, n_ = 0;
+};
+
+/// One MTGP32 stream served from device-generated chunks -- the GPU counterpart of
+/// MtWordSource (word_source.hpp:27-37): fill() returns the next words of the stream exactly
+/// as successive next_u32() calls would.
+class GpuWordSource final : public WordSource {
+public:
+    /// kind != u32 makes fill() return the stream's single-float bit patterns instead.
+    GpuWordSource(const MtgpStatus& params, std::uint32_t seed, OutputKind kind = OutputKind::u32,
+                  int device = 0, std::size_t chunk_words = std::size_t{1} << 20);
+    void fill(std::span<std::uint32_t> out) override;
+    std::uint32_t next_u32();
+    /// next_u32() / 2^32 in [0, 1), draw for draw (generator.hpp:39-41).
+    double next_f64_01() { return static_cast<double>(next_u32()) * (1.0 / 4294967296.0); }
+    std::uint64_t position() const { return consumed_; }
+
+private:
+    void refill();
+    StreamBatch batch_;
+    OutputKind kind_;
+    std::vector<std::uint32_t> buf_;
+    std::size_t pos_ = 0, len_ = 0;
+    std::uint64_t consumed_ = 0;
+};
+
+/// Factory with the reference's shape (word_source.cpp:5-16).
+std::unique_ptr<WordSource> make_word_source(const MtgpStatus& params, std::uint32_t seed);
+
+}  // namespace twistsieve_b200

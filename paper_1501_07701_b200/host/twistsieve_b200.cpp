@@ -1,0 +1,507 @@
+// twistsieve_b200.cpp -- implementation of include/twistsieve_b200/mtgp.hpp over the C-ABI.
+#include "twistsieve_b200/mtgp.hpp"
+
+#include <algorithm>
+#include <cctype>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <sstream>
+
+namespace twistsieve_b200 {
+
+namespace {
+
+// C-ABI status -> the reference's exception types (std::invalid_argument for bad input,
+// std::runtime_error otherwise; proj/src/params.cpp:23-39, proj/src/cli.cpp:429-435).
+void check(int rc, const char* what) {
+    if (rc == MTGP_OK) return;
+    std::string msg = std::string(what) + ": " + mtgp_last_error();
+    if (rc == MTGP_EINVAL) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+}
+
+constexpr std::uint32_t kMask32 = 0xFFFFFFFFu;
+
+std::uint32_t state_mask(std::uint32_t mexp) {
+    const std::uint32_t r = 32 * (mexp / 32 + 1) - mexp;
+    return r ? (kMask32 << r) : kMask32;
+}
+
+void linear_tables(const std::uint32_t bt[4], const std::uint32_t bm[4], MtgpStatus& p) {
+    for (int i = 0; i < 16; ++i) {
+        std::uint32_t t = 0, m = 0;
+        for (int b = 0; b < 4; ++b)
+            if (i >> b & 1) {
+                t ^= bt[b];
+                m ^= bm[b];
+            }
+        p.tbl[i] = t;
+        p.tmp_tbl[i] = m;
+        p.flt_tmp_tbl[i] = (m >> 9) | 0x3F800000u;
+    }
+}
+
+// ---------------- minimal flat JSON (numbers, strings, bools, arrays of numbers) ----------------
+struct JVal {
+    enum Kind { num, str, boolean, arr } kind = num;
+    std::uint64_t n = 0;
+    std::string s;
+    bool b = false;
+    std::vector<std::uint64_t> a;
+};
+
+struct JParser {
+    const std::string& t;
+    std::size_t i = 0;
+    explicit JParser(const std::string& s) : t(s) {}
+    [[noreturn]] void bad(const char* why) {
+        throw std::invalid_argument(std::string("bad status JSON (") + why + ") at offset " + std::to_string(i));
+    }
+    void ws() {
+        while (i < t.size() && std::isspace(static_cast<unsigned char>(t[i]))) ++i;
+    }
+    char peek() {
+        ws();
+        return i < t.size() ? t[i] : '\0';
+    }
+    void expect(char c) {
+        if (peek() != c) bad("unexpected character");
+        ++i;
+    }
+    std::string str() {
+        expect('"');
+        std::string out;
+        while (i < t.size() && t[i] != '"') {
+            if (t[i] == '\\' && i + 1 < t.size()) ++i;
+            out += t[i++];
+        }
+        if (i >= t.size()) bad("unterminated string");
+        ++i;
+        return out;
+    }
+    std::uint64_t number() {
+        ws();
+        std::size_t j = i;
+        while (j < t.size() && (std::isdigit(static_cast<unsigned char>(t[j])))) ++j;
+        if (j == i) bad("number expected");
+        const std::uint64_t v = std::stoull(t.substr(i, j - i));
+        i = j;
+        return v;
+    }
+    JVal value() {
+        JVal v;
+        const char c = peek();
+        if (c == '"') {
+            v.kind = JVal::str;
+            v.s = str();
+        } else if (c == '[') {
+            v.kind = JVal::arr;
+            ++i;
+            if (peek() == ']') {
+                ++i;
+                return v;
+            }
+            for (;;) {
+                v.a.push_back(number());
+                if (peek() == ',') {
+                    ++i;
+                    continue;
+                }
+                expect(']');
+                break;
+            }
+        } else if (t.compare(i, 4, "true") == 0) {
+            v.kind = JVal::boolean;
+            v.b = true;
+            i += 4;
+        } else if (t.compare(i, 5, "false") == 0) {
+            v.kind = JVal::boolean;
+            i += 5;
+        } else {
+            v.n = number();
+        }
+        return v;
+    }
+    std::map<std::string, JVal> object() {
+        std::map<std::string, JVal> m;
+        expect('{');
+        if (peek() == '}') {
+            ++i;
+            return m;
+        }
+        for (;;) {
+            const std::string k = str();
+            expect(':');
+            m[k] = value();
+            if (peek() == ',') {
+                ++i;
+                continue;
+            }
+            expect('}');
+            break;
+        }
+        return m;
+    }
+};
+
+std::uint64_t parse_uint(const std::string& v) {
+    std::size_t used = 0;
+    const std::uint64_t out = std::stoull(v, &used, 0);  // base 0: 0x accepted (status_io.cpp:36-41)
+    if (used != v.size()) throw std::invalid_argument("bad numeric value: " + v);
+    return out;
+}
+
+std::vector<std::uint64_t> parse_list(const std::string& v) {
+    std::vector<std::uint64_t> out;
+    std::stringstream ss(v);
+    std::string item;
+    while (std::getline(ss, item, ',')) out.push_back(parse_uint(item));
+    return out;
+}
+
+void copy16(std::uint32_t* dst, const std::vector<std::uint64_t>& src, const char* name) {
+    if (src.size() != 16) throw std::invalid_argument(std::string(name) + " must have 16 entries");
+    for (int i = 0; i < 16; ++i) dst[i] = static_cast<std::uint32_t>(src[i]);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+void MtgpStatus::validate() const {
+    const mtgp_params c = to_c();
+    check(mtgp_validate_params(&c), "invalid MTGP32 status");
+}
+
+mtgp_params MtgpStatus::to_c() const {
+    mtgp_params c{};
+    c.mexp = mexp;
+    c.pos = pos;
+    c.sh1 = sh1;
+    c.sh2 = sh2;
+    c.mask = mask;
+    std::memcpy(c.tbl, tbl, sizeof(tbl));
+    std::memcpy(c.tmp_tbl, tmp_tbl, sizeof(tmp_tbl));
+    std::memcpy(c.flt_tmp_tbl, flt_tmp_tbl, sizeof(flt_tmp_tbl));
+    return c;
+}
+
+std::string status_display_id(const MtgpStatus& p) {
+    return "mtgp" + std::to_string(p.mexp) + "-id" + std::to_string(p.id);
+}
+
+std::vector<MtgpStatus> curand_mtgp32_11213(const std::string& header) {
+    std::string path = header;
+    if (path.empty()) {
+        for (const char* env : {"CUDA_HOME", "CUDA_PATH"}) {
+            const char* v = std::getenv(env);
+            if (v && *v) {
+                path = std::string(v) + "/include/curand_mtgp32dc_p_11213.h";
+                if (std::ifstream(path)) break;
+                path.clear();
+            }
+        }
+        if (path.empty()) path = "/usr/local/cuda/include/curand_mtgp32dc_p_11213.h";
+    }
+    std::ifstream in(path);
+    if (!in) throw std::runtime_error("cannot open " + path);
+    std::stringstream ss;
+    ss << in.rdbuf();
+    const std::string text = ss.str();
+    std::size_t i = text.find("mtgp32dc_params_fast_11213[]");
+    if (i == std::string::npos) throw std::runtime_error("no MTGP32 table in " + path);
+    // numbers of the initializer list, skipping comments (which hold "No.k delta:.. weight:..")
+    std::vector<std::uint64_t> nums;
+    const std::size_t end = text.find("};", i);
+    i = text.find('{', i);
+    while (i < end) {
+        if (text.compare(i, 2, "/*") == 0) {
+            i = text.find("*/", i) + 2;
+            continue;
+        }
+        if (std::isdigit(static_cast<unsigned char>(text[i]))) {
+            std::size_t used = 0;
+            nums.push_back(std::stoull(text.substr(i, 24), &used, 0));
+            i += used;
+            continue;
+        }
+        ++i;
+    }
+    constexpr std::size_t kRec = 4 + 48 + 1 + 21;
+    if (nums.size() != 200 * kRec) throw std::runtime_error("unexpected MTGP32 table layout in " + path);
+    std::vector<MtgpStatus> out(200);
+    for (std::size_t k = 0; k < 200; ++k) {
+        const std::uint64_t* v = nums.data() + k * kRec;
+        MtgpStatus& p = out[k];
+        p.id = static_cast<std::uint32_t>(k);
+        p.mexp = static_cast<std::uint32_t>(v[0]);
+        p.pos = static_cast<std::uint32_t>(v[1]);
+        p.sh1 = static_cast<std::uint32_t>(v[2]);
+        p.sh2 = static_cast<std::uint32_t>(v[3]);
+        for (int j = 0; j < 16; ++j) {
+            p.tbl[j] = static_cast<std::uint32_t>(v[4 + j]);
+            p.tmp_tbl[j] = static_cast<std::uint32_t>(v[20 + j]);
+            p.flt_tmp_tbl[j] = static_cast<std::uint32_t>(v[36 + j]);
+        }
+        p.mask = static_cast<std::uint32_t>(v[52]);
+        static const char* hex = "0123456789abcdef";
+        for (int j = 0; j < 20; ++j) {
+            p.poly_sha1 += hex[(v[53 + j] >> 4) & 15];
+            p.poly_sha1 += hex[v[53 + j] & 15];
+        }
+        p.certified = true;
+    }
+    return out;
+}
+
+MtgpStatus synthetic_status(std::uint32_t mexp, std::uint32_t idx, std::uint64_t family_seed) {
+    MtgpStatus p;
+    p.id = idx;
+    p.mexp = mexp;
+    const std::uint32_t n = mexp / 32 + 1;
+    const std::uint32_t team = mexp == 11213 ? 256 : mexp == 23209 ? 512 : mexp == 44497 ? 1024 : 256;
+    std::uint64_t ctr = splitmix64(family_seed) ^ (static_cast<std::uint64_t>(mexp) << 32) ^
+                        (static_cast<std::uint64_t>(idx) * 0x100000001B3ull);
+    auto draw = [&] { return splitmix64(++ctr); };
+    const std::uint32_t pos_max = std::max<std::uint32_t>(3, n > team ? n - team : 0);
+    p.pos = 3 + static_cast<std::uint32_t>(draw() % (pos_max - 3 + 1));
+    p.sh1 = 1 + static_cast<std::uint32_t>(draw() % 30);
+    p.sh2 = 1 + static_cast<std::uint32_t>(draw() % 19);
+    std::uint32_t bt[4], bm[4];
+    for (auto& b : bt) b = static_cast<std::uint32_t>(draw() & kMask32);
+    for (auto& b : bm) b = static_cast<std::uint32_t>(draw() & kMask32);
+    linear_tables(bt, bm, p);
+    p.mask = state_mask(mexp);
+    p.certified = false;
+    return p;
+}
+
+// ---------------------------------------------------------------------------------------------
+std::string status_to_json_line(const StatusRecord& rec) {
+    const MtgpStatus& p = rec.status;
+    std::ostringstream o;
+    auto arr = [&](const std::uint32_t* v) {
+        o << '[';
+        for (int i = 0; i < 16; ++i) o << (i ? "," : "") << v[i];
+        o << ']';
+    };
+    o << "{\"id\":" << p.id << ",\"engine\":\"mtgp32\",\"mexp\":" << p.mexp << ",\"pos\":" << p.pos
+      << ",\"sh1\":" << p.sh1 << ",\"sh2\":" << p.sh2 << ",\"mask\":" << p.mask << ",\"tbl\":";
+    arr(p.tbl);
+    o << ",\"tmp_tbl\":";
+    arr(p.tmp_tbl);
+    o << ",\"flt_tmp_tbl\":";
+    arr(p.flt_tmp_tbl);
+    o << ",\"poly_sha1\":\"" << p.poly_sha1 << "\",\"certified\":" << (p.certified ? "true" : "false");
+    if (rec.seed) o << ",\"seed\":" << *rec.seed;
+    o << '}';
+    return o.str();
+}
+
+StatusRecord status_from_line(const std::string& line) {
+    StatusRecord rec;
+    MtgpStatus& p = rec.status;
+    const auto first = line.find_first_not_of(" \t");
+    bool have_flt = false, have_mask = false;
+    if (first != std::string::npos && line[first] == '{') {
+        JParser jp(line);
+        jp.i = first;
+        auto m = jp.object();
+        auto need = [&](const char* k) -> JVal& {
+            auto it = m.find(k);
+            if (it == m.end()) throw std::invalid_argument(std::string("missing status field: ") + k);
+            return it->second;
+        };
+        if (m.count("engine") && m["engine"].s != "mtgp32")
+            throw std::invalid_argument("not an mtgp32 status: engine=" + m["engine"].s);
+        p.id = m.count("id") ? static_cast<std::uint32_t>(m["id"].n) : 0;
+        p.mexp = static_cast<std::uint32_t>(need("mexp").n);
+        p.pos = static_cast<std::uint32_t>(need("pos").n);
+        p.sh1 = static_cast<std::uint32_t>(need("sh1").n);
+        p.sh2 = static_cast<std::uint32_t>(need("sh2").n);
+        copy16(p.tbl, need("tbl").a, "tbl");
+        copy16(p.tmp_tbl, need("tmp_tbl").a, "tmp_tbl");
+        if (m.count("flt_tmp_tbl")) {
+            copy16(p.flt_tmp_tbl, m["flt_tmp_tbl"].a, "flt_tmp_tbl");
+            have_flt = true;
+        }
+        if (m.count("mask")) {
+            p.mask = static_cast<std::uint32_t>(m["mask"].n);
+            have_mask = true;
+        }
+        if (m.count("poly_sha1")) p.poly_sha1 = m["poly_sha1"].s;
+        if (m.count("certified")) p.certified = m["certified"].b;
+        if (m.count("seed")) rec.seed = static_cast<std::uint32_t>(m["seed"].n);
+    } else {
+        std::istringstream in(line);
+        std::string token;
+        while (in >> token) {
+            const auto eq = token.find('=');
+            if (eq == std::string::npos) throw std::invalid_argument("expected key=value, got: " + token);
+            const std::string key = token.substr(0, eq), value = token.substr(eq + 1);
+            if (key == "id") p.id = static_cast<std::uint32_t>(parse_uint(value));
+            else if (key == "engine") {
+                if (value != "mtgp32") throw std::invalid_argument("not an mtgp32 status: engine=" + value);
+            } else if (key == "mexp") p.mexp = static_cast<std::uint32_t>(parse_uint(value));
+            else if (key == "pos") p.pos = static_cast<std::uint32_t>(parse_uint(value));
+            else if (key == "sh1") p.sh1 = static_cast<std::uint32_t>(parse_uint(value));
+            else if (key == "sh2") p.sh2 = static_cast<std::uint32_t>(parse_uint(value));
+            else if (key == "mask") {
+                p.mask = static_cast<std::uint32_t>(parse_uint(value));
+                have_mask = true;
+            } else if (key == "tbl") copy16(p.tbl, parse_list(value), "tbl");
+            else if (key == "tmp_tbl") copy16(p.tmp_tbl, parse_list(value), "tmp_tbl");
+            else if (key == "flt_tmp_tbl") {
+                copy16(p.flt_tmp_tbl, parse_list(value), "flt_tmp_tbl");
+                have_flt = true;
+            } else if (key == "poly_sha1") p.poly_sha1 = value;
+            else if (key == "certified") p.certified = value == "1" || value == "true" || value == "yes";
+            else if (key == "seed") rec.seed = static_cast<std::uint32_t>(parse_uint(value));
+            else throw std::invalid_argument("unknown status field: " + key);
+        }
+    }
+    if (!have_flt)
+        for (int i = 0; i < 16; ++i) p.flt_tmp_tbl[i] = (p.tmp_tbl[i] >> 9) | 0x3F800000u;
+    if (!have_mask) p.mask = state_mask(p.mexp);
+    p.validate();
+    return rec;
+}
+
+std::vector<StatusRecord> read_status_file(const std::filesystem::path& path) {
+    std::ifstream in(path);
+    if (!in) throw std::runtime_error("cannot open status file: " + path.string());
+    std::vector<StatusRecord> out;
+    std::string line;
+    std::size_t lineno = 0;
+    while (std::getline(in, line)) {
+        ++lineno;
+        const auto first = line.find_first_not_of(" \t\r");
+        if (first == std::string::npos || line[first] == '#') continue;
+        try {
+            out.push_back(status_from_line(line));
+        } catch (const std::exception& e) {
+            throw std::runtime_error(path.string() + ":" + std::to_string(lineno) + ": " + e.what());
+        }
+    }
+    return out;
+}
+
+void write_status_file(const std::filesystem::path& path, const std::vector<StatusRecord>& records) {
+    std::ofstream out(path);
+    if (!out) throw std::runtime_error("cannot write status file: " + path.string());
+    for (const auto& rec : records) out << status_to_json_line(rec) << '\n';
+    if (!out) throw std::runtime_error("write failed: " + path.string());
+}
+
+std::uint64_t splitmix64(std::uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+std::uint32_t derive_seed(std::uint64_t source, std::uint32_t j) {
+    return static_cast<std::uint32_t>(splitmix64(source + j));
+}
+
+// ---------------------------------------------------------------------------------------------
+StreamBatch::StreamBatch(const std::vector<MtgpStatus>& sets, const std::vector<std::uint32_t>& seeds, int device) {
+    if (sets.empty()) throw std::invalid_argument("no parameter sets");
+    if (sets.size() != seeds.size()) throw std::invalid_argument("one seed per parameter set");
+    std::vector<mtgp_params> c;
+    c.reserve(sets.size());
+    for (const auto& s : sets) c.push_back(s.to_c());
+    check(mtgp_ctx_create(&ctx_, device, c.data(), static_cast<std::uint32_t>(c.size()), seeds.data(), nullptr),
+          "mtgp_ctx_create");
+    check(mtgp_ctx_info(ctx_, &n_sets_, &n_, nullptr), "mtgp_ctx_info");
+}
+
+StreamBatch::~StreamBatch() {
+    if (ctx_) mtgp_ctx_destroy(ctx_);
+}
+
+StreamBatch::StreamBatch(StreamBatch&& o) noexcept : ctx_(o.ctx_), n_sets_(o.n_sets_), n_(o.n_) { o.ctx_ = nullptr; }
+
+StreamBatch& StreamBatch::operator=(StreamBatch&& o) noexcept {
+    if (this != &o) {
+        if (ctx_) mtgp_ctx_destroy(ctx_);
+        ctx_ = o.ctx_;
+        n_sets_ = o.n_sets_;
+        n_ = o.n_;
+        o.ctx_ = nullptr;
+    }
+    return *this;
+}
+
+void StreamBatch::generate_host(OutputKind kind, void* out, std::uint64_t words) {
+    check(mtgp_generate(ctx_, static_cast<int>(kind), out, words, 0), "mtgp_generate");
+}
+
+void StreamBatch::generate_device(OutputKind kind, void* out, std::uint64_t words) {
+    check(mtgp_generate(ctx_, static_cast<int>(kind), out, words, 1), "mtgp_generate");
+}
+
+void StreamBatch::skip(std::uint64_t words) { check(mtgp_skip(ctx_, words), "mtgp_skip"); }
+
+std::uint64_t StreamBatch::position(std::uint32_t s) const {
+    std::uint64_t v = 0;
+    check(mtgp_position(ctx_, s, &v), "mtgp_position");
+    return v;
+}
+
+std::vector<mtgp_cksum> StreamBatch::checksums() const {
+    std::vector<mtgp_cksum> v(n_sets_);
+    check(mtgp_checksums(ctx_, v.data()), "mtgp_checksums");
+    return v;
+}
+
+void StreamBatch::set_option(int option, std::int64_t value) {
+    check(mtgp_set_option(ctx_, option, value), "mtgp_set_option");
+}
+
+void StreamBatch::synchronize() { check(mtgp_sync(ctx_), "mtgp_sync"); }
+
+// ---------------------------------------------------------------------------------------------
+GpuWordSource::GpuWordSource(const MtgpStatus& params, std::uint32_t seed, OutputKind kind, int device,
+                             std::size_t chunk_words)
+    : batch_({params}, {seed}, device), kind_(kind), buf_(std::max<std::size_t>(chunk_words, 256)) {}
+
+void GpuWordSource::refill() {
+    batch_.generate_host(kind_, buf_.data(), buf_.size());
+    pos_ = 0;
+    len_ = buf_.size();
+}
+
+void GpuWordSource::fill(std::span<std::uint32_t> out) {
+    std::size_t done = 0;
+    while (done < out.size()) {
+        if (pos_ == len_) {
+            const std::size_t rest = out.size() - done;
+            if (rest >= buf_.size()) {
+                // large request: generate straight into the caller's span
+                batch_.generate_host(kind_, out.data() + done, rest);
+                done += rest;
+                break;
+            }
+            refill();
+        }
+        const std::size_t n = std::min(len_ - pos_, out.size() - done);
+        std::memcpy(out.data() + done, buf_.data() + pos_, n * sizeof(std::uint32_t));
+        pos_ += n;
+        done += n;
+    }
+    consumed_ += out.size();
+}
+
+std::uint32_t GpuWordSource::next_u32() {
+    if (pos_ == len_) refill();
+    ++consumed_;
+    return buf_[pos_++];
+}
+
+std::unique_ptr<WordSource> make_word_source(const MtgpStatus& params, std::uint32_t seed) {
+    return std::make_unique<GpuWordSource>(params, seed);
+}
+
+}  // namespace twistsieve_b200

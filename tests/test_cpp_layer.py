@@ -1,0 +1,62 @@
+"""Build and run the C++ drop-in layer's tests (tests/cpp/test_twistsieve_b200.cpp) and the
+jump-ahead algebra test (tests/cpp/test_gf2.cpp)."""
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from paper_1501_07701_b200 import tables
+
+ROOT = Path(__file__).resolve().parents[1]
+PKG = ROOT / "paper_1501_07701_b200"
+
+
+def _build(tmp_path, name, srcs, extra=()):
+    exe = tmp_path / name
+    cmd = ["g++", "-std=c++20", "-O2", "-I", str(ROOT / "include"), "-I", str(PKG / "csrc"), "-I", str(ROOT / "oracle"),
+           *map(str, srcs), *extra, "-o", str(exe)]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return exe
+
+
+@pytest.fixture(scope="module")
+def layer_exe(tmp_path_factory):
+    d = tmp_path_factory.mktemp("cpp")
+    return _build(d, "test_twistsieve_b200", [ROOT / "tests/cpp/test_twistsieve_b200.cpp"],
+                  ["-L", str(PKG), "-ltwistsieve_b200", "-lmtgp_b200", f"-Wl,-rpath,{PKG}"])
+
+
+def _pyfile(tmp_path):
+    f = tmp_path / "py_sets.jsonl"
+    tables.write_status_file(f, [tables.load_curand_11213()[0], tables.synthetic_set(23209, 1)])
+    return f
+
+
+def test_cpp_layer_cpu(layer_exe, tmp_path):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("the no-device case is for CPU hosts; GPU hosts run test_cpp_layer_gpu")
+    r = subprocess.run([str(layer_exe), str(ROOT / "tests/golden/mtgp32_11213_curand.json"), "--cpu",
+                        str(_pyfile(tmp_path))], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_layer_gpu(layer_exe, tmp_path):
+    r = subprocess.run([str(layer_exe), str(ROOT / "tests/golden/mtgp32_11213_curand.json"), "--gpu",
+                        str(_pyfile(tmp_path))], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_gf2_jump_algebra(tmp_path):
+    """BM charpoly, Barrett x^o mod P, and jumped windows vs the oracle (certified + synthetic)."""
+    exe = _build(tmp_path, "test_gf2", [ROOT / "tests/cpp/test_gf2.cpp", PKG / "csrc/gf2.cpp"],
+                 ["-mpclmul", "-msse4.1", "-x", "c", str(ROOT / "oracle/mtgp32_oracle.c"),
+                  str(ROOT / "oracle/mt_oracle.c"), "-x", "none", "-lpthread"])
+    sets = tables.load_curand_11213()[:2] + tables.synthetic_sets(44497, 1)
+    pf = tmp_path / "params.txt"
+    pf.write_text("".join(" ".join(str(v) for v in [p.mexp, p.pos, p.sh1, p.sh2, *p.tbl, *p.tmp_tbl, p.mask]) + "\n"
+                          for p in sets))
+    r = subprocess.run([str(exe), str(pf)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "BM degree 11213" in r.stdout
