@@ -181,14 +181,14 @@ def main():
 
     import torch
     import torch.distributed as dist
-    from paper_1501_07701_b200 import mtgp, tables
+    from paper_1501_07701_b200 import mtgp, shard, tables
 
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     mexp, kind, L_step, label = CONFIGS[args.config]
     S = args.sets
-    sets = tables.sets_for(mexp, S, first=rank * S)
+    sets = shard.sets_for_rank(mexp, S, rank)
     seeds = [1] * S
     calls = max(1, args.calls)
     Lc = L_step // calls
@@ -246,11 +246,9 @@ def main():
         t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        # per-stream checksum gather (NCCL; the only inter-GPU traffic)
-        ck = torch.tensor([[c[0] & 0x7FFFFFFFFFFFFFFF, c[1], c[2]] for c in ctx.checksums()],
-                          device=f"cuda:{local}", dtype=torch.int64)
-        allck = [torch.empty_like(ck) for _ in range(world)]
-        dist.all_gather(allck, ck)
+    # per-stream checksum gather (NCCL all_gather; the only inter-GPU traffic)
+    allck = shard.gather_checksums(ctx.checksums(), device=f"cuda:{local}")
+    gathered_streams = len(allck)
 
     samples_rank = S * L_step * args.steps
     total = samples_rank * world
@@ -304,6 +302,7 @@ def main():
             "config": {"workload": label, "sets_per_gpu": S, "seed": 1, "words_per_set_per_step": L_step,
                        "calls_per_step": calls, "kernel": f"v{kver}", "pieces_per_call": pieces,
                        "checksums_fused": not args.no_checksum,
+                       "checksums_gathered_streams": gathered_streams,
                        "l2": "output 4*S*L/calls bytes per call >> 126 MB L2; no flush needed",
                        "parameter_sets": "cuRAND MTGP32-11213 (certified)" if (mexp == 11213 and rank == 0 and S <= 200)
                        else "synthetic (uncertified period)"},

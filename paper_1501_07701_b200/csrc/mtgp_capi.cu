@@ -249,7 +249,7 @@ int mtgp_set_option(mtgp_ctx* ctx, int option, int64_t value) {
     switch (option) {
         case MTGP_OPT_CHECKSUM: ctx->cksum = value != 0; return MTGP_OK;
         case MTGP_OPT_KERNEL:
-            if (value < 0 || value > 2) return fail(MTGP_EINVAL, "kernel must be 0, 1 or 2");
+            if (value < 0 || value > 3) return fail(MTGP_EINVAL, "kernel must be 0 (auto), 1, 2 or 3");
             ctx->kernel = (int)value;
             return MTGP_OK;
         case MTGP_OPT_MAX_PIECES:
@@ -304,6 +304,7 @@ int generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
         run.max_pieces = ctx->max_pieces;
         run.min_piece_words = ctx->min_piece_words;
         run.timing = ctx->timing ? &ctx->pool : nullptr;
+        run.want_kernel = ctx->kernel;
         std::string err;
         cudaError_t e = ctx->planner->run(run, err);
         if (e != cudaSuccess) return fail(e == cudaErrorMemoryAllocation ? MTGP_ENOMEM : MTGP_ECUDA, "v2 generation: %s (%s)", err.c_str(), cudaGetErrorString(e));
@@ -311,7 +312,7 @@ int generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
         ctx->total_launches += run.launches;
         ctx->last_pieces = run.pieces;
         ctx->last_warps = run.warps_per_piece;
-        ctx->last_kernel = 2;
+        ctx->last_kernel = (uint32_t)run.version;
     }
     for (auto& p : ctx->position) p += L;
     return MTGP_OK;

@@ -322,9 +322,17 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         err = "v2 kernel does not support this parameter shape";
         return cudaSuccess;
     }
-    const int cps = gen_ctas_per_sm(I.M, r.kind, r.cksum);
+    // v3 (register-resident ring) serves MTGP32-11213 when every piece starts 16-byte aligned:
+    // 16-byte aligned output, L % 4 == 0 (piece offsets are multiples of 4 by construction)
+    const bool v3_ok = I.M == 11213 && r.L % 4 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 15) == 0;
+    if (r.want_kernel == 3 && !v3_ok) {
+        err = "kernel v3 needs mexp 11213, words_per_stream % 4 == 0 and 16-byte aligned output";
+        return cudaSuccess;
+    }
+    const bool use_v3 = v3_ok && r.want_kernel != 2;
+    const int cps = use_v3 ? gen3_ctas_per_sm(r.kind, r.cksum) : gen_ctas_per_sm(I.M, r.kind, r.cksum);
     if (cps <= 0) {
-        err = "v2 kernel cannot be resident";
+        err = "generation kernel cannot be resident";
         return cudaSuccess;
     }
     uint32_t T = (uint32_t)(cps * kWarpsPerCta * I.num_sms);
@@ -383,7 +391,10 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     ga.L = r.L;
     ga.ck = r.ck;
     if (r.timing) r.timing->record(r.stream, &g0);
-    if ((e = launch_gen(I.M, r.kind, r.cksum, ga, r.stream)) != cudaSuccess) return e;
+    if ((e = use_v3 ? launch_gen3(r.kind, r.cksum, ga, r.stream) : launch_gen(I.M, r.kind, r.cksum, ga, r.stream)) !=
+        cudaSuccess)
+        return e;
+    r.version = use_v3 ? 3 : 2;
     if (r.timing) {
         r.timing->record(r.stream, &g1);
         r.timing->gen.push_back({g0, g1});

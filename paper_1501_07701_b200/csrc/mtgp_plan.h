@@ -25,6 +25,8 @@ struct PlanRun {
     uint32_t max_pieces = 0;
     uint64_t min_piece_words = 1ull << 21;
     EventPool* timing = nullptr;  // non-null: record event pairs around the launches
+    int want_kernel = 0;          // 0 auto, 2 force v2, 3 force v3
+    int version = 0;              // kernel that ran
     // results
     uint64_t launches = 0;        // kernels launched by this call
     uint32_t pieces = 0, warps_per_piece = 0;

@@ -47,5 +47,8 @@ cudaError_t launch_prefix(const DevParams* params, const uint32_t* win, const ui
 cudaError_t launch_jump(uint32_t mexp, const JumpArgs& a, uint32_t n_jump_sets, cudaStream_t st);
 cudaError_t launch_gen(uint32_t mexp, int kind, bool cksum, const GenArgs& a, cudaStream_t st);
 int gen_ctas_per_sm(uint32_t mexp, int kind, bool cksum);
+// v3: register-resident ring, MTGP32-11213 only (mtgp_v3.cu)
+cudaError_t launch_gen3(int kind, bool cksum, const GenArgs& a, cudaStream_t st);
+int gen3_ctas_per_sm(int kind, bool cksum);
 
 }  // namespace mtgpb

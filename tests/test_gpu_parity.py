@@ -199,3 +199,45 @@ def test_v2_long_streams_full_compare(curand_sets):
     assert pieces >= 256
     ref, _ = oracle_py.mtgp_bulk(sets, seeds, L, threads=8)
     assert np.array_equal(got, ref)
+
+
+# ---------------- v3: register-resident ring (MTGP32-11213) ----------------
+
+@pytest.mark.parametrize("kind", [mtgp.U32, mtgp.F32_12, mtgp.F32_01OC])
+def test_v3_bit_exact_with_jumps(curand_sets, kind):
+    sets = curand_sets[60:68]
+    seeds = list(range(70, 78))
+    L = 123456  # multiple of 4
+    with _ctx(sets, seeds, 3, {mtgp.OPT_MIN_PIECE_WORDS: 2000}) as ctx:
+        w1 = ctx.generate_host(kind, L)
+        pieces, _, kv = ctx.last_plan()
+        assert kv == 3 and pieces > 8 * 20
+        w2 = ctx.generate_host(kind, 4096)
+        ck = ctx.checksums()
+    ref, _ = oracle_py.mtgp_bulk(sets, seeds, L + 4096, kind=kind, threads=8)
+    assert np.array_equal(w1, ref[:, :L])
+    assert np.array_equal(w2, ref[:, L:])
+    for s in range(8):
+        assert ck[s] == (int(ref[s].astype(np.uint64).sum()), int(np.bitwise_xor.reduce(ref[s])), L + 4096)
+
+
+@pytest.mark.parametrize("L", [4, 256, 260, 352, 600, 1024, 65536 + 12])
+def test_v3_short_and_edge_lengths(curand_sets, L):
+    """Pieces shorter than N, one-step pieces, and tails of 4..252 words; every pos residue."""
+    idx = [0, 1, 2, 3, 10, 50, 100, 199]
+    sets = [curand_sets[i] for i in idx]
+    assert {p.pos % 4 for p in sets} == {0, 1, 2, 3}
+    with _ctx(sets, [1] * 8, 3) as ctx:
+        a = ctx.fill_u32(L)
+        b = ctx.fill_u32(L)
+        assert ctx.last_plan()[2] == 3
+    ref, _ = oracle_py.mtgp_bulk(sets, [1] * 8, 2 * L, threads=8)
+    assert np.array_equal(a, ref[:, :L]) and np.array_equal(b, ref[:, L:])
+
+
+def test_v3_all_200_sets_jumped(curand_sets, curand_golden):
+    """Every cuRAND set (pos 3..93, all thresholds incl. the pos/4 == 23 edge) through v3 pieces."""
+    with _ctx(curand_sets, [1] * 200, 3, {mtgp.OPT_MIN_PIECE_WORDS: 4096}) as ctx:
+        w = ctx.fill_u32(1 << 16)
+        assert ctx.last_plan()[0] >= 3000
+    assert w.astype(np.uint64).sum(axis=1).tolist() == curand_golden["all200_seed1_n65536_sum64"]

@@ -1,0 +1,80 @@
+"""N>1 host logic on CPU: world_size-2 gloo processes shard parameter-set IDs and gather the
+per-stream checksums exactly as bench.py does over NCCL on GPUs. Each rank computes its streams'
+checksums with the oracle (standing in for its GPU); rank 0 checks the gathered table."""
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, sets_per_rank, L, q):
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    sys.path.insert(0, str(root))
+    sys.path.insert(0, str(root / "oracle"))
+    import torch.distributed as dist
+
+    import oracle_py
+    from paper_1501_07701_b200 import shard
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sets = shard.sets_for_rank(11213, sets_per_rank, rank)
+    words, _ = oracle_py.mtgp_bulk(sets, [1] * len(sets), L, threads=2)
+    local = [(int(w.astype("uint64").sum()) % (1 << 64), int(__import__("numpy").bitwise_xor.reduce(w)), L)
+             for w in words]
+    allck = shard.gather_checksums(local)
+    if rank == 0:
+        q.put(allck)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_shard_and_gather(world):
+    from paper_1501_07701_b200 import shard, tables
+    import oracle_py
+
+    sets_per_rank, L = 3, 5000
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, sets_per_rank, L, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    allck = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # disjoint ID ranges covering [0, world*sets_per_rank)
+    ids = [i for r in range(world) for i in shard.set_range(r, sets_per_rank)]
+    assert ids == list(range(world * sets_per_rank))
+    every = tables.sets_for(11213, world * sets_per_rank)
+    assert len(allck) == len(every)
+    for gid, (p, ck) in enumerate(zip(every, allck)):
+        w = oracle_py.MtgpOracle(p, 1).fill(L)
+        assert ck == (int(w.astype("uint64").sum()), int(__import__("numpy").bitwise_xor.reduce(w)), L), gid
+    # rank 1's sets are the certified cuRAND sets 3..5 (global IDs continue across ranks)
+    cur = tables.load_curand_11213()
+    assert [s.pos for s in shard.sets_for_rank(11213, sets_per_rank, 1)] == [s.pos for s in cur[3:6]]
+
+
+def test_sets_beyond_the_table_are_synthetic_and_distinct():
+    from paper_1501_07701_b200 import shard
+    r7 = shard.sets_for_rank(11213, 200, 7)  # IDs 1400..1599
+    assert all(not s.certified for s in r7)
+    keys = {(s.pos, s.sh1, s.sh2, tuple(s.tbl)) for s in r7}
+    assert len(keys) == 200
+    r0 = shard.sets_for_rank(11213, 200, 0)
+    assert all(s.certified for s in r0)
