@@ -50,8 +50,11 @@ static void test_case(const char* name, const std::function<void()>& f) {
 }
 
 // pull "u32": [...] of the first32 case (set, seed) out of the golden JSON without a JSON lib
-static std::vector<std::uint32_t> golden_first32(const std::string& text, int set, std::uint32_t seed) {
-    const std::string key = "\"set\": " + std::to_string(set) + ", \"seed\": " + std::to_string(seed) + ", \"u32\": [";
+static std::vector<std::uint32_t> golden_first32(const std::string& raw, int set, std::uint32_t seed) {
+    std::string text;  // whitespace-free copy (the fixture is pretty-printed)
+    for (char ch : raw)
+        if (ch != ' ' && ch != '\n' && ch != '\r' && ch != '\t') text += ch;
+    const std::string key = "\"set\":" + std::to_string(set) + ",\"seed\":" + std::to_string(seed) + ",\"u32\":[";
     const auto i = text.find(key);
     std::vector<std::uint32_t> out;
     if (i == std::string::npos) return out;
@@ -133,6 +136,12 @@ int main(int argc, char** argv) {
             const auto py = read_status_file(argv[3]);
             CHECK(py.size() >= 2 && py[0].status == sets[0] && py[1].status == synthetic_status(23209, 1));
         }
+    });
+
+    test_case("golden fixture parses (cuRAND first32 cases)", [&] {
+        CHECK(golden_first32(golden, 0, 1).size() == 32);
+        CHECK(golden_first32(golden, 0, 1)[0] == 360948779u);
+        CHECK(golden_first32(golden, 199, 0xFFFFFFFFu).size() == 32);
     });
 
     test_case("splitmix64 / derive_seed (word_source.cpp:18-27)", [&] {

@@ -27,8 +27,8 @@ for path in libs:
     for _ in range(4):
         ctx.generate_device(kind, out.data_ptr(), words)
     g, gn, j, jn = ctx.kernel_timing()
-    pieces = ctx.last_plan()[0]
+    pieces, _, kv = ctx.last_plan()
     ctx.close()
     gbs = 4.0 * 200 * words / (g / gn / 1e3) / 1e9
     print(json.dumps({"variant": path.stem, "gen_ms": round(g / gn, 4), "gen_GBps": round(gbs, 1),
-                      "jump_ms": round(j / max(1, jn), 4), "pieces": pieces, "kind": kind, "mexp": mexp}), flush=True)
+                      "jump_ms": round(j / max(1, jn), 4), "pieces": pieces, "kernel": kv, "kind": kind, "mexp": mexp}), flush=True)
