@@ -224,7 +224,9 @@ def test_v3_bit_exact_with_jumps(curand_sets, kind):
 @pytest.mark.parametrize("L", [4, 256, 260, 352, 600, 1024, 65536 + 12])
 def test_v3_short_and_edge_lengths(curand_sets, L):
     """Pieces shorter than N, one-step pieces, and tails of 4..252 words; every pos residue."""
-    idx = [0, 1, 2, 3, 10, 50, 100, 199]
+    idx = [next(i for i, p in enumerate(curand_sets) if p.pos % 4 == r) for r in range(4)]
+    idx += [next(i for i, p in enumerate(curand_sets) if p.pos // 4 == 23)]  # threshold-32 edge
+    idx += [0, 100, 199]
     sets = [curand_sets[i] for i in idx]
     assert {p.pos % 4 for p in sets} == {0, 1, 2, 3}
     with _ctx(sets, [1] * 8, 3) as ctx:
