@@ -33,6 +33,9 @@ namespace mtgpb {
 #ifndef MTGP3_MIN_CTAS
 #define MTGP3_MIN_CTAS 6
 #endif
+#ifndef MTGP3_FOLD_PAIR
+#define MTGP3_FOLD_PAIR 1
+#endif
 
 namespace {
 
@@ -60,6 +63,7 @@ __device__ __forceinline__ uint32_t rec3(const V3Ctx& p, uint32_t a, uint32_t b,
     return y ^ __shfl_sync(FULL, p.tblr, y, 16);
 }
 
+#if !MTGP3_FOLD_PAIR
 __device__ __forceinline__ uint32_t temper3(const V3Ctx& p, uint32_t r, uint32_t t) {
 #if MTGP3_FOLD_IMAD
     t ^= __umulhi(t, p.m16);
@@ -69,6 +73,17 @@ __device__ __forceinline__ uint32_t temper3(const V3Ctx& p, uint32_t r, uint32_t
     t ^= t >> 8;
 #endif
     return r ^ __shfl_sync(FULL, p.tmpr, t, 16);
+}
+#endif
+
+// Tempering indices of two words at once: the XOR of the low nibbles of each word's four bytes.
+// Halves are paired with byte permutes so one LOP3/SHF serves both words (6 ALU ops per two
+// words instead of 8): w = (t1.lo16 ^ t1.hi16) | (t2.lo16 ^ t2.hi16) << 16; z = w ^ (w >> 8).
+__device__ __forceinline__ void fold2(uint32_t t1, uint32_t t2, uint32_t& i1, uint32_t& i2) {
+    const uint32_t w = __byte_perm(t1, t2, 0x5410) ^ __byte_perm(t1, t2, 0x7632);
+    const uint32_t z = w ^ (w >> 8);
+    i1 = z;        // bits [3:0]; shfl.idx over 16-lane segments ignores the rest
+    i2 = z >> 16;
 }
 
 template <int KIND>
@@ -111,10 +126,17 @@ __device__ __forceinline__ void step3(const V3Ctx& p, const uint4& h1, const uin
     for (int u = 0; u < 2; ++u) {
         uint32_t r[4], o[4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            r[c] = rec3(p, WA[u][c], WA[u][c + 1], WC[u][c + 1]);
-            o[c] = conv3<KIND>(p, temper3(p, r[c], WC[u][c]));
-        }
+        for (int c = 0; c < 4; ++c) r[c] = rec3(p, WA[u][c], WA[u][c + 1], WC[u][c + 1]);
+#if MTGP3_FOLD_PAIR
+        uint32_t ix[4];
+        fold2(WC[u][0], WC[u][1], ix[0], ix[1]);
+        fold2(WC[u][2], WC[u][3], ix[2], ix[3]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) o[c] = conv3<KIND>(p, r[c] ^ __shfl_sync(FULL, p.tmpr, ix[c], 16));
+#else
+#pragma unroll
+        for (int c = 0; c < 4; ++c) o[c] = conv3<KIND>(p, temper3(p, r[c], WC[u][c]));
+#endif
         const uint32_t w0 = n + 128 * u + 4 * p.lane;  // piece word of o[0]
         if (!TAIL || w0 < len) {
             __stcs(reinterpret_cast<uint4*>(optr + w0), make_uint4(o[0], o[1], o[2], o[3]));

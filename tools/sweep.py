@@ -1,6 +1,16 @@
-"""Time the v2 generation kernel of each library variant in paper_1501_07701_b200/variants/."""
+"""Time the generation kernel of each library variant in paper_1501_07701_b200/variants/.
+
+Variants are measured in interleaved rounds (A B C A B C ...) so power-cap clock drift does not
+favour whichever ran first; the SM clock is sampled through NVML during each measurement and
+the result is reported both as GB/s and as SM cycles per launch (clock-independent).
+
+    python tools/sweep.py [words_per_stream] [kind] [mexp] [rounds]
+"""
 import json
+import statistics
 import sys
+import threading
+import time
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
@@ -12,23 +22,63 @@ from paper_1501_07701_b200 import mtgp, tables  # noqa: E402
 words = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 25
 kind = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 mexp = int(sys.argv[3]) if len(sys.argv) > 3 else 11213
+rounds = int(sys.argv[4]) if len(sys.argv) > 4 else 3
+cksum = int(sys.argv[5]) if len(sys.argv) > 5 else 1
+
+try:
+    import pynvml
+    pynvml.nvmlInit()
+    nv = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+except Exception:  # noqa: BLE001
+    nv = None
+
+
+class Clock:
+    def __init__(self):
+        self.samples, self.stop = [], False
+
+    def run(self):
+        while not self.stop:
+            if nv is not None:
+                self.samples.append(pynvml.nvmlDeviceGetClockInfo(nv, pynvml.NVML_CLOCK_SM))
+            time.sleep(0.002)
+
+
 sets = tables.sets_for(mexp, 200)
 out = torch.empty((200, words), dtype=torch.int32, device="cuda")
 libs = sorted((ROOT / "paper_1501_07701_b200" / "variants").glob("*.so"))
 libs.insert(0, mtgp.LIB_PATH)
+ctxs = []
 for path in libs:
     lib = mtgp.load_library(str(path))
     ctx = mtgp.MtgpContext(sets, [1] * 200, lib=lib)
-    for _ in range(2):
-        ctx.generate_device(kind, out.data_ptr(), words)
+    ctx.set_option(mtgp.OPT_CHECKSUM, cksum)
+    ctx.generate_device(kind, out.data_ptr(), words)  # plan + warm
     ctx.sync()
-    ctx.kernel_timing_reset()
-    ctx.set_option(mtgp.OPT_TIMING, 1)
-    for _ in range(4):
-        ctx.generate_device(kind, out.data_ptr(), words)
-    g, gn, j, jn = ctx.kernel_timing()
+    ctxs.append((path.stem, ctx))
+res = {name: [] for name, _ in ctxs}
+for r in range(rounds):
+    for name, ctx in ctxs:
+        ctx.kernel_timing_reset()
+        ctx.set_option(mtgp.OPT_TIMING, 1)
+        clk = Clock()
+        th = threading.Thread(target=clk.run)
+        th.start()
+        for _ in range(2):
+            ctx.generate_device(kind, out.data_ptr(), words)
+        g, gn, j, jn = ctx.kernel_timing()
+        clk.stop = True
+        th.join()
+        ctx.set_option(mtgp.OPT_TIMING, 0)
+        mhz = statistics.median(clk.samples) if clk.samples else float("nan")
+        res[name].append((g / gn, j / max(1, jn), mhz))
+for name, ctx in ctxs:
     pieces, _, kv = ctx.last_plan()
+    ms = min(x[0] for x in res[name])
+    best = min(res[name], key=lambda x: x[0])
+    cycles = min(x[0] * 1e-3 * x[2] * 1e6 for x in res[name])
+    print(json.dumps({"variant": name, "gen_ms": round(ms, 4), "gen_GBps": round(4.0 * 200 * words / (ms / 1e3) / 1e9, 1),
+                      "mcycles_per_launch": round(cycles / 1e6, 3), "mhz_at_best": best[2],
+                      "jump_ms": round(best[1], 4), "pieces": pieces, "kernel": kv, "kind": kind, "mexp": mexp, "cksum": cksum}),
+          flush=True)
     ctx.close()
-    gbs = 4.0 * 200 * words / (g / gn / 1e3) / 1e9
-    print(json.dumps({"variant": path.stem, "gen_ms": round(g / gn, 4), "gen_GBps": round(gbs, 1),
-                      "jump_ms": round(j / max(1, jn), 4), "pieces": pieces, "kernel": kv, "kind": kind, "mexp": mexp}), flush=True)
