@@ -310,7 +310,7 @@ def main():
                          "frac": round(achieved / hbm, 4), "traffic": traffic_per_launch(bytes_per_launch),
                          "traffic_source": "profiles/gen_traffic.json (ncu dram__bytes_read+write per algorithmic byte)",
                          "peak_source": hbm_src,
-                         "kernel": "gen_kernel (v2)", "launches_timed": gen_n,
+                         "kernel": f"gen{kver if kver == 3 else ''}_kernel (v{kver})", "launches_timed": gen_n,
                          "avg_launch_ms": round(gen_avg_ms, 4),
                          "algorithmic_bytes_per_launch": bytes_per_launch,
                          "step_write_GBps": round(step_gbs, 1),

@@ -36,6 +36,9 @@ namespace mtgpb {
 #ifndef MTGP3_FOLD_PAIR
 #define MTGP3_FOLD_PAIR 1
 #endif
+#ifndef MTGP3_CK_WIDE
+#define MTGP3_CK_WIDE 0
+#endif
 
 namespace {
 
@@ -141,8 +144,14 @@ __device__ __forceinline__ void step3(const V3Ctx& p, const uint4& h1, const uin
         if (!TAIL || w0 < len) {
             __stcs(reinterpret_cast<uint4*>(optr + w0), make_uint4(o[0], o[1], o[2], o[3]));
             if (CK) {
+#if MTGP3_CK_WIDE
+                // 64-bit sum on the FMA pipe: IMAD.WIDE.U32 sum = o * one + sum (one is opaque)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(sum) : "r"(o[c]), "r"(p.one));
+#else
 #pragma unroll
                 for (int c = 0; c < 4; ++c) sum += o[c];
+#endif
                 xr ^= o[0] ^ o[1] ^ o[2] ^ o[3];
             }
         }
