@@ -377,6 +377,18 @@ int mtgp_skip(mtgp_ctx* ctx, uint64_t words) {
     if (!ctx) return fail(MTGP_EINVAL, "null context");
     if (words == 0) return MTGP_OK;
     CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (words < 4096) {
+        // short skips: generating is cheaper than a jump (and jumps start past the transient)
+        void* scratch = nullptr;
+        CK(cudaMalloc(&scratch, (size_t)words * ctx->n_sets * 4), "cudaMalloc skip scratch");
+        const bool ck = ctx->cksum;
+        ctx->cksum = false;
+        const int rc = generate_device(ctx, MTGP_U32, scratch, words);
+        ctx->cksum = ck;
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(scratch);
+        return rc;
+    }
     std::string err;
     cudaError_t e = ctx->planner->skip(ctx->d_params, ctx->d_win, words, ctx->stream, err);
     if (e != cudaSuccess) return fail(MTGP_ECUDA, "skip: %s (%s)", err.c_str(), cudaGetErrorString(e));

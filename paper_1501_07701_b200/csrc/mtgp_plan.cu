@@ -74,10 +74,14 @@ struct PlannerImpl {
     uint32_t M = 0, N = 0, S = 0;
     bool v2 = false;
 
-    // algebra (per set)
+    // algebra (per set). Polynomials annihilate the state sequence from the reference point
+    // x_{t0} on (t0 = N + 8, rounded to 4): degenerate (uncertified) recursions have a
+    // pre-period, so the sequence from x_0 need not be annihilated by the minimal polynomial.
     bool analyzed = false;
-    bool jumps_ok = false;
+    bool jumps_ok = false;             // at least one set can be split
+    std::vector<int> set_ok;           // per set: annihilator found
     std::vector<std::unique_ptr<gf2::Modulus>> mods;
+    uint32_t t0 = 0;
 
     // cached plan
     uint64_t plan_L = 0;
@@ -101,12 +105,15 @@ struct PlannerImpl {
             b->release();
     }
 
+    // words the jump kernel stages per row (from x_{t0})
     uint32_t prefix_len() const {
         const uint32_t qw = (M + 31) / 32;
         const uint32_t jblk = 32 * 12;
         const uint32_t need = 32 * qw + jblk * ((N + jblk - 1) / jblk) + 36;
         return (need + 31) & ~31u;
     }
+    // words the prefix kernel generates per row (x_0 .. ), rows 128-byte aligned
+    uint32_t prefix_stride() const { return (t0 + prefix_len() + 31) & ~31u; }
 
     cudaError_t analyze(const DevParams* params, const uint32_t* win, cudaStream_t st, std::string& err);
     cudaError_t build_plan(uint64_t L, uint32_t T, uint64_t min_piece, std::string& err);
@@ -118,6 +125,7 @@ Planner::Planner(const std::vector<mtgp_params>& sets, int num_sms) : impl_(new 
     impl_->S = (uint32_t)sets.size();
     impl_->M = sets[0].mexp;
     impl_->N = state_words(impl_->M);
+    impl_->t0 = (impl_->N + 8 + 3) & ~3u;
     impl_->v2 = v2_supports(impl_->M);
     for (const auto& p : sets)
         if (p.pos + kStepWords > impl_->N) impl_->v2 = false;  // needs N - pos >= 256
@@ -133,7 +141,7 @@ void Planner::invalidate() {
 
 cudaError_t PlannerImpl::analyze(const DevParams* params, const uint32_t* win, cudaStream_t st, std::string& err) {
     if (analyzed) return cudaSuccess;
-    const uint32_t len = ((2 * M + N + 64) + 31) & ~31u;
+    const uint32_t len = ((t0 + 2 * M + N + 64) + 31) & ~31u;
     std::vector<uint32_t> rows(S);
     for (uint32_t s = 0; s < S; ++s) rows[s] = s;
     cudaError_t e;
@@ -154,9 +162,8 @@ cudaError_t PlannerImpl::analyze(const DevParams* params, const uint32_t* win, c
     mods.clear();
     mods.resize(S);
     std::vector<int> ok(S, 0);
-    const uint32_t mask0 = sets[0].mask;
     parallel_for(S, [&](size_t s) {
-        const uint32_t* x = h.data() + s * len;
+        const uint32_t* x = h.data() + s * len + t0;  // reference point x_{t0}
         // functionals: bit 31, bit 0, then parities of pseudo-random masks
         const uint32_t fmask[] = {0x80000000u, 0x00000001u, 0x00010000u, 0x9E3779B9u, 0x7F4A7C15u,
                                   0x85EBCA6Bu, 0xC2B2AE35u, 0x27D4EB2Fu, 0x165667B1u, 0xD3A2646Cu};
@@ -165,7 +172,7 @@ cudaError_t PlannerImpl::analyze(const DevParams* params, const uint32_t* win, c
         for (uint32_t fi = 0; fi < sizeof(fmask) / sizeof(fmask[0]) && !good; ++fi) {
             std::vector<uint64_t> bits((2 * (size_t)M + 63) / 64 + 1, 0);
             for (size_t k = 0; k < 2 * (size_t)M; ++k)
-                if (__builtin_parity(x[k + 1] & fmask[fi])) bits[k >> 6] |= 1ull << (k & 63);
+                if (__builtin_parity(x[k] & fmask[fi])) bits[k >> 6] |= 1ull << (k & 63);
             gf2::Poly Q = gf2::berlekamp_massey(bits, 2 * (size_t)M);
             if (fi == 0) {
                 P = Q;
@@ -177,7 +184,8 @@ cudaError_t PlannerImpl::analyze(const DevParams* params, const uint32_t* win, c
                 P = gf2::mul(P, qq);
             }
             if (P.degree() > (int)M) break;
-            // annihilation on all bits of the window (j = 0: live bits only)
+            // P annihilates every bit of the whole window at the reference point, hence (by
+            // linearity of the transition) every later window
             std::vector<int> idx;
             for (int i = 0; i <= P.degree(); ++i)
                 if (P.coeff(i)) idx.push_back(i);
@@ -185,7 +193,6 @@ cudaError_t PlannerImpl::analyze(const DevParams* params, const uint32_t* win, c
             for (uint32_t j = 0; j < N && ann; ++j) {
                 uint32_t acc = 0;
                 for (int i : idx) acc ^= x[i + j];
-                if (j == 0) acc &= mask0;
                 ann = acc == 0;
             }
             good = ann;
@@ -195,11 +202,12 @@ cudaError_t PlannerImpl::analyze(const DevParams* params, const uint32_t* win, c
             ok[s] = 1;
         }
     });
-    jumps_ok = true;
+    set_ok = ok;
+    jumps_ok = false;
     for (uint32_t s = 0; s < S; ++s)
-        if (!ok[s]) jumps_ok = false;
+        if (ok[s]) jumps_ok = true;
     analyzed = true;
-    if (!jumps_ok) err.clear();  // not an error: the planner falls back to one piece per stream
+    err.clear();  // a set without an annihilator is simply never split (one piece per call)
     return cudaSuccess;
 }
 
@@ -215,20 +223,34 @@ cudaError_t PlannerImpl::build_plan(uint64_t L, uint32_t T, uint64_t min_piece, 
     want = std::max<uint64_t>(want, (W + kMaxPieceWords - 1) / kMaxPieceWords);
     pieces.clear();
     teams.clear();
-    if (want <= S || !jumps_ok) {
-        if (!jumps_ok && L > kMaxPieceWords) {
-            err = "request needs jump-ahead pieces but no annihilating polynomial was found";
-            return cudaSuccess;
-        }
+    if (L > kMaxPieceWords)
+        for (uint32_t s = 0; s < S; ++s)
+            if (!set_ok[s]) {
+                err = "request needs jump-ahead pieces but stream " + std::to_string(s) +
+                      " has no annihilating polynomial";
+                return cudaSuccess;
+            }
+    if (want <= S || !jumps_ok || L < 2ull * t0) {
         for (uint32_t s = 0; s < S; ++s) {
             pieces.push_back(Piece{s, -1, 0, L});
             teams.push_back(TeamWork{s, 1});
         }
     } else {
-        // split the concatenation of all streams into `want` equal ranges, cut at stream
-        // boundaries; range starts rounded to 4 words so most pieces start 16B-aligned
+        // Split the concatenation of all streams into `want` equal ranges cut at stream
+        // boundaries; cuts are multiples of 4 words (16-byte aligned pieces), never inside a
+        // stream that cannot be jumped, and never in (0, t0) of a stream (jumps start at x_{t0}).
+        std::vector<uint64_t> cut(want + 1);
+        cut[0] = 0;
+        cut[want] = W;
+        for (uint64_t g = 1; g < want; ++g) {
+            uint64_t c = (W * g / want) & ~3ull;
+            const uint64_t s = c / L, off = c % L;
+            if (off && !set_ok[s]) c = (off < L / 2) ? s * L : (s + 1) * L;
+            else if (off && off < t0) c = s * L + t0;
+            cut[g] = std::min<uint64_t>(std::max<uint64_t>(c, cut[g - 1]), W);
+        }
         for (uint64_t g = 0; g < want; ++g) {
-            uint64_t a = (W * g / want) & ~3ull, b = g + 1 == want ? W : (W * (g + 1) / want) & ~3ull;
+            uint64_t a = cut[g], b = cut[g + 1];
             if (b <= a) continue;
             TeamWork tw{(uint32_t)pieces.size(), 0};
             while (a < b) {
@@ -263,7 +285,7 @@ cudaError_t PlannerImpl::build_plan(uint64_t L, uint32_t T, uint64_t min_piece, 
         max_jobs_per_row = std::max<uint32_t>(max_jobs_per_row, (uint32_t)kv.second.size());
     }
     n_q = (uint32_t)qlist.size();
-    // jump polynomials x^offset mod P, chained per set
+    // jump polynomials x^(offset - t0) mod P (relative to the reference point), chained per set
     std::vector<uint32_t> hq((size_t)n_q * q_words, 0);
     std::vector<uint32_t> rows_list(jump_rows);
     parallel_for(rows_list.size(), [&](size_t r) {
@@ -275,7 +297,7 @@ cudaError_t PlannerImpl::build_plan(uint64_t L, uint32_t T, uint64_t min_piece, 
         bool have = false;
         for (uint32_t jj = job_off[r]; jj < job_off[r + 1]; ++jj) {
             const uint32_t pi = jobs[jj].piece;
-            const uint64_t off = pieces[pi].offset;
+            const uint64_t off = pieces[pi].offset - t0;
             if (!have) {
                 cur = md.x_pow(off);
                 have = true;
@@ -299,7 +321,7 @@ cudaError_t PlannerImpl::build_plan(uint64_t L, uint32_t T, uint64_t min_piece, 
     if ((e = d_pwin_ptrs.ensure(sizeof(uint32_t*) * pieces.size())) != cudaSuccess) return e;
     if ((e = d_pwin.ensure(sizeof(uint32_t) * N * std::max<size_t>(1, pieces.size()))) != cudaSuccess) return e;
     if ((e = d_q.ensure(sizeof(uint32_t) * std::max<size_t>(1, hq.size()))) != cudaSuccess) return e;
-    if ((e = d_pre.ensure(sizeof(uint32_t) * (size_t)pre_len * std::max<size_t>(1, jump_rows.size()))) != cudaSuccess) return e;
+    if ((e = d_pre.ensure(sizeof(uint32_t) * (size_t)prefix_stride() * std::max<size_t>(1, jump_rows.size()))) != cudaSuccess) return e;
     if ((e = d_rows.ensure(sizeof(uint32_t) * std::max<size_t>(1, jump_rows.size()))) != cudaSuccess) return e;
     if ((e = d_joboff.ensure(sizeof(uint32_t) * job_off.size())) != cudaSuccess) return e;
     if ((e = d_jobs.ensure(sizeof(JumpJob) * std::max<size_t>(1, jobs.size()))) != cudaSuccess) return e;
@@ -361,11 +383,13 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     if (!I.jump_rows.empty()) {
         if (r.timing) r.timing->record(r.stream, &j0);
         if ((e = launch_prefix(r.params, r.win, I.d_rows.as<uint32_t>(), (uint32_t)I.jump_rows.size(), I.N,
-                               I.d_pre.as<uint32_t>(), I.pre_len, r.stream)) != cudaSuccess)
+                               I.d_pre.as<uint32_t>(), I.prefix_stride(), r.stream)) != cudaSuccess)
             return e;
         JumpArgs ja;
         ja.pre = I.d_pre.as<uint32_t>();
         ja.pre_len = I.pre_len;
+        ja.pre_stride = I.prefix_stride();
+        ja.pre_off = I.t0;
         ja.set_of = I.d_rows.as<uint32_t>();
         ja.job_off = I.d_joboff.as<uint32_t>();
         ja.jobs = I.d_jobs.as<JumpJob>();
@@ -416,18 +440,24 @@ cudaError_t Planner::skip(const DevParams* params, uint32_t* win, uint64_t words
     }
     cudaError_t e;
     if (!I.analyzed && (e = I.analyze(params, win, st, err)) != cudaSuccess) return e;
-    if (!I.jumps_ok) {
-        err = "no annihilating polynomial found for some stream";
+    for (uint32_t s = 0; s < I.S; ++s)
+        if (!I.set_ok[s]) {
+            err = "no annihilating polynomial found for stream " + std::to_string(s);
+            return cudaSuccess;
+        }
+    if (words < I.t0) {
+        err = "skip distance below the jump reference offset";
         return cudaSuccess;
     }
     const uint32_t qw = (I.M + 31) / 32;
     std::vector<uint32_t> hq((size_t)I.S * qw, 0);
     parallel_for(I.S, [&](size_t s) {
-        gf2::Poly q = I.mods[s]->x_pow(words);
+        gf2::Poly q = I.mods[s]->x_pow(words - I.t0);
         for (int i = 0; i <= q.degree(); ++i)
             if (q.coeff(i)) hq[s * qw + (i >> 5)] |= 1u << (i & 31);
     });
     const uint32_t pre_len = I.prefix_len();
+    const uint32_t pre_stride = I.prefix_stride();
     DevBuf pre, q, rows, joff, jobs, out;
     std::vector<uint32_t> hrows(I.S), hoff(I.S + 1);
     std::vector<JumpJob> hjobs(I.S);
@@ -440,7 +470,7 @@ cudaError_t Planner::skip(const DevParams* params, uint32_t* win, uint64_t words
     auto cleanup = [&] {
         for (DevBuf* b : {&pre, &q, &rows, &joff, &jobs, &out}) b->release();
     };
-    if ((e = pre.ensure((size_t)pre_len * I.S * 4)) != cudaSuccess || (e = q.ensure(hq.size() * 4)) != cudaSuccess ||
+    if ((e = pre.ensure((size_t)pre_stride * I.S * 4)) != cudaSuccess || (e = q.ensure(hq.size() * 4)) != cudaSuccess ||
         (e = rows.ensure(I.S * 4)) != cudaSuccess || (e = joff.ensure((I.S + 1) * 4)) != cudaSuccess ||
         (e = jobs.ensure(I.S * sizeof(JumpJob))) != cudaSuccess || (e = out.ensure((size_t)I.S * I.N * 4)) != cudaSuccess) {
         cleanup();
@@ -450,11 +480,13 @@ cudaError_t Planner::skip(const DevParams* params, uint32_t* win, uint64_t words
     cudaMemcpyAsync(rows.p, hrows.data(), I.S * 4, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(joff.p, hoff.data(), (I.S + 1) * 4, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(jobs.p, hjobs.data(), I.S * sizeof(JumpJob), cudaMemcpyHostToDevice, st);
-    e = launch_prefix(params, win, rows.as<uint32_t>(), I.S, I.N, pre.as<uint32_t>(), pre_len, st);
+    e = launch_prefix(params, win, rows.as<uint32_t>(), I.S, I.N, pre.as<uint32_t>(), pre_stride, st);
     if (e == cudaSuccess) {
         JumpArgs ja;
         ja.pre = pre.as<uint32_t>();
         ja.pre_len = pre_len;
+        ja.pre_stride = pre_stride;
+        ja.pre_off = I.t0;
         ja.set_of = rows.as<uint32_t>();
         ja.job_off = joff.as<uint32_t>();
         ja.jobs = jobs.as<JumpJob>();

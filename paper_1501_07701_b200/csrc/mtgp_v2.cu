@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(kJumpWarps * 32) jump_kernel(JumpArgs a) {
     const uint32_t first = a.job_off[row] + blockIdx.y * kJumpWarps;
     const uint32_t end = a.job_off[row + 1];
     if (first >= end) return;
-    const uint4* src = reinterpret_cast<const uint4*>(a.pre + (size_t)row * a.pre_len);
+    const uint4* src = reinterpret_cast<const uint4*>(a.pre + (size_t)row * a.pre_stride + a.pre_off);
     for (uint32_t i = threadIdx.x; i < a.pre_len / 4; i += blockDim.x) jsm4[i] = src[i];
     __syncthreads();
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -28,7 +28,9 @@ struct JumpJob {
 
 struct JumpArgs {
     const uint32_t* pre;      // [n_jump_sets][pre_len] state-word prefixes
-    uint32_t pre_len;         // >= M + N
+    uint32_t pre_len;         // words staged per row (>= M + N + slack)
+    uint32_t pre_stride;      // words between rows
+    uint32_t pre_off;         // reference offset t0: the staged sequence starts at x_{t0}
     const uint32_t* set_of;   // [n_jump_sets] set index of each prefix row
     const uint32_t* job_off;  // [n_jump_sets + 1] CSR offsets into jobs
     const JumpJob* jobs;

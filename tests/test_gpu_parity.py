@@ -243,3 +243,30 @@ def test_v3_all_200_sets_jumped(curand_sets, curand_golden):
         w = ctx.fill_u32(1 << 16)
         assert ctx.last_plan()[0] >= 3000
     assert w.astype(np.uint64).sum(axis=1).tolist() == curand_golden["all200_seed1_n65536_sum64"]
+
+
+@pytest.mark.parametrize("mexp", [23209, 44497])
+def test_synthetic_degenerate_sets_jump(mexp):
+    """Uncertified synthetic sets have pre-periods / reducible annihilators; jumps are taken
+    relative to the reference point x_{N+8} and every stream must still be bit-exact."""
+    sets = tables.synthetic_sets(mexp, 16)
+    seeds = list(range(16))
+    L = 40000
+    with _ctx(sets, seeds, 2, {mtgp.OPT_MIN_PIECE_WORDS: 4000}) as ctx:
+        w = ctx.fill_u32(L)
+        assert ctx.last_plan()[0] >= 16 * 5
+    ref, _ = oracle_py.mtgp_bulk(sets, seeds, L, threads=8)
+    assert np.array_equal(w, ref)
+
+
+def test_short_skip_generates(curand_sets):
+    sets = curand_sets[5:7]
+    with _ctx(sets, [3, 4], 0) as ctx:
+        ctx.skip(100)
+        ctx.skip(3)
+        w = ctx.fill_u32(1000)
+        assert ctx.checksums()[0][2] == 1000  # skipped words are not checksummed
+    for s in range(2):
+        o = oracle_py.MtgpOracle(sets[s], 3 + s)
+        o.skip(103)
+        assert np.array_equal(w[s], o.fill(1000))
