@@ -164,9 +164,17 @@ cudaError_t PlannerImpl::analyze(const DevParams* params, const uint32_t* win, c
     std::vector<int> ok(S, 0);
     parallel_for(S, [&](size_t s) {
         const uint32_t* x = h.data() + s * len + t0;  // reference point x_{t0}
-        // functionals: bit 31, bit 0, then parities of pseudo-random masks
-        const uint32_t fmask[] = {0x80000000u, 0x00000001u, 0x00010000u, 0x9E3779B9u, 0x7F4A7C15u,
-                                  0x85EBCA6Bu, 0xC2B2AE35u, 0x27D4EB2Fu, 0x165667B1u, 0xD3A2646Cu};
+        // Functionals: parities of dense pseudo-random word masks (the LCM over all single-word
+        // functionals is the state's annihilator; degenerate uncertified recursions can hide whole
+        // components from single bits, e.g. a constant bit 0). Certified sets finish after one.
+        uint32_t fmask[24];
+        uint64_t sm = 0x4D54475041ull;
+        for (auto& m : fmask) {
+            sm += 0x9E3779B97F4A7C15ull;
+            uint64_t z = (sm ^ (sm >> 30)) * 0xBF58476D1CE4E5B9ull;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+            m = static_cast<uint32_t>(z ^ (z >> 31)) | 0x80000001u;
+        }
         gf2::Poly P;
         bool good = false;
         for (uint32_t fi = 0; fi < sizeof(fmask) / sizeof(fmask[0]) && !good; ++fi) {
