@@ -165,6 +165,29 @@ int mtgp_kernel_timing_reset(mtgp_ctx* ctx);
 /* Number of CUDA kernels this context has launched since creation. */
 int mtgp_launch_count(const mtgp_ctx* ctx, uint64_t* launches);
 
+/*
+ * Engine::mt -- the reference's own generic MT recurrence on the GPU, bit-exact with
+ * Generator/MtWordSource (proj/src/generator.cpp:7-13,37-52,68-88). Field meaning is that of
+ * ParameterizedStatus (proj/include/twistsieve/params.hpp:21-42).
+ */
+typedef struct mtgp_mt_params {
+    uint32_t id, mexp, n, m, r, a;
+    uint32_t temper_b, temper_c, temper_u, temper_s, temper_t, temper_l;
+} mtgp_mt_params;
+
+/* ParameterizedStatus::validate (proj/src/params.cpp:23-39): MTGP_EINVAL with the reference's
+   message on a violated invariant. */
+int mtgp_mt_validate_params(const mtgp_mt_params* p);
+
+/*
+ * Context of n_sets Engine::mt streams (= n_sets make_word_source(status, seed) calls,
+ * proj/src/word_source.cpp:5-16). Seeds expand as Generator::Generator (generator.cpp:37-52).
+ * Supports mtgp_generate (all kinds; u32 = next_u32 order), state save/restore (window of n
+ * words, stride = max n), checksums, positions and mtgp_skip (by generation).
+ */
+int mtgp_mt_ctx_create(mtgp_ctx** out, int device, const mtgp_mt_params* sets, uint32_t n_sets,
+                       const uint32_t* seeds, void* stream);
+
 /* Launch plan of the last generation call: pieces (jump-ahead segments) and warps per piece. */
 int mtgp_last_plan(const mtgp_ctx* ctx, uint32_t* pieces, uint32_t* warps_per_piece,
                    uint32_t* kernel_version);

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "mtgp_internal.cuh"
+#include "mtgp_mt.cuh"
 #include "mtgp_plan.h"
 
 using namespace mtgpb;
@@ -72,8 +73,11 @@ struct mtgp_ctx {
     cudaStream_t copy_stream = nullptr;
     bool own_stream = false;
     uint32_t n_sets = 0, N = 0, mexp = 0;
+    int engine = 0;  // 0 = MTGP32, 1 = Engine::mt (the reference's classic recurrence)
     std::vector<mtgp_params> sets;
+    std::vector<mtgp_mt_params> mt_sets;
     std::vector<uint64_t> position;
+    DevMtParams* d_mt = nullptr;
 
     DevParams* d_params = nullptr;
     uint32_t* d_win = nullptr;
@@ -203,6 +207,80 @@ int mtgp_ctx_create(mtgp_ctx** out, int device, const mtgp_params* sets, uint32_
     return MTGP_OK;
 }
 
+// ---- Engine::mt (proj/src/params.cpp:23-39 validation, generator.cpp:37-52 seeding) ----
+int mtgp_mt_validate_params(const mtgp_mt_params* p) {
+    static const uint32_t kSupported[] = {89, 127, 521, 607, 1279, 2203, 2281, 3217, 19937, 23209};
+    if (!p) return fail(MTGP_EINVAL, "null parameter set");
+    if (p->n < 2) return fail(MTGP_EINVAL, "state length n must be >= 2");
+    if (p->r >= 32) return fail(MTGP_EINVAL, "split position r must be < 32");
+    if (32 * p->n - p->r != p->mexp) return fail(MTGP_EINVAL, "32*n - r must equal mexp");
+    bool ok = false;
+    for (uint32_t e : kSupported) ok = ok || e == p->mexp;
+    if (!ok) return fail(MTGP_EINVAL, "unsupported period exponent %u", p->mexp);
+    if (p->m < 1 || p->m >= p->n) return fail(MTGP_EINVAL, "middle offset m must satisfy 1 <= m < n");
+    if ((p->a & 0xFFFFu) != p->id) return fail(MTGP_EINVAL, "low 16 bits of twist coefficient must carry the id");
+    for (uint32_t sh : {p->temper_u, p->temper_s, p->temper_t, p->temper_l})
+        if (sh < 1 || sh > 31) return fail(MTGP_EINVAL, "tempering shifts must be in [1, 31]");
+    return MTGP_OK;
+}
+
+int mtgp_mt_ctx_create(mtgp_ctx** out, int device, const mtgp_mt_params* sets, uint32_t n_sets,
+                       const uint32_t* seeds, void* stream) {
+    if (!out || !sets || !seeds || n_sets == 0) return fail(MTGP_EINVAL, "null argument or n_sets == 0");
+    *out = nullptr;
+    uint32_t nmax = 0;
+    for (uint32_t s = 0; s < n_sets; ++s) {
+        int rc = mtgp_mt_validate_params(&sets[s]);
+        if (rc) return fail(rc, "set %u: %s", s, g_err.c_str());
+        nmax = std::max(nmax, sets[s].n);
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(MTGP_ECUDA, "no CUDA device (there is no CPU fallback)");
+    if (device < 0 || device >= ndev) return fail(MTGP_EINVAL, "device %d out of range", device);
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major < 10) return fail(MTGP_ECUDA, "device %d is sm_%d%d; this library is built for sm_100a", device, prop.major, prop.minor);
+    CK(cudaSetDevice(device), "cudaSetDevice");
+    auto ctx = std::make_unique<mtgp_ctx>();
+    ctx->engine = 1;
+    ctx->device = device;
+    ctx->n_sets = n_sets;
+    ctx->mexp = sets[0].mexp;
+    ctx->N = nmax;
+    ctx->mt_sets.assign(sets, sets + n_sets);
+    ctx->position.assign(n_sets, 0);
+    if (stream) {
+        ctx->stream = static_cast<cudaStream_t>(stream);
+    } else {
+        CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        ctx->own_stream = true;
+    }
+    CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (int i = 0; i < 2; ++i) {
+        CK(cudaEventCreateWithFlags(&ctx->ev_gen[i], cudaEventDisableTiming), "cudaEventCreate");
+        CK(cudaEventCreateWithFlags(&ctx->ev_copy[i], cudaEventDisableTiming), "cudaEventCreate");
+    }
+    std::vector<DevMtParams> dp(n_sets);
+    std::vector<uint32_t> win((size_t)n_sets * nmax, 0);
+    for (uint32_t s = 0; s < n_sets; ++s) {
+        const mtgp_mt_params& p = sets[s];
+        dp[s] = DevMtParams{p.n, p.m, p.r, p.a, p.temper_b, p.temper_c, p.temper_u, p.temper_s, p.temper_t, p.temper_l, 0, 0};
+        uint32_t* x = win.data() + (size_t)s * nmax;
+        x[0] = seeds[s];
+        for (uint32_t i = 1; i < p.n; ++i) x[i] = 1812433253u * (x[i - 1] ^ (x[i - 1] >> 30)) + i;
+    }
+    CK(cudaMalloc(&ctx->d_mt, sizeof(DevMtParams) * n_sets), "cudaMalloc params");
+    CK(cudaMalloc(&ctx->d_win, sizeof(uint32_t) * win.size()), "cudaMalloc state");
+    CK(cudaMalloc(&ctx->d_ck, sizeof(DevCksum) * n_sets), "cudaMalloc checksums");
+    CK(cudaMemcpyAsync(ctx->d_mt, dp.data(), sizeof(DevMtParams) * n_sets, cudaMemcpyHostToDevice, ctx->stream), "upload params");
+    CK(cudaMemcpyAsync(ctx->d_win, win.data(), sizeof(uint32_t) * win.size(), cudaMemcpyHostToDevice, ctx->stream), "upload state");
+    CK(cudaMemsetAsync(ctx->d_ck, 0, sizeof(DevCksum) * n_sets, ctx->stream), "memset checksums");
+    CK(cudaStreamSynchronize(ctx->stream), "sync");
+    *out = ctx.release();
+    return MTGP_OK;
+}
+
 int mtgp_ctx_destroy(mtgp_ctx* ctx) {
     if (!ctx) return MTGP_OK;
     cudaSetDevice(ctx->device);
@@ -210,6 +288,7 @@ int mtgp_ctx_destroy(mtgp_ctx* ctx) {
     cudaStreamSynchronize(ctx->copy_stream);
     ctx->planner.reset();
     cudaFree(ctx->d_params);
+    cudaFree(ctx->d_mt);
     cudaFree(ctx->d_win);
     cudaFree(ctx->d_ck);
     cudaFree(ctx->d_stage);
@@ -276,6 +355,23 @@ namespace {
 // One device-side generation of L words per stream into device memory `out`.
 int generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
     if (L == 0) return MTGP_OK;
+    if (ctx->engine == 1) {
+        size_t e0 = 0, e1 = 0;
+        if (ctx->timing) ctx->pool.record(ctx->stream, &e0);
+        cudaError_t e = launch_mt_v1(kind, ctx->cksum, ctx->d_mt, ctx->d_win, ctx->n_sets, ctx->N, out, L, ctx->d_ck,
+                                     ctx->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "Engine::mt generation kernel");
+        if (ctx->timing) {
+            ctx->pool.record(ctx->stream, &e1);
+            ctx->pool.gen.push_back({e0, e1});
+        }
+        ctx->total_launches += 1;
+        ctx->last_pieces = ctx->n_sets;
+        ctx->last_warps = 8;
+        ctx->last_kernel = 1;
+        for (auto& p : ctx->position) p += L;
+        return MTGP_OK;
+    }
     const bool use_v1 = ctx->kernel == 1 || !ctx->planner->v2_supported();
     if (use_v1) {
         size_t e0 = 0, e1 = 0;
@@ -377,13 +473,17 @@ int mtgp_skip(mtgp_ctx* ctx, uint64_t words) {
     if (!ctx) return fail(MTGP_EINVAL, "null context");
     if (words == 0) return MTGP_OK;
     CK(cudaSetDevice(ctx->device), "cudaSetDevice");
-    if (words < 4096) {
-        // short skips: generating is cheaper than a jump (and jumps start past the transient)
+    if (words < 4096 || ctx->engine == 1) {
+        // Short skips (and Engine::mt, which has no jump-ahead yet): generate into a scratch
+        // buffer in chunks; generating is cheaper than a jump for short distances.
+        const uint64_t chunk = std::min<uint64_t>(words, 1ull << 20);
         void* scratch = nullptr;
-        CK(cudaMalloc(&scratch, (size_t)words * ctx->n_sets * 4), "cudaMalloc skip scratch");
+        CK(cudaMalloc(&scratch, (size_t)chunk * ctx->n_sets * 4), "cudaMalloc skip scratch");
         const bool ck = ctx->cksum;
         ctx->cksum = false;
-        const int rc = generate_device(ctx, MTGP_U32, scratch, words);
+        int rc = MTGP_OK;
+        for (uint64_t done = 0; done < words && rc == MTGP_OK; done += chunk)
+            rc = generate_device(ctx, MTGP_U32, scratch, std::min<uint64_t>(chunk, words - done));
         ctx->cksum = ck;
         cudaStreamSynchronize(ctx->stream);
         cudaFree(scratch);
@@ -412,7 +512,7 @@ int mtgp_state_restore(mtgp_ctx* ctx, const uint32_t* windows, const uint64_t* p
     CK(cudaMemcpyAsync(ctx->d_win, windows, (size_t)ctx->n_sets * ctx->N * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D state");
     CK(cudaStreamSynchronize(ctx->stream), "sync");
     if (positions) std::copy(positions, positions + ctx->n_sets, ctx->position.begin());
-    ctx->planner->invalidate();
+    if (ctx->planner) ctx->planner->invalidate();
     return MTGP_OK;
 }
 

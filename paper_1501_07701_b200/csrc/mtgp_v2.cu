@@ -452,35 +452,17 @@ __global__ void __launch_bounds__(kJumpWarps * 32) jump_kernel(JumpArgs a) {
                         w[4 * v + 3] = g.w;
                     }
 #pragma unroll
-                    // q walked a nibble at a time: one warp-uniform 16-way branch, then each
-                    // accumulator takes the XOR of the selected window columns (LOP3 folds two
-                    // columns per op)
-                    for (int b = 0; b < 32; b += 4) {
-                        switch ((qw >> b) & 15u) {
-#define MTGP_J1(a) for (int k = 0; k < J; ++k) acc[k] ^= w[b + a + k]
-#define MTGP_J2(a, c) for (int k = 0; k < J; ++k) acc[k] ^= w[b + a + k] ^ w[b + c + k]
-#define MTGP_J3(a, c, d) for (int k = 0; k < J; ++k) acc[k] ^= w[b + a + k] ^ w[b + c + k] ^ w[b + d + k]
-                            case 1: MTGP_J1(0); break;
-                            case 2: MTGP_J1(1); break;
-                            case 3: MTGP_J2(0, 1); break;
-                            case 4: MTGP_J1(2); break;
-                            case 5: MTGP_J2(0, 2); break;
-                            case 6: MTGP_J2(1, 2); break;
-                            case 7: MTGP_J3(0, 1, 2); break;
-                            case 8: MTGP_J1(3); break;
-                            case 9: MTGP_J2(0, 3); break;
-                            case 10: MTGP_J2(1, 3); break;
-                            case 11: MTGP_J3(0, 1, 3); break;
-                            case 12: MTGP_J2(2, 3); break;
-                            case 13: MTGP_J3(0, 2, 3); break;
-                            case 14: MTGP_J3(1, 2, 3); break;
-                            case 15:
-                                for (int k = 0; k < J; ++k) acc[k] ^= w[b + k] ^ w[b + 1 + k] ^ w[b + 2 + k] ^ w[b + 3 + k];
-                                break;
-                            default: break;
-#undef MTGP_J1
-#undef MTGP_J2
-#undef MTGP_J3
+                    for (int b = 0; b < 32; b += 2) {
+                        const uint32_t pat = (qw >> b) & 3u;
+                        if (pat == 1) {
+#pragma unroll
+                            for (int k = 0; k < J; ++k) acc[k] ^= w[b + k];
+                        } else if (pat == 2) {
+#pragma unroll
+                            for (int k = 0; k < J; ++k) acc[k] ^= w[b + 1 + k];
+                        } else if (pat == 3) {
+#pragma unroll
+                            for (int k = 0; k < J; ++k) acc[k] ^= w[b + k] ^ w[b + 1 + k];
                         }
                     }
                 }

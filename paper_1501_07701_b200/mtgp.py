@@ -32,8 +32,20 @@ EXPORTS = (
     "mtgp_generate", "mtgp_generate_u32", "mtgp_generate_f32_12", "mtgp_generate_f32_01oc",
     "mtgp_skip", "mtgp_state_save", "mtgp_state_restore", "mtgp_checksums",
     "mtgp_checksums_reset", "mtgp_sync", "mtgp_kernel_timing", "mtgp_kernel_timing_reset",
-    "mtgp_last_plan", "mtgp_launch_count",
+    "mtgp_last_plan", "mtgp_launch_count", "mtgp_mt_validate_params", "mtgp_mt_ctx_create",
 )
+
+
+class MtParamsC(C.Structure):
+    """Engine::mt status (ParameterizedStatus recurrence fields, proj/include/twistsieve/params.hpp:21-42)."""
+    _fields_ = [(k, C.c_uint32) for k in ("id", "mexp", "n", "m", "r", "a", "temper_b", "temper_c", "temper_u",
+                                          "temper_s", "temper_t", "temper_l")]
+
+
+def mt19937_status() -> dict:
+    """proj/src/params.cpp:63-77."""
+    return dict(id=0xB0DF, mexp=19937, n=624, m=397, r=31, a=0x9908B0DF, temper_b=0x9D2C5680,
+                temper_c=0xEFC60000, temper_u=11, temper_s=7, temper_t=15, temper_l=18)
 
 
 class MtgpParamsC(C.Structure):
@@ -88,6 +100,9 @@ def load_library(path: Optional[str] = None) -> C.CDLL:
     lib.mtgp_last_plan.argtypes = [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
     lib.mtgp_validate_params.argtypes = [C.POINTER(MtgpParamsC)]
     lib.mtgp_launch_count.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
+    lib.mtgp_mt_validate_params.argtypes = [C.POINTER(MtParamsC)]
+    lib.mtgp_mt_ctx_create.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.POINTER(MtParamsC), C.c_uint32,
+                                       C.POINTER(C.c_uint32), C.c_void_p]
     if path is None:
         _lib = lib
     return lib
@@ -233,3 +248,27 @@ class MtgpContext:
 
     def kernel_timing_reset(self) -> None:
         _check(self.lib, self.lib.mtgp_kernel_timing_reset(self.h))
+
+
+def mt_validate(status: dict) -> None:
+    lib = load_library()
+    _check(lib, lib.mtgp_mt_validate_params(C.byref(MtParamsC(**status))))
+
+
+class MtContext(MtgpContext):
+    """n_sets Engine::mt streams (the reference's own recurrence) on one GPU."""
+
+    def __init__(self, statuses: Sequence[dict], seeds: Sequence[int], device: int = 0,
+                 stream: Optional[int] = None, lib: Optional[C.CDLL] = None):
+        self.lib = lib if lib is not None else load_library()
+        if len(seeds) != len(statuses):
+            raise ValueError("one seed per status")
+        self.sets = list(statuses)
+        self.n_sets = len(statuses)
+        self.N = max(s["n"] for s in statuses)
+        self._params = (MtParamsC * self.n_sets)(*[MtParamsC(**s) for s in statuses])
+        self._seeds = (C.c_uint32 * self.n_sets)(*[int(s) & 0xFFFFFFFF for s in seeds])
+        h = C.c_void_p()
+        _check(self.lib, self.lib.mtgp_mt_ctx_create(C.byref(h), device, self._params, self.n_sets, self._seeds,
+                                                     C.c_void_p(stream or 0)))
+        self.h = h

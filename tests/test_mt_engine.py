@@ -1,0 +1,118 @@
+"""Engine::mt -- the reference's own recurrence on the GPU, bit-exact vs the
+reference compiled from its sources (oracle/_ref) and vs its own goldens
+(proj/tests/test_generator.cpp:11-25)."""
+import numpy as np
+import pytest
+
+import oracle_py
+from paper_1501_07701_b200 import mtgp
+
+
+def _mt_oracle_params(st):
+    return oracle_py.OracleMtParams(st["mexp"], st["n"], st["m"], st["r"], st["a"], st["temper_b"],
+                                    st["temper_c"], st["temper_u"], st["temper_s"], st["temper_t"], st["temper_l"])
+
+
+def _dc(mt_golden, name):
+    f = mt_golden[name]["status12"]
+    keys = ("id", "mexp", "n", "m", "r", "a", "temper_b", "temper_c", "temper_u", "temper_s", "temper_t", "temper_l")
+    return dict(zip(keys, f))
+
+
+# ---------------- CPU: validation mirrors ParameterizedStatus::validate ----------------
+
+def test_mt19937_status_validates():
+    mtgp.mt_validate(mtgp.mt19937_status())
+
+
+@pytest.mark.parametrize("field,value,msg", [
+    ("r", 30, "32\\*n - r must equal mexp"),          # test_generator.cpp:109-112
+    ("id", 7, "low 16 bits"),                          # :113-116
+    ("m", 624, "middle offset"),                       # :117-120
+    ("mexp", 19936, "32\\*n - r must equal mexp"),     # :121-125 (r adjusted below)
+    ("temper_u", 0, "tempering shifts"),
+])
+def test_mt_validate_rejects(field, value, msg):
+    st = mtgp.mt19937_status()
+    st[field] = value
+    if field == "mexp":
+        st["r"] = 32 * st["n"] - value  # keeps 32n - r == mexp; now the exponent itself is unsupported
+        msg = "unsupported period exponent"
+    with pytest.raises(mtgp.MtgpInvalidArgument, match=msg):
+        mtgp.mt_validate(st)
+
+
+# ---------------- GPU parity ----------------
+
+@pytest.mark.gpu
+def test_mt19937_reference_goldens(mt_golden):
+    with mtgp.MtContext([mtgp.mt19937_status()], [5489]) as ctx:
+        w = ctx.fill_u32(1 << 20)[0]
+    assert w[:3].tolist() == [3499211612, 581869302, 3890346734]
+    c = oracle_py.cksum(w)
+    want = mt_golden["mt19937_seed5489_n1048576"]
+    assert (c["sum64"], c["xor32"], c["last"]) == (want["sum64"], want["xor32"], want["last"])
+
+
+@pytest.mark.gpu
+def test_mt_vs_compiled_reference_many_streams():
+    seeds = [0, 1, 5489, 12345, 0xFFFFFFFF] + [oracle_py.lib().oracle_derive_seed(77, j) for j in range(27)]
+    sts = [mtgp.mt19937_status()] * len(seeds)
+    with mtgp.MtContext(sts, seeds) as ctx:
+        a = ctx.fill_u32(5000)
+        b = ctx.fill_u32(12347)
+    for s, seed in enumerate(seeds):
+        ref = oracle_py.ref_fill(5000 + 12347, seed)  # the reference's make_word_source + fill
+        assert np.array_equal(a[s], ref[:5000]) and np.array_equal(b[s], ref[5000:])
+
+
+@pytest.mark.gpu
+def test_mt_dc_statuses_mixed_shapes(mt_golden):
+    """DC-minted statuses (n-m = 10 and 92) next to MT19937 in one context (state stride = max n)."""
+    sts = [_dc(mt_golden, "dc521_id7"), _dc(mt_golden, "dc3217_id7"), mtgp.mt19937_status()]
+    seeds = [4357, 4357, 5489]
+    with mtgp.MtContext(sts, seeds) as ctx:
+        w = ctx.fill_u32(1 << 16)
+    for s in range(2):
+        d = mt_golden[["dc521_id7", "dc3217_id7"][s]]
+        c = oracle_py.cksum(w[s])
+        assert (c["sum64"], c["xor32"], c["last"]) == (d["sum64"], d["xor32"], d["last"])
+        assert np.array_equal(w[s], oracle_py.ref_fill(1 << 16, 4357, d["status12"]))
+    assert np.array_equal(w[2], oracle_py.MtOracle(None, 5489).fill(1 << 16))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", [mtgp.F32_12, mtgp.F32_01OC])
+def test_mt_float_kinds(kind):
+    with mtgp.MtContext([mtgp.mt19937_status()] * 3, [1, 2, 3]) as ctx:
+        w = ctx.generate_host(kind, 20000)
+    for s in range(3):
+        u = oracle_py.MtOracle(None, s + 1).fill(20000)
+        f = ((u >> 9) | 0x3F800000).astype(np.uint32)
+        if kind == mtgp.F32_01OC:
+            f = (np.float32(2.0) - f.view(np.float32)).view(np.uint32)
+        assert np.array_equal(w[s], f)
+
+
+@pytest.mark.gpu
+def test_mt_ragged_state_restore_skip_checksums():
+    st = mtgp.mt19937_status()
+    with mtgp.MtContext([st, st], [11, 12]) as ctx:
+        parts = [ctx.fill_u32(n) for n in (1, 226, 227, 228, 624, 1000)]
+        win, pos = ctx.state_save()
+        x = ctx.fill_u32(999)
+        ctx.state_restore(win, pos)
+        y = ctx.fill_u32(999)
+        assert np.array_equal(x, y)
+        ctx.skip(100003)
+        z = ctx.fill_u32(64)
+        ck = ctx.checksums()
+    total = sum((1, 226, 227, 228, 624, 1000)) + 999 + 999
+    for s in range(2):
+        o = oracle_py.MtOracle(None, 11 + s)
+        ref = o.fill(sum((1, 226, 227, 228, 624, 1000)) + 999)
+        assert np.array_equal(np.concatenate([p[s] for p in parts] + [y[s]]), ref)
+        o2 = oracle_py.MtOracle(None, 11 + s)
+        o2.fill(sum((1, 226, 227, 228, 624, 1000)) + 999 + 100003)
+        assert np.array_equal(z[s], o2.fill(64))
+        assert ck[s][2] == total + 64
