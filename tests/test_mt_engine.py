@@ -36,8 +36,8 @@ def test_mt_validate_rejects(field, value, msg):
     st = mtgp.mt19937_status()
     st[field] = value
     if field == "mexp":
-        st["r"] = 32 * st["n"] - value  # keeps 32n - r == mexp; now the exponent itself is unsupported
-        msg = "unsupported period exponent"
+        st["r"] = 32 * st["n"] - value  # = 32, rejected like the reference (params.cpp:27 before :30)
+        msg = "split position r must be < 32"
     with pytest.raises(mtgp.MtgpInvalidArgument, match=msg):
         mtgp.mt_validate(st)
 
