@@ -74,6 +74,30 @@ struct MtgpStatus {
     bool operator==(const MtgpStatus&) const = default;
 };
 
+/// Engine::mt status: the recurrence fields of the reference's ParameterizedStatus
+/// (proj/include/twistsieve/params.hpp:21-42), generated on the GPU bit-exactly.
+struct MtStatus {
+    std::uint32_t id = 0;
+    std::uint32_t mexp = 0;
+    std::uint32_t n = 0;
+    std::uint32_t m = 0;
+    std::uint32_t r = 0;
+    std::uint32_t a = 0;
+    std::uint32_t temper_b = 0;
+    std::uint32_t temper_c = 0;
+    std::uint32_t temper_u = 11;
+    std::uint32_t temper_s = 7;
+    std::uint32_t temper_t = 15;
+    std::uint32_t temper_l = 18;
+    /// Throws std::invalid_argument like ParameterizedStatus::validate (params.cpp:23-39).
+    void validate() const;
+    mtgp_mt_params to_c() const;
+    bool operator==(const MtStatus&) const = default;
+};
+
+/// The MT19937 preset (proj/src/params.cpp:63-77).
+MtStatus mt19937_status();
+
 /// Stable identifier for reports, e.g. "mtgp11213-id7" (cf. status_display_id, params.hpp:45).
 std::string status_display_id(const MtgpStatus& p);
 
@@ -103,6 +127,8 @@ std::uint32_t derive_seed(std::uint64_t source, std::uint32_t j);
 class StreamBatch {
 public:
     StreamBatch(const std::vector<MtgpStatus>& sets, const std::vector<std::uint32_t>& seeds, int device = 0);
+    /// Engine::mt streams (the reference's classic recurrence).
+    StreamBatch(const std::vector<MtStatus>& sets, const std::vector<std::uint32_t>& seeds, int device = 0);
     ~StreamBatch();
     StreamBatch(const StreamBatch&) = delete;
     StreamBatch& operator=(const StreamBatch&) = delete;
@@ -135,6 +161,9 @@ public:
     /// kind != u32 makes fill() return the stream's single-float bit patterns instead.
     GpuWordSource(const MtgpStatus& params, std::uint32_t seed, OutputKind kind = OutputKind::u32,
                   int device = 0, std::size_t chunk_words = std::size_t{1} << 20);
+    /// Engine::mt stream: the GPU counterpart of MtWordSource itself (word_source.hpp:27-37).
+    GpuWordSource(const MtStatus& params, std::uint32_t seed, OutputKind kind = OutputKind::u32,
+                  int device = 0, std::size_t chunk_words = std::size_t{1} << 20);
     void fill(std::span<std::uint32_t> out) override;
     std::uint32_t next_u32();
     /// next_u32() / 2^32 in [0, 1), draw for draw (generator.hpp:39-41).
@@ -152,5 +181,6 @@ private:
 
 /// Factory with the reference's shape (word_source.cpp:5-16).
 std::unique_ptr<WordSource> make_word_source(const MtgpStatus& params, std::uint32_t seed);
+std::unique_ptr<WordSource> make_word_source(const MtStatus& params, std::uint32_t seed);
 
 }  // namespace twistsieve_b200

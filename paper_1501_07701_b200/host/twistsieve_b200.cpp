@@ -187,6 +187,28 @@ mtgp_params MtgpStatus::to_c() const {
     return c;
 }
 
+void MtStatus::validate() const {
+    const mtgp_mt_params c = to_c();
+    check(mtgp_mt_validate_params(&c), "invalid MT status");
+}
+
+mtgp_mt_params MtStatus::to_c() const {
+    return mtgp_mt_params{id, mexp, n, m, r, a, temper_b, temper_c, temper_u, temper_s, temper_t, temper_l};
+}
+
+MtStatus mt19937_status() {
+    MtStatus p;
+    p.id = 0xB0DF;
+    p.mexp = 19937;
+    p.n = 624;
+    p.m = 397;
+    p.r = 31;
+    p.a = 0x9908B0DF;
+    p.temper_b = 0x9D2C5680;
+    p.temper_c = 0xEFC60000;
+    return p;
+}
+
 std::string status_display_id(const MtgpStatus& p) {
     return "mtgp" + std::to_string(p.mexp) + "-id" + std::to_string(p.id);
 }
@@ -417,6 +439,17 @@ StreamBatch::StreamBatch(const std::vector<MtgpStatus>& sets, const std::vector<
     check(mtgp_ctx_info(ctx_, &n_sets_, &n_, nullptr), "mtgp_ctx_info");
 }
 
+StreamBatch::StreamBatch(const std::vector<MtStatus>& sets, const std::vector<std::uint32_t>& seeds, int device) {
+    if (sets.empty()) throw std::invalid_argument("no parameter sets");
+    if (sets.size() != seeds.size()) throw std::invalid_argument("one seed per parameter set");
+    std::vector<mtgp_mt_params> c;
+    c.reserve(sets.size());
+    for (const auto& s : sets) c.push_back(s.to_c());
+    check(mtgp_mt_ctx_create(&ctx_, device, c.data(), static_cast<std::uint32_t>(c.size()), seeds.data(), nullptr),
+          "mtgp_mt_ctx_create");
+    check(mtgp_ctx_info(ctx_, &n_sets_, &n_, nullptr), "mtgp_ctx_info");
+}
+
 StreamBatch::~StreamBatch() {
     if (ctx_) mtgp_ctx_destroy(ctx_);
 }
@@ -467,6 +500,10 @@ GpuWordSource::GpuWordSource(const MtgpStatus& params, std::uint32_t seed, Outpu
                              std::size_t chunk_words)
     : batch_({params}, {seed}, device), kind_(kind), buf_(std::max<std::size_t>(chunk_words, 256)) {}
 
+GpuWordSource::GpuWordSource(const MtStatus& params, std::uint32_t seed, OutputKind kind, int device,
+                             std::size_t chunk_words)
+    : batch_(std::vector<MtStatus>{params}, {seed}, device), kind_(kind), buf_(std::max<std::size_t>(chunk_words, 256)) {}
+
 void GpuWordSource::refill() {
     batch_.generate_host(kind_, buf_.data(), buf_.size());
     pos_ = 0;
@@ -501,6 +538,10 @@ std::uint32_t GpuWordSource::next_u32() {
 }
 
 std::unique_ptr<WordSource> make_word_source(const MtgpStatus& params, std::uint32_t seed) {
+    return std::make_unique<GpuWordSource>(params, seed);
+}
+
+std::unique_ptr<WordSource> make_word_source(const MtStatus& params, std::uint32_t seed) {
     return std::make_unique<GpuWordSource>(params, seed);
 }
 

@@ -9,6 +9,7 @@
 #include <filesystem>
 #include <fstream>
 #include <functional>
+#include <random>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -144,6 +145,16 @@ int main(int argc, char** argv) {
         CHECK(golden_first32(golden, 199, 0xFFFFFFFFu).size() == 32);
     });
 
+    test_case("Engine::mt status invariants (test_generator.cpp:105-126)", [&] {
+        MtStatus p = mt19937_status();
+        p.validate();
+        CHECK_THROWS_AS([&] { auto q = p; q.r = 30; q.validate(); }(), std::invalid_argument);
+        CHECK_THROWS_AS([&] { auto q = p; q.id = 7; q.validate(); }(), std::invalid_argument);
+        CHECK_THROWS_AS([&] { auto q = p; q.m = q.n; q.validate(); }(), std::invalid_argument);
+        CHECK_THROWS_AS([&] { auto q = p; q.mexp = 19936; q.r = 32 * q.n - 19936; q.validate(); }(),
+                        std::invalid_argument);
+    });
+
     test_case("splitmix64 / derive_seed (word_source.cpp:18-27)", [&] {
         CHECK(splitmix64(0) == 0xE220A8397B1DCDAFull);
         CHECK(derive_seed(10, 3) == static_cast<std::uint32_t>(splitmix64(13)));
@@ -192,6 +203,25 @@ int main(int argc, char** argv) {
             f01.fill(b);
             CHECK(a[0] == 0x3f8ac1d2u && a[1] == 0x3fa3ca34u && a[2] == 0x3fc4f5e7u && a[3] == 0x3fc21b32u);
             CHECK(b[0] == 0x3f6a7c5cu && b[1] == 0x3f386b98u && b[2] == 0x3eec2864u && b[3] == 0x3ef79338u);
+        });
+        test_case("Engine::mt on the GPU matches std::mt19937 (the reference's own oracle, test_generator.cpp:11-25)", [&] {
+            GpuWordSource gen(mt19937_status(), 5489);
+            CHECK(gen.next_u32() == 3499211612u);
+            CHECK(gen.next_u32() == 581869302u);
+            CHECK(gen.next_u32() == 3890346734u);
+            auto mine = make_word_source(mt19937_status(), 5489);
+            std::mt19937 oracle(5489);
+            std::vector<std::uint32_t> w(100000);
+            mine->fill(w);
+            bool eq = true;
+            for (auto v : w) eq = eq && v == oracle();
+            CHECK(eq);
+            // identical seeds give identical outputs (test_generator.cpp:36-40)
+            GpuWordSource a(mt19937_status(), 12345), b(mt19937_status(), 12345);
+            std::vector<std::uint32_t> x(1000000), y(1000000);
+            a.fill(x);
+            b.fill(y);
+            CHECK(x == y);
         });
         test_case("make_word_source factory + StreamBatch checksums + skip", [&] {
             auto src = make_word_source(sets[0], 1);
