@@ -166,6 +166,15 @@ int mtgp_kernel_timing_reset(mtgp_ctx* ctx);
 int mtgp_launch_count(const mtgp_ctx* ctx, uint64_t* launches);
 
 /*
+ * Characteristic-polynomial digests (replaces verify_digest / poly_digest for the MTGP engine,
+ * proj/include/twistsieve/dynamic_creator.hpp:16-51): out receives n_sets NUL-terminated
+ * 41-byte hex SHA-1 strings of each stream's minimal polynomial (Berlekamp-Massey over a
+ * device-generated prefix), printed as '0'/'1' coefficients lowest degree first -- the form
+ * the MTGP tables' poly_sha1 uses (curand_mtgp32.h:140-152). Empty string: none found.
+ */
+int mtgp_charpoly_sha1(mtgp_ctx* ctx, char* out);
+
+/*
  * Engine::mt -- the reference's own generic MT recurrence on the GPU, bit-exact with
  * Generator/MtWordSource (proj/src/generator.cpp:7-13,37-52,68-88). Field meaning is that of
  * ParameterizedStatus (proj/include/twistsieve/params.hpp:21-42).

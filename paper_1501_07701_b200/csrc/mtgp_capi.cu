@@ -497,6 +497,22 @@ int mtgp_skip(mtgp_ctx* ctx, uint64_t words) {
     return MTGP_OK;
 }
 
+int mtgp_charpoly_sha1(mtgp_ctx* ctx, char* out) {
+    if (!ctx || !out) return fail(MTGP_EINVAL, "null argument");
+    if (ctx->engine != 0) return fail(MTGP_EINVAL, "charpoly digests are implemented for MTGP32 contexts");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    std::vector<std::string> d;
+    std::string err;
+    cudaError_t e = ctx->planner->charpoly_sha1(ctx->d_params, ctx->d_win, ctx->stream, d, err);
+    if (e != cudaSuccess) return cuda_fail(e, "charpoly analysis");
+    if (!err.empty()) return fail(MTGP_EINVAL, "%s", err.c_str());
+    for (uint32_t s = 0; s < ctx->n_sets; ++s) {
+        std::memset(out + 41 * s, 0, 41);
+        std::memcpy(out + 41 * s, d[s].data(), std::min<size_t>(40, d[s].size()));
+    }
+    return MTGP_OK;
+}
+
 int mtgp_state_save(mtgp_ctx* ctx, uint32_t* windows, uint64_t* positions) {
     if (!ctx || !windows) return fail(MTGP_EINVAL, "null argument");
     CK(cudaSetDevice(ctx->device), "cudaSetDevice");

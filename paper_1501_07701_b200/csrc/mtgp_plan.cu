@@ -19,6 +19,7 @@
 #include "gf2.h"
 #include "mtgp_plan.h"
 #include "mtgp_v2.cuh"
+#include "sha1.h"
 
 namespace mtgpb {
 
@@ -438,6 +439,23 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     r.pieces = (uint32_t)I.pieces.size();
     r.warps_per_piece = 1;
     return cudaGetLastError();
+}
+
+cudaError_t Planner::charpoly_sha1(const DevParams* params, uint32_t* win, cudaStream_t st,
+                                   std::vector<std::string>& out, std::string& err) {
+    PlannerImpl& I = *impl_;
+    cudaError_t e;
+    if (!I.analyzed && (e = I.analyze(params, win, st, err)) != cudaSuccess) return e;
+    out.assign(I.S, std::string());
+    parallel_for(I.S, [&](size_t s) {
+        if (!I.set_ok[s]) return;
+        const gf2::Poly& P = I.mods[s]->p;
+        std::string c(P.degree() + 1, '0');
+        for (int i = 0; i <= P.degree(); ++i)
+            if (P.coeff(i)) c[i] = '1';
+        out[s] = sha1_hex(c);
+    });
+    return cudaSuccess;
 }
 
 cudaError_t Planner::skip(const DevParams* params, uint32_t* win, uint64_t words, cudaStream_t st, std::string& err) {

@@ -44,6 +44,10 @@ public:
     cudaError_t run(PlanRun& r, std::string& err);
     cudaError_t skip(const DevParams* params, uint32_t* win, uint64_t words, cudaStream_t st,
                      std::string& err);
+    // SHA-1 of each stream's minimal (for certified sets: characteristic) polynomial, printed as
+    // '0'/'1' coefficients lowest degree first; empty where none was found.
+    cudaError_t charpoly_sha1(const DevParams* params, uint32_t* win, cudaStream_t st,
+                              std::vector<std::string>& out, std::string& err);
 
 private:
     std::unique_ptr<PlannerImpl> impl_;

@@ -33,6 +33,7 @@ EXPORTS = (
     "mtgp_skip", "mtgp_state_save", "mtgp_state_restore", "mtgp_checksums",
     "mtgp_checksums_reset", "mtgp_sync", "mtgp_kernel_timing", "mtgp_kernel_timing_reset",
     "mtgp_last_plan", "mtgp_launch_count", "mtgp_mt_validate_params", "mtgp_mt_ctx_create",
+    "mtgp_charpoly_sha1",
 )
 
 
@@ -101,6 +102,7 @@ def load_library(path: Optional[str] = None) -> C.CDLL:
     lib.mtgp_validate_params.argtypes = [C.POINTER(MtgpParamsC)]
     lib.mtgp_launch_count.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
     lib.mtgp_mt_validate_params.argtypes = [C.POINTER(MtParamsC)]
+    lib.mtgp_charpoly_sha1.argtypes = [C.c_void_p, C.c_char_p]
     lib.mtgp_mt_ctx_create.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.POINTER(MtParamsC), C.c_uint32,
                                        C.POINTER(C.c_uint32), C.c_void_p]
     if path is None:
@@ -240,6 +242,13 @@ class MtgpContext:
         g, gl, j, jl = C.c_double(), C.c_uint64(), C.c_double(), C.c_uint64()
         _check(self.lib, self.lib.mtgp_kernel_timing(self.h, C.byref(g), C.byref(gl), C.byref(j), C.byref(jl)))
         return g.value, gl.value, j.value, jl.value
+
+    def charpoly_sha1(self):
+        """SHA-1 of each stream's minimal polynomial ('0'/'1' coefficients, lowest degree first)."""
+        buf = C.create_string_buffer(41 * self.n_sets)
+        _check(self.lib, self.lib.mtgp_charpoly_sha1(self.h, buf))
+        raw = buf.raw
+        return [raw[41 * s:41 * s + 40].split(b"\0")[0].decode() for s in range(self.n_sets)]
 
     def launch_count(self) -> int:
         v = C.c_uint64()

@@ -259,6 +259,15 @@ def test_synthetic_degenerate_sets_jump(mexp):
     assert np.array_equal(w, ref)
 
 
+def test_charpoly_digests_match_the_certified_table(curand_sets):
+    """The BM-derived characteristic polynomial of every cuRAND MTGP32-11213 set, digested the way
+    the MTGP tables do, equals the table's poly_sha1 -- an independent pin of the recurrence,
+    the seeding and the jump-ahead algebra (cf. verify_digest, proj/src/dynamic_creator.cpp:100-103)."""
+    with _ctx(curand_sets, [1] * 200, 0) as ctx:
+        dig = ctx.charpoly_sha1()
+    assert dig == [p.poly_sha1 for p in curand_sets]
+
+
 def test_short_skip_generates(curand_sets):
     sets = curand_sets[5:7]
     with _ctx(sets, [3, 4], 0) as ctx:
