@@ -7,8 +7,11 @@
 #include <cstring>
 #include <vector>
 
+#include <string>
+
 #include "gf2.h"
 #include "oracle.h"
+#include "sha1.h"
 
 using namespace mtgpb::gf2;
 
@@ -95,6 +98,12 @@ int main(int argc, char** argv) {
             if (x[k + 1] >> 31) bits[k >> 6] |= 1ull << (k & 63);
         Poly P = berlekamp_massey(bits, 2 * (size_t)M);
         std::printf("set %d mexp %u: BM degree %d\n", nset, M, P.degree());
+        {
+            std::string coeffs(P.degree() + 1, '0');
+            for (int i = 0; i <= P.degree(); ++i)
+                if (P.coeff(i)) coeffs[i] = '1';
+            std::printf("  digest %s\n", mtgpb::sha1_hex(coeffs).c_str());
+        }
         // annihilation on every bit: sum_i P_i x_{i+j} == 0, j>=1 (j=0: live bits only)
         bool ok = true;
         for (uint32_t j = 0; j < N && ok; ++j) {

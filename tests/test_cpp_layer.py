@@ -50,7 +50,7 @@ def test_cpp_layer_gpu(layer_exe, tmp_path):
 
 def test_gf2_jump_algebra(tmp_path):
     """BM charpoly, Barrett x^o mod P, and jumped windows vs the oracle (certified + synthetic)."""
-    exe = _build(tmp_path, "test_gf2", [ROOT / "tests/cpp/test_gf2.cpp", PKG / "csrc/gf2.cpp"],
+    exe = _build(tmp_path, "test_gf2", [ROOT / "tests/cpp/test_gf2.cpp", PKG / "csrc/gf2.cpp", PKG / "csrc/sha1.cpp"],
                  ["-mpclmul", "-msse4.1", "-x", "c", str(ROOT / "oracle/mtgp32_oracle.c"),
                   str(ROOT / "oracle/mt_oracle.c"), "-x", "none", "-lpthread"])
     sets = tables.load_curand_11213()[:2] + tables.synthetic_sets(44497, 1)
@@ -60,3 +60,6 @@ def test_gf2_jump_algebra(tmp_path):
     r = subprocess.run([str(exe), str(pf)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "BM degree 11213" in r.stdout
+    # the characteristic polynomials of the certified sets digest to the table's poly_sha1
+    digests = [line.split()[1] for line in r.stdout.splitlines() if line.strip().startswith("digest")]
+    assert digests[:2] == [sets[0].poly_sha1, sets[1].poly_sha1]
