@@ -64,15 +64,46 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi sampling during the timed region (the profiling recipe's clocks line)."""
+    """SM clock + throttle reasons sampled DURING the timed region (the profiling recipe's clocks
+    line): NVML in-process every 10 ms; falls back to an nvidia-smi subprocess."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, index: int):
         self.index = index
         self.rows = []
         self.proc = None
         self.t = None
+        self.nv = None
+        self.stop_flag = False
+        self.nvml_rows = []
+
+    def _nvml_loop(self):
+        import pynvml
+        while not self.stop_flag:
+            try:
+                mhz = pynvml.nvmlDeviceGetClockInfo(self.nv, pynvml.NVML_CLOCK_SM)
+                mx = pynvml.nvmlDeviceGetMaxClockInfo(self.nv, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.nv)
+                pw = pynvml.nvmlDeviceGetPowerUsage(self.nv) / 1000.0
+                self.nvml_rows.append((mhz, mx, rs, pw))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.01)
 
     def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.t = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.t.start()
+            return
+        except Exception:  # noqa: BLE001
+            self.nv = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index),
@@ -94,6 +125,22 @@ class ClockSampler:
                 self.rows.append(parts)
 
     def stop(self):
+        if self.nv is not None:
+            import pynvml
+            self.stop_flag = True
+            self.t.join(timeout=2)
+            sm = [r[0] for r in self.nvml_rows]
+            smax = float(self.nvml_rows[-1][1]) if self.nvml_rows else None
+            reasons = set()
+            for r in self.nvml_rows:
+                for name, attr in self.REASONS:
+                    if r[2] & getattr(pynvml, attr, 0):
+                        reasons.add(name)
+            loaded = [v for v in sm if smax and v > 0.5 * smax] or sm
+            return {"sm_mhz": float(np.median(loaded)) if loaded else None, "sm_max_mhz": smax,
+                    "sm_mhz_min": float(min(loaded)) if loaded else None, "reasons": sorted(reasons),
+                    "power_w_max": max((r[3] for r in self.nvml_rows), default=None),
+                    "samples": len(sm), "source": "nvml, 10 ms"}
         if self.proc:
             self.proc.terminate()
             try:
@@ -220,7 +267,15 @@ def main():
     ctx.set_option(mtgp.OPT_TIMING, 1)
     launches0 = ctx.launch_count()
 
-    clocks = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local)
+    nvml_index = local
+    try:  # map the CUDA device to its NVML index (CUDA_VISIBLE_DEVICES may reorder devices)
+        import pynvml
+        pynvml.nvmlInit()
+        uuid = "GPU-" + str(torch.cuda.get_device_properties(local).uuid)
+        nvml_index = pynvml.nvmlDeviceGetIndex(pynvml.nvmlDeviceGetHandleByUUID(uuid))
+    except Exception:  # noqa: BLE001
+        pass
+    clocks = ClockSampler(nvml_index)
     clocks.start()
     if world > 1:
         dist.barrier()
