@@ -287,7 +287,7 @@ cudaError_t PlannerImpl::build_plan(uint64_t L, uint32_t T, uint64_t min_piece, 
         jump_rows.push_back(kv.first);
         for (uint32_t pi : kv.second) {
             pieces[pi].jump_idx = (int32_t)qlist.size();
-            jobs.push_back(JumpJob{pi, (uint32_t)qlist.size()});
+            jobs.push_back(JumpJob{pi, (uint32_t)qlist.size(), (uint32_t)jump_rows.size() - 1});
             qlist.push_back({pi, kv.first});
         }
         job_off.push_back((uint32_t)jobs.size());
@@ -406,6 +406,7 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         ja.q_words = I.q_words;
         ja.piece_win = I.d_pwin.as<uint32_t>();
         ja.max_jobs_per_row = I.max_jobs_per_row;
+        ja.n_jobs = (uint32_t)I.jobs.size();
         if ((e = launch_jump(I.M, ja, (uint32_t)I.jump_rows.size(), r.stream)) != cudaSuccess) return e;
         if (r.timing) {
             r.timing->record(r.stream, &j1);
@@ -490,7 +491,7 @@ cudaError_t Planner::skip(const DevParams* params, uint32_t* win, uint64_t words
     for (uint32_t s = 0; s < I.S; ++s) {
         hrows[s] = s;
         hoff[s] = s;
-        hjobs[s] = JumpJob{s, s};
+        hjobs[s] = JumpJob{s, s, s};
     }
     hoff[I.S] = I.S;
     auto cleanup = [&] {
@@ -519,6 +520,7 @@ cudaError_t Planner::skip(const DevParams* params, uint32_t* win, uint64_t words
         ja.q = q.as<uint32_t>();
         ja.q_words = qw;
         ja.piece_win = out.as<uint32_t>();
+        ja.n_jobs = I.S;
         e = launch_jump(I.M, ja, I.S, st);
     }
     if (e == cudaSuccess) e = cudaMemcpyAsync(win, out.p, (size_t)I.S * I.N * 4, cudaMemcpyDeviceToDevice, st);

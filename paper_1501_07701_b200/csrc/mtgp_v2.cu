@@ -474,8 +474,76 @@ __global__ void __launch_bounds__(kJumpWarps * 32) jump_kernel(JumpArgs a) {
     }
 }
 
+// Flat variant: one warp per job, any mix of streams per CTA, the (L2-resident) prefix read
+// through the read-only L1 path instead of being staged in shared memory -- no shared-memory
+// occupancy limit, so every job runs in the first wave with no idle warps.
+constexpr int kJumpFlatWarps = 4;
+
+template <uint32_t MEXP>
+__global__ void __launch_bounds__(kJumpFlatWarps * 32) jump_flat_kernel(JumpArgs a) {
+    constexpr uint32_t N = MEXP / 32 + 1;
+    constexpr int J = kJumpJ;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t job = blockIdx.x * kJumpFlatWarps + warp;
+    if (job >= a.n_jobs) return;
+    const JumpJob jb = a.jobs[job];
+    const uint4* x4 = reinterpret_cast<const uint4*>(a.pre + (size_t)jb.row * a.pre_stride + a.pre_off);
+    const uint32_t* q = a.q + (size_t)jb.q * a.q_words;
+    uint32_t* dst = a.piece_win + (size_t)jb.piece * N;
+    for (uint32_t j0 = 0; j0 < N; j0 += 32 * J) {
+        const uint32_t jl = j0 + J * lane;  // multiple of 4
+        uint32_t acc[J];
+#pragma unroll
+        for (int k = 0; k < J; ++k) acc[k] = 0;
+        for (uint32_t iw0 = 0; iw0 < a.q_words; iw0 += 32) {
+            const uint32_t qmine = iw0 + lane < a.q_words ? __ldg(q + iw0 + lane) : 0u;
+            const uint32_t nw = min(32u, a.q_words - iw0);
+            for (uint32_t k32 = 0; k32 < nw; ++k32) {
+                const uint32_t qw = __shfl_sync(FULL, qmine, k32);
+                if (qw == 0) continue;
+                const uint32_t base4 = ((iw0 + k32) * 32 + jl) >> 2;
+                uint32_t w[J + 32];
+#pragma unroll
+                for (int v = 0; v < (J + 32) / 4; ++v) {
+                    const uint4 g = __ldg(x4 + base4 + v);
+                    w[4 * v] = g.x;
+                    w[4 * v + 1] = g.y;
+                    w[4 * v + 2] = g.z;
+                    w[4 * v + 3] = g.w;
+                }
+#pragma unroll
+                for (int b = 0; b < 32; b += 2) {
+                    const uint32_t pat = (qw >> b) & 3u;
+                    if (pat == 1) {
+#pragma unroll
+                        for (int k = 0; k < J; ++k) acc[k] ^= w[b + k];
+                    } else if (pat == 2) {
+#pragma unroll
+                        for (int k = 0; k < J; ++k) acc[k] ^= w[b + 1 + k];
+                    } else if (pat == 3) {
+#pragma unroll
+                        for (int k = 0; k < J; ++k) acc[k] ^= w[b + k] ^ w[b + 1 + k];
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < J; ++k)
+            if (jl + k < N) dst[jl + k] = acc[k];
+    }
+}
+
+#ifndef MTGP_JUMP_FLAT
+#define MTGP_JUMP_FLAT 1
+#endif
+
 template <uint32_t MEXP>
 static cudaError_t launch_jump_t(const JumpArgs& a, uint32_t n_rows, cudaStream_t st) {
+    if (MTGP_JUMP_FLAT) {
+        if (a.n_jobs == 0) return cudaSuccess;
+        jump_flat_kernel<MEXP><<<(a.n_jobs + kJumpFlatWarps - 1) / kJumpFlatWarps, kJumpFlatWarps * 32, 0, st>>>(a);
+        return cudaGetLastError();
+    }
     const size_t smem = (size_t)a.pre_len * 4;
     cudaError_t e = cudaFuncSetAttribute(jump_kernel<MEXP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

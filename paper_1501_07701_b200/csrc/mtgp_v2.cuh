@@ -24,6 +24,7 @@ struct GenArgs {
 struct JumpJob {
     uint32_t piece;  // destination: jumped window of this piece
     uint32_t q;      // index of its jump polynomial
+    uint32_t row;    // prefix row (the piece's stream)
 };
 
 struct JumpArgs {
@@ -38,6 +39,7 @@ struct JumpArgs {
     uint32_t q_words;
     uint32_t* piece_win;      // [n_pieces][N]
     uint32_t max_jobs_per_row = 1;
+    uint32_t n_jobs = 0;
 };
 
 // ring size (words) of one warp team for exponent mexp
