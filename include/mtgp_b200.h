@@ -52,6 +52,8 @@ extern "C" {
 #define MTGP_U32 0      /* tempered 32-bit word                                  */
 #define MTGP_F32_12 1   /* single float in [1,2): bits (u32 >> 9) | 0x3F800000   */
 #define MTGP_F32_01OC 2 /* single float in (0,1]: 2.0f - [1,2) value (exact)     */
+#define MTGP_F64_01 3   /* double in [0,1): u32 * 2^-32, draw for draw (Generator::next_f64_01,
+                           proj/include/twistsieve/generator.hpp:39-41); 8 bytes per sample */
 
 /*
  * One MTGP32 parameter set. Field meaning follows mtgp32_params_fast

@@ -372,7 +372,8 @@ int generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
         for (auto& p : ctx->position) p += L;
         return MTGP_OK;
     }
-    const bool use_v1 = ctx->kernel == 1 || !ctx->planner->v2_supported();
+    // doubles (8 B/sample, the reference's next_f64_01) are produced by the stream-per-CTA kernel
+    const bool use_v1 = ctx->kernel == 1 || !ctx->planner->v2_supported() || kind == MTGP_F64_01;
     if (use_v1) {
         size_t e0 = 0, e1 = 0;
         if (ctx->timing) ctx->pool.record(ctx->stream, &e0);
@@ -420,7 +421,7 @@ extern "C" {
 
 int mtgp_generate(mtgp_ctx* ctx, int kind, void* out, uint64_t L, int out_is_device) {
     if (!ctx) return fail(MTGP_EINVAL, "null context");
-    if (kind < MTGP_U32 || kind > MTGP_F32_01OC) return fail(MTGP_EINVAL, "unknown output kind %d", kind);
+    if (kind < MTGP_U32 || kind > MTGP_F64_01) return fail(MTGP_EINVAL, "unknown output kind %d", kind);
     if (!out && L) return fail(MTGP_EINVAL, "null output");
     CK(cudaSetDevice(ctx->device), "cudaSetDevice");
     if (out_is_device) return generate_device(ctx, kind, out, L);
@@ -428,8 +429,9 @@ int mtgp_generate(mtgp_ctx* ctx, int kind, void* out, uint64_t L, int out_is_dev
     // Host output: generate chunks of Lc words per stream into a double-buffered device stage
     // and copy each chunk out with one strided 2-D copy, overlapping generation of chunk c+1
     // with the copy of chunk c.
+    const size_t es = kind == MTGP_F64_01 ? 8 : 4;  // bytes per sample
     const uint64_t Lc = std::min<uint64_t>(L, ctx->host_chunk);
-    const size_t chunk_bytes = (size_t)Lc * ctx->n_sets * 4;
+    const size_t chunk_bytes = (size_t)Lc * ctx->n_sets * es;
     if (ctx->stage_bytes < 2 * chunk_bytes) {
         CK(cudaStreamSynchronize(ctx->copy_stream), "sync");
         cudaFree(ctx->d_stage);
@@ -450,7 +452,7 @@ int mtgp_generate(mtgp_ctx* ctx, int kind, void* out, uint64_t L, int out_is_dev
         if (rc) return rc;
         CK(cudaEventRecord(ctx->ev_gen[b], ctx->stream), "event");
         CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_gen[b], 0), "wait");
-        CK(cudaMemcpy2DAsync(host + done * 4, (size_t)L * 4, stage, (size_t)len * 4, (size_t)len * 4,
+        CK(cudaMemcpy2DAsync(host + done * es, (size_t)L * es, stage, (size_t)len * es, (size_t)len * es,
                              ctx->n_sets, cudaMemcpyDeviceToHost, ctx->copy_stream),
            "D2H copy");
         CK(cudaEventRecord(ctx->ev_copy[b], ctx->copy_stream), "event");

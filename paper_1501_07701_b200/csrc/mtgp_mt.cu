@@ -50,11 +50,16 @@ __global__ void __launch_bounds__(256) mt_v1_kernel(const DevMtParams* __restric
             v ^= (v << p.s) & p.b;
             v ^= (v << p.t) & p.c;
             v ^= v >> p.l;
-            if (KIND != MTGP_U32) {
-                v = (v >> 9) | 0x3F800000u;
-                if (KIND == MTGP_F32_01OC) v = __float_as_uint(2.0f - __uint_as_float(v));
+            if (KIND == MTGP_F64_01) {
+                // Generator::next_f64_01: u32 * 2^-32 (proj/include/twistsieve/generator.hpp:39-41)
+                __stcs(reinterpret_cast<double*>(out) + (size_t)set * L + base + t, (double)v * 0x1p-32);
+            } else {
+                if (KIND != MTGP_U32) {
+                    v = (v >> 9) | 0x3F800000u;
+                    if (KIND == MTGP_F32_01OC) v = __float_as_uint(2.0f - __uint_as_float(v));
+                }
+                __stcs(o + base + t, v);
             }
-            __stcs(o + base + t, v);
             if (CK) {
                 sum += v;
                 xr ^= v;
@@ -102,6 +107,8 @@ cudaError_t launch_mt_v1(int kind, bool cksum, const DevMtParams* params, uint32
         case 3: return launch_mt_t<MTGP_F32_12, true>(params, win, n_sets, nmax, out, L, ck, st);
         case 4: return launch_mt_t<MTGP_F32_01OC, false>(params, win, n_sets, nmax, out, L, ck, st);
         case 5: return launch_mt_t<MTGP_F32_01OC, true>(params, win, n_sets, nmax, out, L, ck, st);
+        case 6: return launch_mt_t<MTGP_F64_01, false>(params, win, n_sets, nmax, out, L, ck, st);
+        case 7: return launch_mt_t<MTGP_F64_01, true>(params, win, n_sets, nmax, out, L, ck, st);
     }
     return cudaErrorInvalidValue;
 }

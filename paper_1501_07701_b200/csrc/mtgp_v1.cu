@@ -60,11 +60,16 @@ __global__ void __launch_bounds__(256) mtgp_v1_kernel(const DevParams* __restric
             tt ^= tt >> 16;
             tt ^= tt >> 8;
             uint32_t v = r ^ s_tmp[tt & 15u];
-            if (KIND != MTGP_U32) {
-                v = (v >> 9) | 0x3F800000u;
-                if (KIND == MTGP_F32_01OC) v = __float_as_uint(2.0f - __uint_as_float(v));
+            if (KIND == MTGP_F64_01) {
+                // next_f64_01: u32 * 2^-32 (proj/include/twistsieve/generator.hpp:39-41)
+                __stcs(reinterpret_cast<double*>(out) + (size_t)set * L + base + t, (double)v * 0x1p-32);
+            } else {
+                if (KIND != MTGP_U32) {
+                    v = (v >> 9) | 0x3F800000u;
+                    if (KIND == MTGP_F32_01OC) v = __float_as_uint(2.0f - __uint_as_float(v));
+                }
+                __stcs(o + base + t, v);
             }
-            __stcs(o + base + t, v);
             if (CKSUM) {
                 sum += v;
                 xr ^= v;
@@ -114,6 +119,8 @@ cudaError_t launch_v1(int kind, bool cksum, const DevParams* params, uint32_t* w
         case 3: return launch_v1_t<MTGP_F32_12, true>(params, win, n_sets, N, out, L, ck, st);
         case 4: return launch_v1_t<MTGP_F32_01OC, false>(params, win, n_sets, N, out, L, ck, st);
         case 5: return launch_v1_t<MTGP_F32_01OC, true>(params, win, n_sets, N, out, L, ck, st);
+        case 6: return launch_v1_t<MTGP_F64_01, false>(params, win, n_sets, N, out, L, ck, st);
+        case 7: return launch_v1_t<MTGP_F64_01, true>(params, win, n_sets, N, out, L, ck, st);
     }
     return cudaErrorInvalidValue;
 }

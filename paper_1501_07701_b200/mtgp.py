@@ -22,7 +22,7 @@ _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libmtgp_b200.so"
 
 MTGP_OK, MTGP_EINVAL, MTGP_ECUDA, MTGP_ENOMEM, MTGP_ESTATE = 0, 1, 2, 3, 4
-U32, F32_12, F32_01OC = 0, 1, 2
+U32, F32_12, F32_01OC, F64_01 = 0, 1, 2, 3
 OPT_CHECKSUM, OPT_KERNEL, OPT_MAX_PIECES, OPT_MIN_PIECE_WORDS, OPT_TIMING, OPT_HOST_CHUNK = 1, 2, 3, 4, 5, 6
 
 # Every symbol include/mtgp_b200.h declares (checked by the CPU test suite).
@@ -196,10 +196,12 @@ class MtgpContext:
         _check(self.lib, self.lib.mtgp_generate(self.h, kind, C.c_void_p(ptr), words_per_stream, 1))
 
     def generate_host(self, kind: int, words_per_stream: int, out: Optional[np.ndarray] = None) -> np.ndarray:
-        """Synchronous generation into host memory; returns an (n_sets, L) uint32 array."""
+        """Synchronous generation into host memory; returns an (n_sets, L) array (uint32 bit
+        patterns for the u32/f32 kinds, float64 for F64_01)."""
+        dt = np.float64 if kind == F64_01 else np.uint32
         if out is None:
-            out = np.empty((self.n_sets, words_per_stream), dtype=np.uint32)
-        assert out.dtype == np.uint32 and out.flags.c_contiguous and out.size == self.n_sets * words_per_stream
+            out = np.empty((self.n_sets, words_per_stream), dtype=dt)
+        assert out.dtype == dt and out.flags.c_contiguous and out.size == self.n_sets * words_per_stream
         _check(self.lib, self.lib.mtgp_generate(self.h, kind, out.ctypes.data_as(C.c_void_p),
                                                 words_per_stream, 0))
         return out

@@ -259,6 +259,19 @@ def test_synthetic_degenerate_sets_jump(mexp):
     assert np.array_equal(w, ref)
 
 
+def test_f64_01_matches_next_f64_01(curand_sets):
+    """MTGP_F64_01 = u32 * 2^-32 draw for draw, like Generator::next_f64_01 (generator.hpp:39-41)."""
+    sets = curand_sets[:3]
+    with _ctx(sets, [1, 2, 3], 0) as ctx:
+        d = ctx.generate_host(mtgp.F64_01, 30001)
+        u = ctx.fill_u32(5)  # the stream continues after the doubles
+    for s in range(3):
+        ref = oracle_py.MtgpOracle(sets[s], s + 1).fill(30006)
+        assert np.array_equal(d[s], ref[:30001].astype(np.float64) * (1.0 / 4294967296.0))
+        assert np.array_equal(u[s], ref[30001:])
+    assert d.min() >= 0.0 and d.max() < 1.0
+
+
 def test_charpoly_digests_match_the_certified_table(curand_sets):
     """The BM-derived characteristic polynomial of every cuRAND MTGP32-11213 set, digested the way
     the MTGP tables do, equals the table's poly_sha1 -- an independent pin of the recurrence,

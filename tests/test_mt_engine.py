@@ -95,6 +95,16 @@ def test_mt_float_kinds(kind):
 
 
 @pytest.mark.gpu
+def test_mt_next_f64_01():
+    """next_f64_01 == next_u32 / 2^32 draw for draw (proj/tests/test_generator.cpp:90-103)."""
+    with mtgp.MtContext([mtgp.mt19937_status()], [99]) as ctx:
+        d = ctx.generate_host(mtgp.F64_01, 10000)[0]
+    u = oracle_py.MtOracle(None, 99).fill(10000)
+    assert np.array_equal(d, u.astype(np.float64) * (1.0 / 4294967296.0))
+    assert d.min() >= 0.0 and d.max() < 1.0
+
+
+@pytest.mark.gpu
 def test_mt_ragged_state_restore_skip_checksums():
     st = mtgp.mt19937_status()
     with mtgp.MtContext([st, st], [11, 12]) as ctx:
