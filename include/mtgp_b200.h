@@ -203,6 +203,78 @@ int mtgp_mt_ctx_create(mtgp_ctx** out, int device, const mtgp_mt_params* sets, u
 int mtgp_last_plan(const mtgp_ctx* ctx, uint32_t* pieces, uint32_t* warps_per_piece,
                    uint32_t* kernel_version);
 
+/* ------------------------------------------------------------------------------------------
+ * Device-side statistical tests (GPU-fed consumers).
+ *
+ * The reference runs each campaign cell (status, seed, test) as run_test(BufferedStream over a
+ * fresh make_word_source(status, seed)) (proj/src/sieve.cpp:156-158) with the four templates of
+ * proj/include/twistsieve/stat_tests.hpp:83-309. mtgp_stat_run does the same for every stream
+ * of a context at once: the words are generated and counted on the GPU (they never leave HBM),
+ * and the host turns the integer counts into the statistic, p-value and class with a
+ * restatement of the reference's numerics (proj/src/stats.cpp, classify.cpp). Counts are
+ * bit-exact with the reference templates over the same words, and so are statistic and p-value
+ * (same arithmetic in the same order).
+ * ------------------------------------------------------------------------------------------ */
+#define MTGP_STAT_GAP 0            /* gap_test            stat_tests.hpp:83-138  */
+#define MTGP_STAT_HAMMING_INDEP 1  /* hamming_indep_test  stat_tests.hpp:149-208 */
+#define MTGP_STAT_COLLISION_OVER 2 /* collision_over_test stat_tests.hpp:214-248 */
+#define MTGP_STAT_RANDOM_WALK 3    /* random_walk_test    stat_tests.hpp:253-309 */
+
+/* PValueClass (proj/include/twistsieve/classify.hpp:11) */
+#define MTGP_PCLASS_CORRECT 0
+#define MTGP_PCLASS_SUSPECT 1
+#define MTGP_PCLASS_DISASTROUS 2
+
+/* per-stream result error codes */
+#define MTGP_STAT_OK 0
+#define MTGP_STAT_EXHAUSTED 2      /* StreamExhausted ("insufficient stream"), word_source.hpp:15-17 */
+
+/* TestSpec (stat_tests.hpp:18-33); `test` replaces the test_id string. */
+typedef struct mtgp_stat_spec {
+    int32_t test;
+    uint32_t N;      /* replication count (kept at 1) */
+    uint64_t n;      /* gaps / blocks / pairs / walks */
+    uint32_t r, s, L, d, l, t;
+    double alpha, beta;
+} mtgp_stat_spec;
+
+/* TestResult (stat_tests.hpp:35-42) for one stream, plus the words the test consumed. */
+typedef struct mtgp_stat_result {
+    double statistic, p_value;
+    int32_t classification, degenerate;
+    int32_t error;   /* MTGP_STAT_OK or MTGP_STAT_EXHAUSTED (then the other fields are 0) */
+    int32_t pad;
+    uint64_t words_used;
+} mtgp_stat_result;
+
+/* TestSpec::validate (stat_tests.cpp:7-30) plus each test's pre-consumption checks ("sample
+   too small", "spec out of sparse regime"); MTGP_EINVAL with the reference's message. */
+int mtgp_stat_validate(const mtgp_stat_spec* spec);
+
+/* Runs the test on every stream of ctx, each from the context's current position; results[s]
+   for stream s. The context's state and checksums are left unchanged. */
+int mtgp_stat_run(mtgp_ctx* ctx, const mtgp_stat_spec* spec, mtgp_stat_result* results);
+
+/* The host half alone: result from a test's integer counts. Layout: gap tcut+1 gap-length
+   counts; hamming_indep {table[0][0], [0][1], [1][0], [1][1]}; collision_over {collisions};
+   random_walk l+1 right-step counts. *n_counts from mtgp_stat_counts_len. */
+int mtgp_stat_counts_len(const mtgp_stat_spec* spec, uint64_t* n_counts);
+int mtgp_stat_finish(const mtgp_stat_spec* spec, const uint64_t* counts, uint64_t n_counts,
+                     mtgp_stat_result* result);
+
+/* The numerics (proj/include/twistsieve/stats.hpp, classify.hpp); MTGP_EINVAL where the
+   reference throws std::invalid_argument. */
+int mtgp_ln_gamma(double x, double* out);
+int mtgp_gamma_p(double a, double x, double* out);
+int mtgp_gamma_q(double a, double x, double* out);
+int mtgp_chi_square_pvalue(double statistic, uint32_t df, double* out);
+int mtgp_poisson_cdf(uint64_t k, double lambda, double* out);
+int mtgp_poisson_sf(uint64_t k, double lambda, double* out);
+int mtgp_poisson_pmf(uint64_t k, double lambda, double* out);
+int mtgp_binomial_log_pmf(uint64_t k, uint64_t n, double p, double* out);
+int mtgp_binomial_upper_tail(uint64_t count, uint64_t n, double p, double* out);
+int mtgp_classify_pvalue(double p, int32_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,68 @@
+// mtgp_ctx.h -- the context object behind the C-ABI handle (private to libmtgp_b200.so), shared
+// by the API translation units (mtgp_capi.cu, mtgp_stat.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "mtgp_b200.h"
+#include "mtgp_internal.cuh"
+#include "mtgp_mt.cuh"
+#include "mtgp_plan.h"
+
+using mtgpb::DevCksum;
+using mtgpb::DevMtParams;
+using mtgpb::DevParams;
+using mtgpb::EventPool;
+using mtgpb::Planner;
+
+struct mtgp_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    bool own_stream = false;
+    uint32_t n_sets = 0, N = 0, mexp = 0;
+    int engine = 0;  // 0 = MTGP32, 1 = Engine::mt (the reference's classic recurrence)
+    std::vector<mtgp_params> sets;
+    std::vector<mtgp_mt_params> mt_sets;
+    std::vector<uint64_t> position;
+    DevMtParams* d_mt = nullptr;
+
+    DevParams* d_params = nullptr;
+    uint32_t* d_win = nullptr;
+    DevCksum* d_ck = nullptr;
+
+    // options
+    bool cksum = true;
+    int kernel = 0;
+    uint32_t max_pieces = 0;
+    uint64_t min_piece_words = 1ull << 21;
+    bool timing = false;
+    uint64_t host_chunk = 1ull << 20;
+
+    // host-output staging
+    void* d_stage = nullptr;
+    size_t stage_bytes = 0;
+    cudaEvent_t ev_gen[2] = {nullptr, nullptr};
+    cudaEvent_t ev_copy[2] = {nullptr, nullptr};
+
+    // timing
+    EventPool pool;
+    double gen_ms = 0, jump_ms = 0;
+    uint64_t gen_launches = 0, jump_launches = 0;
+    uint64_t total_launches = 0;  // every kernel this context launched
+
+    // v2 planner / jump-ahead state
+    std::unique_ptr<Planner> planner;
+    uint32_t last_pieces = 0, last_warps = 0, last_kernel = 0;
+};
+
+namespace mtgpb {
+// Sets the thread-local mtgp_last_error() message; returns `code`.
+int set_error(int code, const char* fmt, ...);
+int cuda_error(cudaError_t e, const char* what);
+// One device-side generation of L words per stream into device memory `out` (advances positions).
+int ctx_generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L);
+}  // namespace mtgpb

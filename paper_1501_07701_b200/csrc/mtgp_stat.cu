@@ -1,0 +1,637 @@
+// mtgp_stat.cu -- device-side statistical tests over generated streams.
+//
+// The reference runs a campaign cell as run_test(BufferedStream(make_word_source(status, seed)))
+// (proj/src/sieve.cpp:156-158): a fresh stream per (status, seed, test), consumed word by word by
+// one of four templates (proj/include/twistsieve/stat_tests.hpp:84-309). Here every stream of a
+// context is tested at once: the context generates the next C words of all S streams into one
+// HBM chunk (its normal generation kernels), a counting kernel folds the chunk into per-stream
+// integer counts, and the chunk buffer is reused. Words never leave the GPU; the host only turns
+// the final counts into statistic / p-value / class (stat_host.cpp).
+//
+// Chunk sizes are whole multiples of each test's unit (walks; pairs of L-bit blocks), so the
+// fixed-length tests need no state across chunks. The gap test is data-dependent (it reads until
+// the n-th gap closes, within a word budget); it carries {hits so far, last hit position} per
+// stream and finds hit ordinals with a per-chunk tile scan. Counts are exact integers, so results
+// are bit-identical to the reference templates over the same words.
+//
+// All four kernels read each word once (coalesced) and do O(1) work per word: HBM/L2-read bound,
+// cheap next to generation. Roofline note in DESIGN.md §4.5.
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+#include <vector>
+
+#include "mtgp_ctx.h"
+#include "stat_host.h"
+
+namespace mtgpb {
+namespace {
+
+constexpr uint32_t kThreads = 256;
+constexpr uint32_t kWarps = kThreads / 32;
+constexpr uint32_t kFull = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t letter_of(uint32_t w, uint32_t r, uint32_t s) {
+    // detail::letter_of (stat_tests.hpp:60-63): the s most significant bits left after dropping r
+    return (w >> (32u - r - s)) & ((1u << s) - 1u);
+}
+
+__device__ __forceinline__ uint32_t low_mask(uint32_t k) { return k >= 32 ? kFull : ((1u << k) - 1u); }
+
+// popcount of bits [a, e) of a bitmap (bit i of word q is item 32q + i), a < e
+__device__ uint32_t range_popc(const uint32_t* bm, uint32_t a, uint32_t e) {
+    const uint32_t qa = a >> 5, qe = (e - 1) >> 5, sa = a & 31u;
+    if (qa == qe) return __popc((bm[qa] >> sa) & low_mask(e - a));
+    uint32_t h = __popc(bm[qa] >> sa);
+    for (uint32_t q = qa + 1; q < qe; ++q) h += __popc(bm[q]);
+    return h + __popc(bm[qe] & low_mask(((e - 1) & 31u) + 1));
+}
+
+// ---------------------------------------------------------------------------------------------
+// random walk (stat_tests.hpp:253-309): walk i = words [i l, (i+1) l); H = number of odd words.
+// A CTA takes wpt whole walks: bit 0 of its words -> shared bitmap by warp ballots (coalesced
+// loads), then one thread per walk popcounts its bit range.
+template <bool SMEM_HIST>
+__global__ void __launch_bounds__(kThreads) walk_kernel(const uint32_t* __restrict__ w, uint64_t C, uint32_t l,
+                                                        uint32_t wpt, uint64_t walk0, uint64_t n,
+                                                        unsigned long long* __restrict__ counts) {
+    extern __shared__ uint32_t sm[];
+    const uint32_t tile_words = wpt * l;
+    const uint32_t nbm = (tile_words + 31) / 32;
+    uint32_t* bm = sm;
+    uint32_t* hist = sm + nbm;
+    const uint32_t st = blockIdx.y;
+    const uint64_t first_walk = walk0 + (uint64_t)blockIdx.x * wpt;
+    if (first_walk >= n) return;
+    const uint32_t* src = w + (size_t)st * C + (size_t)blockIdx.x * tile_words;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    if (SMEM_HIST)
+        for (uint32_t i = threadIdx.x; i <= l; i += kThreads) hist[i] = 0;
+    for (uint32_t q = warp; q < nbm; q += kWarps) {
+        const uint32_t j = q * 32 + lane;
+        const uint32_t odd = j < tile_words ? (__ldg(src + j) & 1u) : 0u;
+        const uint32_t b = __ballot_sync(kFull, odd);
+        if (lane == 0) bm[q] = b;
+    }
+    __syncthreads();
+    unsigned long long* cs = counts + (size_t)st * (l + 1);
+    for (uint32_t t = threadIdx.x; t < wpt && first_walk + t < n; t += kThreads) {
+        const uint32_t h = range_popc(bm, t * l, t * l + l);
+        if (SMEM_HIST)
+            atomicAdd(hist + h, 1u);
+        else
+            atomicAdd(cs + h, 1ull);
+    }
+    if (SMEM_HIST) {
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i <= l; i += kThreads)
+            if (hist[i]) atomicAdd(cs + i, (unsigned long long)hist[i]);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Hamming-weight independence (stat_tests.hpp:149-208): s-bit letters concatenated MSB first
+// into L-bit blocks; blocks (2i, 2i+1) form pair i. A CTA takes ppt whole pairs (tile_words
+// words, a multiple of the pair unit 2L/gcd(2L, s)): letters and an exclusive prefix sum of
+// their popcounts go to shared memory, then each block's weight is O(1): the partial first
+// letter + prefix difference + the partial last letter.
+__global__ void __launch_bounds__(kThreads) hamming_kernel(const uint32_t* __restrict__ w, uint64_t C, uint32_t r,
+                                                           uint32_t sb, uint32_t L, uint32_t ppt,
+                                                           uint32_t tile_words, uint64_t pair0, uint64_t npairs,
+                                                           unsigned long long* __restrict__ table) {
+    extern __shared__ uint32_t sm[];
+    uint32_t* let = sm;               // [tile_words]
+    uint32_t* pre = sm + tile_words;  // [tile_words + 1], pre[j] = sum_{i<j} popc(let[i])
+    __shared__ uint32_t warp_tot[kWarps];
+    __shared__ uint32_t cat[4];
+    const uint32_t st = blockIdx.y;
+    const uint64_t first_pair = pair0 + (uint64_t)blockIdx.x * ppt;
+    if (first_pair >= npairs) return;
+    const uint32_t* src = w + (size_t)st * C + (size_t)blockIdx.x * tile_words;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    if (threadIdx.x < 4) cat[threadIdx.x] = 0;
+    for (uint32_t j = threadIdx.x; j < tile_words; j += kThreads) let[j] = letter_of(__ldg(src + j), r, sb);
+    __syncthreads();
+
+    // block-wide exclusive scan over contiguous per-thread segments
+    const uint32_t ipt = (tile_words + kThreads - 1) / kThreads;
+    const uint32_t j0 = min(threadIdx.x * ipt, tile_words), j1 = min(j0 + ipt, tile_words);
+    uint32_t own = 0;
+    for (uint32_t j = j0; j < j1; ++j) own += __popc(let[j]);
+    uint32_t incl = own;
+    for (uint32_t d = 1; d < 32; d <<= 1) {
+        const uint32_t v = __shfl_up_sync(kFull, incl, d);
+        if (lane >= d) incl += v;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    uint32_t run = incl - own;
+    for (uint32_t i = 0; i < warp; ++i) run += warp_tot[i];
+    for (uint32_t j = j0; j < j1; ++j) {
+        pre[j] = run;
+        run += __popc(let[j]);
+    }
+    if (threadIdx.x == kThreads - 1) pre[tile_words] = run;
+    __syncthreads();
+
+    const uint32_t half = L / 2;
+    for (uint32_t pp = threadIdx.x; pp < ppt && first_pair + pp < npairs; pp += kThreads) {
+        uint32_t sign[2];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const uint32_t B = (2 * pp + b) * L, E = B + L;  // local bit range [B, E)
+            const uint32_t jf = B / sb, of = B - jf * sb;     // first letter, bits already taken
+            const uint32_t jl = (E - 1) / sb, eo = E - jl * sb;  // last letter, bits taken from it
+            uint32_t wt;
+            if (jf == jl)
+                wt = __popc((let[jf] >> (sb - eo)) & low_mask(eo - of));
+            else
+                wt = __popc(let[jf] & low_mask(sb - of)) + (pre[jl] - pre[jf + 1]) + __popc(let[jl] >> (sb - eo));
+            sign[b] = wt > half ? 1u : 0u;
+        }
+        atomicAdd(&cat[sign[0] * 2 + sign[1]], 1u);  // table[first_sign][second_sign]
+    }
+    __syncthreads();
+    if (threadIdx.x < 4 && cat[threadIdx.x])
+        atomicAdd(table + (size_t)st * 4 + threadIdx.x, (unsigned long long)cat[threadIdx.x]);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Overlapping-pairs collisions (stat_tests.hpp:214-248): cell i = letter(w_i) << s | letter(w_i+1),
+// i < n; a collision is a visit to an occupied cell. The count n - |distinct cells| does not
+// depend on visiting order, so cells are marked with atomicOr in a per-stream 2^(2s)-bit map.
+// The word before the chunk comes from the previous chunk (prev_in / prev_out ping-pong).
+__global__ void __launch_bounds__(kThreads) opso_kernel(const uint32_t* __restrict__ w, uint64_t C, uint64_t P,
+                                                        uint32_t r, uint32_t sb, uint64_t n,
+                                                        uint32_t* __restrict__ bitmap, uint64_t bm_words,
+                                                        const uint32_t* __restrict__ prev_in,
+                                                        uint32_t* __restrict__ prev_out,
+                                                        unsigned long long* __restrict__ coll) {
+    const uint32_t st = blockIdx.y;
+    const uint32_t* src = w + (size_t)st * C;
+    uint32_t* bmp = bitmap + (size_t)st * bm_words;
+    uint32_t mine = 0;
+    for (uint64_t j = (uint64_t)blockIdx.x * kThreads + threadIdx.x; j < C; j += (uint64_t)gridDim.x * kThreads) {
+        const uint32_t cur_w = __ldg(src + j);
+        if (j == C - 1) prev_out[st] = cur_w;
+        const uint64_t g = P + j;  // global word index; it closes cell g - 1
+        if (g == 0 || g - 1 >= n) continue;
+        const uint32_t prv_w = j ? __ldg(src + j - 1) : prev_in[st];
+        const uint32_t cell = (letter_of(prv_w, r, sb) << sb) | letter_of(cur_w, r, sb);
+        const uint32_t bit = 1u << (cell & 31u);
+        mine += (atomicOr(bmp + (cell >> 5), bit) & bit) ? 1u : 0u;
+    }
+    for (int d = 16; d > 0; d >>= 1) mine += __shfl_xor_sync(kFull, mine, d);
+    if ((threadIdx.x & 31u) == 0 && mine) atomicAdd(coll + st, (unsigned long long)mine);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Gap test (stat_tests.hpp:84-138). Hits h_0 < h_1 < ... are the words whose kept bits fall in
+// [alpha, beta) (integer thresholds lo <= v < hi); gap k = h_k - h_{k-1} - 1 for k = 1..n goes to
+// bin min(gap, tcut). Only words below the budget count (the reference throws StreamExhausted
+// when it would read word `budget`). Per chunk: (1) per-tile hit count / first / last,
+// (2) per-tile ordinal base from a scan of the earlier tiles plus the stream's carried state,
+// then the tile's gaps, (3) per-stream state update.
+constexpr uint32_t kGapTile = 4096;                   // words per CTA
+constexpr uint32_t kGapGroups = kGapTile / kThreads;  // 32-word groups per warp (16)
+
+struct GapTile {
+    uint32_t count;
+    int32_t first, last;  // CHUNK-local word index of the tile's first / last hit, -1 if none
+};
+
+struct GapState {
+    unsigned long long hits;  // hits seen so far (h_0 included)
+    long long last_hit;       // global index of the last hit, -1 if none
+    unsigned long long end;   // global index of h_n once done
+    uint32_t done, exhausted;
+};
+
+__device__ __forceinline__ uint32_t gap_ballot(const uint32_t* src, uint64_t j, uint64_t g, uint32_t mask, uint64_t lo,
+                                               uint64_t hi, uint64_t budget) {
+    const uint64_t v = __ldg(src + j) & mask;
+    return __ballot_sync(kFull, g < budget && v >= lo && v < hi);
+}
+
+__global__ void __launch_bounds__(kThreads) gap_count_kernel(const uint32_t* __restrict__ w, uint64_t C, uint64_t P,
+                                                             uint32_t mask, uint64_t lo, uint64_t hi, uint64_t budget,
+                                                             const GapState* __restrict__ state,
+                                                             GapTile* __restrict__ tiles, uint32_t T) {
+    __shared__ uint32_t wc[kWarps];
+    __shared__ int32_t wf[kWarps], wl[kWarps];
+    const uint32_t st = blockIdx.y, tile = blockIdx.x;
+    if (state[st].done) {
+        if (threadIdx.x == 0) tiles[(size_t)st * T + tile] = GapTile{0, -1, -1};
+        return;
+    }
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t* src = w + (size_t)st * C;
+    const uint32_t base = tile * kGapTile + warp * (kGapGroups * 32);
+    uint32_t cnt = 0;
+    int32_t first = -1, last = -1;
+    for (uint32_t g = 0; g < kGapGroups; ++g) {
+        const uint32_t j = base + g * 32;
+        const uint32_t m = gap_ballot(src, j + lane, P + j + lane, mask, lo, hi, budget);
+        if (m) {
+            cnt += __popc(m);
+            if (first < 0) first = (int32_t)(j + __ffs(m) - 1);
+            last = (int32_t)(j + 31 - __clz(m));
+        }
+    }
+    if (lane == 0) {
+        wc[warp] = cnt;
+        wf[warp] = first;
+        wl[warp] = last;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        GapTile t{0, -1, -1};
+        for (uint32_t i = 0; i < kWarps; ++i) {
+            t.count += wc[i];
+            if (t.first < 0) t.first = wf[i];
+            if (wl[i] >= 0) t.last = wl[i];
+        }
+        tiles[(size_t)st * T + tile] = t;
+    }
+}
+
+template <bool SMEM_HIST>
+__global__ void __launch_bounds__(kThreads) gap_hist_kernel(const uint32_t* __restrict__ w, uint64_t C, uint64_t P,
+                                                            uint32_t mask, uint64_t lo, uint64_t hi, uint64_t budget,
+                                                            const GapState* __restrict__ state,
+                                                            const GapTile* __restrict__ tiles, uint32_t T, uint64_t n,
+                                                            uint32_t tcut, unsigned long long* __restrict__ counts,
+                                                            unsigned long long* __restrict__ end_pos) {
+    extern __shared__ uint32_t hist[];
+    __shared__ unsigned long long s_base;
+    __shared__ long long s_prev;
+    __shared__ uint32_t wc[kWarps];
+    __shared__ int32_t wl[kWarps];
+    const uint32_t st = blockIdx.y, tile = blockIdx.x;
+    const GapState S0 = state[st];
+    if (S0.done || tiles[(size_t)st * T + tile].count == 0) return;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    if (warp == 0) {
+        // ordinal of this tile's first hit, and the hit before it
+        unsigned long long sum = 0;
+        long long prev = -1;
+        for (uint32_t t = lane; t < tile; t += 32) {
+            const GapTile g = tiles[(size_t)st * T + t];
+            sum += g.count;
+            if (g.count) prev = max(prev, (long long)g.last);
+        }
+        for (int d = 16; d > 0; d >>= 1) {
+            sum += __shfl_xor_sync(kFull, sum, d);
+            prev = max(prev, (long long)__shfl_xor_sync(kFull, prev, d));
+        }
+        if (lane == 0) {
+            s_base = S0.hits + sum;
+            s_prev = prev >= 0 ? (long long)P + prev : S0.last_hit;
+        }
+    }
+    if (SMEM_HIST)
+        for (uint32_t i = threadIdx.x; i <= tcut; i += kThreads) hist[i] = 0;
+    const uint32_t* src = w + (size_t)st * C;
+    const uint32_t base = tile * kGapTile + warp * (kGapGroups * 32);
+    uint32_t masks[kGapGroups];
+    uint32_t cnt = 0;
+    int32_t last = -1;
+#pragma unroll
+    for (uint32_t g = 0; g < kGapGroups; ++g) {
+        const uint32_t j = base + g * 32;
+        masks[g] = gap_ballot(src, j + lane, P + j + lane, mask, lo, hi, budget);
+        cnt += __popc(masks[g]);
+        if (masks[g]) last = (int32_t)(j + 31 - __clz(masks[g]));
+    }
+    if (lane == 0) {
+        wc[warp] = cnt;
+        wl[warp] = last;
+    }
+    __syncthreads();
+    unsigned long long ord = s_base;
+    long long prev = s_prev;
+    for (uint32_t i = 0; i < warp; ++i) {
+        ord += wc[i];
+        if (wl[i] >= 0) prev = (long long)P + wl[i];
+    }
+    unsigned long long* cs = counts + (size_t)st * (tcut + 1);
+    const uint32_t below_me = (1u << lane) - 1u;
+    if (ord <= n) {
+#pragma unroll
+        for (uint32_t g = 0; g < kGapGroups; ++g) {
+            const uint32_t m = masks[g];
+            if (!m) continue;
+            const long long pos0 = (long long)P + base + g * 32;
+            if (m >> lane & 1u) {
+                const uint32_t below = m & below_me;
+                const unsigned long long k = ord + __popc(below);  // this hit is h_k
+                const long long pv = below ? pos0 + 31 - __clz(below) : prev;
+                if (k >= 1 && k <= n) {
+                    const unsigned long long gap = (unsigned long long)(pos0 + lane - pv - 1);
+                    const uint32_t bin = gap < tcut ? (uint32_t)gap : tcut;
+                    if (SMEM_HIST)
+                        atomicAdd(hist + bin, 1u);
+                    else
+                        atomicAdd(cs + bin, 1ull);
+                    if (k == n) end_pos[st] = (unsigned long long)(pos0 + lane);
+                }
+            }
+            ord += __popc(m);
+            prev = pos0 + 31 - __clz(m);
+        }
+    }
+    if (SMEM_HIST) {
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i <= tcut; i += kThreads)
+            if (hist[i]) atomicAdd(cs + i, (unsigned long long)hist[i]);
+    }
+}
+
+__global__ void gap_update_kernel(const GapTile* __restrict__ tiles, uint32_t T, uint32_t S, uint64_t P, uint64_t C,
+                                  uint64_t budget, uint64_t n, const unsigned long long* __restrict__ end_pos,
+                                  GapState* __restrict__ state) {
+    const uint32_t st = blockIdx.x * blockDim.x + threadIdx.x;
+    if (st >= S) return;
+    GapState g = state[st];
+    if (g.done) return;
+    unsigned long long sum = 0;
+    long long last = -1;
+    for (uint32_t t = 0; t < T; ++t) {
+        const GapTile x = tiles[(size_t)st * T + t];
+        sum += x.count;
+        if (x.count) last = x.last;
+    }
+    g.hits += sum;
+    if (last >= 0) g.last_hit = (long long)P + last;
+    if (g.hits >= n + 1) {
+        g.done = 1;
+        g.end = end_pos[st];
+    } else if (P + C >= budget) {
+        g.done = 1;
+        g.exhausted = 1;
+    }
+    state[st] = g;
+}
+
+// ---------------------------------------------------------------------------------------------
+// host driver
+
+struct DevBuf {
+    void* p = nullptr;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct Failure {
+    int code;
+};
+
+void check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Failure{cuda_error(e, what)};
+}
+
+void alloc(DevBuf& b, size_t bytes, const char* what) { check(cudaMalloc(&b.p, std::max<size_t>(bytes, 16)), what); }
+
+// Saves the context's stream state and restores it on scope exit: the stat run consumes the
+// streams from their current position but leaves them (and the checksums) untouched.
+struct StateGuard {
+    mtgp_ctx* ctx;
+    DevBuf win;
+    std::vector<uint64_t> pos;
+    bool cksum;
+    explicit StateGuard(mtgp_ctx* c) : ctx(c), pos(c->position), cksum(c->cksum) {
+        const size_t bytes = (size_t)ctx->n_sets * ctx->N * 4;
+        alloc(win, bytes, "cudaMalloc state copy");
+        check(cudaMemcpyAsync(win.p, ctx->d_win, bytes, cudaMemcpyDeviceToDevice, ctx->stream), "state copy");
+        ctx->cksum = false;
+    }
+    ~StateGuard() {
+        cudaMemcpyAsync(ctx->d_win, win.p, (size_t)ctx->n_sets * ctx->N * 4, cudaMemcpyDeviceToDevice, ctx->stream);
+        cudaStreamSynchronize(ctx->stream);
+        ctx->position = pos;
+        ctx->cksum = cksum;
+        if (ctx->planner) ctx->planner->invalidate();
+    }
+};
+
+uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+constexpr uint64_t kChunkTarget = 1ull << 20;  // words per stream per chunk (S = 200: 0.8 GB)
+
+void generate_chunk(mtgp_ctx* ctx, uint32_t* buf, uint64_t C) {
+    const int rc = ctx_generate_device(ctx, MTGP_U32, buf, C);
+    if (rc) throw Failure{rc};
+}
+
+void launched(mtgp_ctx* ctx, const char* what) {
+    check(cudaGetLastError(), what);
+    ctx->total_launches += 1;
+}
+
+std::vector<uint64_t> fetch(mtgp_ctx* ctx, const DevBuf& b, size_t n) {
+    std::vector<uint64_t> h(n);
+    check(cudaMemcpyAsync(h.data(), b.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H counts");
+    check(cudaStreamSynchronize(ctx->stream), "sync");
+    return h;
+}
+
+void run_walk(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res) {
+    const uint32_t S = ctx->n_sets, l = sp.l;
+    if (l > (1u << 20)) throw std::invalid_argument("walk length l > 2^20 is not supported on the device path");
+    const uint32_t wpt = std::max<uint32_t>(1, 8192 / l);
+    const uint32_t tile_words = wpt * l;
+    uint32_t tpc = (uint32_t)std::max<uint64_t>(2, kChunkTarget / tile_words);
+    tpc += tpc & 1;  // even: C % 4 == 0 (l is even) keeps the register-ring generator eligible
+    const uint64_t C = (uint64_t)tpc * tile_words;
+    const uint64_t chunks = ceil_div(sp.n, (uint64_t)tpc * wpt);
+    const bool smem_hist = l + 1 <= 16384;
+    const size_t smem = 4 * ((size_t)(tile_words + 31) / 32 + (smem_hist ? l + 1 : 0));
+    DevBuf buf, counts;
+    alloc(buf, (size_t)S * C * 4, "cudaMalloc stat chunk");
+    alloc(counts, (size_t)S * (l + 1) * 8, "cudaMalloc counts");
+    check(cudaMemsetAsync(counts.p, 0, (size_t)S * (l + 1) * 8, ctx->stream), "memset");
+    auto k = smem_hist ? walk_kernel<true> : walk_kernel<false>;
+    check(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attribute");
+    for (uint64_t c = 0; c < chunks; ++c) {
+        generate_chunk(ctx, buf.as<uint32_t>(), C);
+        k<<<dim3(tpc, S), kThreads, smem, ctx->stream>>>(buf.as<uint32_t>(), C, l, wpt, c * tpc * wpt, sp.n,
+                                                         counts.as<unsigned long long>());
+        launched(ctx, "walk kernel");
+    }
+    const auto h = fetch(ctx, counts, (size_t)S * (l + 1));
+    for (uint32_t s = 0; s < S; ++s) {
+        stat::finish(sp, h.data() + (size_t)s * (l + 1), res + s);
+        res[s].words_used = stat::words_needed(sp);
+    }
+}
+
+uint32_t gcd32(uint32_t a, uint32_t b) {
+    while (b) {
+        const uint32_t t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+void run_hamming(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res) {
+    const uint32_t S = ctx->n_sets;
+    // a pair of blocks is 2L bits; the smallest span that is whole words AND whole pairs is
+    // 2L / g words = s / g pairs, g = gcd(2L, s)
+    const uint64_t two_l = 2ull * sp.L;
+    const uint32_t g = two_l > 0xFFFFFFFFull ? 1 : gcd32((uint32_t)two_l, sp.s);
+    const uint64_t unit = two_l / g;
+    if (unit > 8192)
+        throw std::invalid_argument("hamming block pair spans more than 8192 words; not supported on the device path");
+    const uint32_t units = std::max<uint32_t>(1, 8192 / (uint32_t)unit);
+    const uint32_t tile_words = units * (uint32_t)unit;
+    const uint32_t ppt = units * (sp.s / g);  // pairs per tile
+    uint32_t tpc = (uint32_t)std::max<uint64_t>(4, kChunkTarget / tile_words);
+    tpc = (tpc + 3) & ~3u;  // C % 4 == 0
+    const uint64_t C = (uint64_t)tpc * tile_words;
+    const uint64_t npairs = sp.n / 2;
+    const uint64_t chunks = ceil_div(npairs, (uint64_t)tpc * ppt);
+    const size_t smem = 4 * (2 * (size_t)tile_words + 1);
+    DevBuf buf, table;
+    alloc(buf, (size_t)S * C * 4, "cudaMalloc stat chunk");
+    alloc(table, (size_t)S * 4 * 8, "cudaMalloc table");
+    check(cudaMemsetAsync(table.p, 0, (size_t)S * 4 * 8, ctx->stream), "memset");
+    check(cudaFuncSetAttribute(hamming_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attribute");
+    for (uint64_t c = 0; c < chunks; ++c) {
+        generate_chunk(ctx, buf.as<uint32_t>(), C);
+        hamming_kernel<<<dim3(tpc, S), kThreads, smem, ctx->stream>>>(buf.as<uint32_t>(), C, sp.r, sp.s, sp.L, ppt,
+                                                                      tile_words, c * tpc * ppt, npairs,
+                                                                      table.as<unsigned long long>());
+        launched(ctx, "hamming kernel");
+    }
+    const auto h = fetch(ctx, table, (size_t)S * 4);
+    for (uint32_t s = 0; s < S; ++s) {
+        stat::finish(sp, h.data() + (size_t)s * 4, res + s);
+        res[s].words_used = stat::words_needed(sp);
+    }
+}
+
+void run_opso(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res) {
+    const uint32_t S = ctx->n_sets;
+    const uint64_t cells = 1ull << (2 * sp.s);
+    const uint64_t bm_words = std::max<uint64_t>(1, cells / 32);
+    const uint64_t W = sp.n + 1;
+    const uint64_t C = std::min<uint64_t>(kChunkTarget, (W + 3) & ~3ull);
+    const uint64_t chunks = ceil_div(W, C);
+    DevBuf buf, bitmap, prev, coll;
+    alloc(buf, (size_t)S * C * 4, "cudaMalloc stat chunk");
+    alloc(bitmap, (size_t)S * bm_words * 4, "cudaMalloc cell bitmap");
+    alloc(prev, (size_t)S * 2 * 4, "cudaMalloc carry");
+    alloc(coll, (size_t)S * 8, "cudaMalloc collisions");
+    check(cudaMemsetAsync(bitmap.p, 0, (size_t)S * bm_words * 4, ctx->stream), "memset");
+    check(cudaMemsetAsync(prev.p, 0, (size_t)S * 2 * 4, ctx->stream), "memset");
+    check(cudaMemsetAsync(coll.p, 0, (size_t)S * 8, ctx->stream), "memset");
+    const uint32_t gx = (uint32_t)std::min<uint64_t>(ceil_div(C, kThreads), 64);
+    for (uint64_t c = 0; c < chunks; ++c) {
+        generate_chunk(ctx, buf.as<uint32_t>(), C);
+        uint32_t* carry = prev.as<uint32_t>();
+        opso_kernel<<<dim3(gx, S), kThreads, 0, ctx->stream>>>(buf.as<uint32_t>(), C, c * C, sp.r, sp.s, sp.n,
+                                                               bitmap.as<uint32_t>(), bm_words,
+                                                               carry + (c & 1) * S, carry + ((c + 1) & 1) * S,
+                                                               coll.as<unsigned long long>());
+        launched(ctx, "opso kernel");
+    }
+    const auto h = fetch(ctx, coll, S);
+    for (uint32_t s = 0; s < S; ++s) {
+        stat::finish(sp, h.data() + s, res + s);
+        res[s].words_used = W;
+    }
+}
+
+void run_gap(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res) {
+    const uint32_t S = ctx->n_sets;
+    const stat::GapShape g = stat::gap_shape(sp);
+    const uint32_t tcut = (uint32_t)g.tcut;
+    const uint64_t C = kChunkTarget;  // multiple of kGapTile
+    const uint32_t T = (uint32_t)(C / kGapTile);
+    const uint64_t max_chunks = ceil_div(g.budget, C);
+    const double p = sp.beta - sp.alpha;
+    const uint64_t expected_chunks = std::max<uint64_t>(1, (uint64_t)((double)(sp.n + 1) / p / (double)C));
+    const bool smem_hist = tcut + 1 <= 12288;
+    const size_t smem = smem_hist ? 4 * ((size_t)tcut + 1) : 0;
+    DevBuf buf, counts, tiles, state, end;
+    alloc(buf, (size_t)S * C * 4, "cudaMalloc stat chunk");
+    alloc(counts, (size_t)S * (tcut + 1) * 8, "cudaMalloc counts");
+    alloc(tiles, (size_t)S * T * sizeof(GapTile), "cudaMalloc tiles");
+    alloc(state, (size_t)S * sizeof(GapState), "cudaMalloc gap state");
+    alloc(end, (size_t)S * 8, "cudaMalloc end");
+    check(cudaMemsetAsync(counts.p, 0, (size_t)S * (tcut + 1) * 8, ctx->stream), "memset");
+    std::vector<GapState> hs(S, GapState{0, -1, 0, 0, 0});
+    check(cudaMemcpyAsync(state.p, hs.data(), S * sizeof(GapState), cudaMemcpyHostToDevice, ctx->stream), "H2D state");
+    auto hk = smem_hist ? gap_hist_kernel<true> : gap_hist_kernel<false>;
+    if (smem > 48 * 1024)
+        check(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attribute");
+    for (uint64_t c = 0; c < max_chunks; ++c) {
+        const uint64_t P = c * C;
+        generate_chunk(ctx, buf.as<uint32_t>(), C);
+        gap_count_kernel<<<dim3(T, S), kThreads, 0, ctx->stream>>>(buf.as<uint32_t>(), C, P, g.mask, g.lo, g.hi,
+                                                                   g.budget, state.as<GapState>(), tiles.as<GapTile>(), T);
+        launched(ctx, "gap count kernel");
+        hk<<<dim3(T, S), kThreads, smem, ctx->stream>>>(buf.as<uint32_t>(), C, P, g.mask, g.lo, g.hi, g.budget,
+                                                        state.as<GapState>(), tiles.as<GapTile>(), T, sp.n, tcut,
+                                                        counts.as<unsigned long long>(), end.as<unsigned long long>());
+        launched(ctx, "gap hist kernel");
+        gap_update_kernel<<<(S + 127) / 128, 128, 0, ctx->stream>>>(tiles.as<GapTile>(), T, S, P, C, g.budget, sp.n,
+                                                                    end.as<unsigned long long>(), state.as<GapState>());
+        launched(ctx, "gap update kernel");
+        // poll for completion around the expected length, sparsely before it
+        if (c + 1 >= expected_chunks && ((c + 1 - expected_chunks) % 2 == 0 || c + 1 == max_chunks)) {
+            check(cudaMemcpyAsync(hs.data(), state.p, S * sizeof(GapState), cudaMemcpyDeviceToHost, ctx->stream), "D2H state");
+            check(cudaStreamSynchronize(ctx->stream), "sync");
+            if (std::all_of(hs.begin(), hs.end(), [](const GapState& x) { return x.done != 0; })) break;
+        }
+    }
+    check(cudaMemcpyAsync(hs.data(), state.p, S * sizeof(GapState), cudaMemcpyDeviceToHost, ctx->stream), "D2H state");
+    const auto h = fetch(ctx, counts, (size_t)S * (tcut + 1));
+    for (uint32_t s = 0; s < S; ++s) {
+        res[s] = mtgp_stat_result{};
+        if (!hs[s].done || hs[s].exhausted) {
+            res[s].error = MTGP_STAT_EXHAUSTED;
+            res[s].words_used = g.budget;
+            continue;
+        }
+        stat::finish(sp, h.data() + (size_t)s * (tcut + 1), res + s);
+        res[s].words_used = hs[s].end + 1;
+    }
+}
+
+}  // namespace
+}  // namespace mtgpb
+
+extern "C" int mtgp_stat_run(mtgp_ctx* ctx, const mtgp_stat_spec* spec, mtgp_stat_result* results) {
+    using namespace mtgpb;
+    if (!ctx || !spec || !results) return set_error(MTGP_EINVAL, "null argument");
+    try {
+        stat::validate(*spec);
+    } catch (const std::invalid_argument& e) {
+        return set_error(MTGP_EINVAL, "%s", e.what());
+    }
+    if (ctx->n_sets > 65535) return set_error(MTGP_EINVAL, "stat tests support at most 65535 streams per context");
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) return cuda_error(e, "cudaSetDevice");
+    std::memset(results, 0, sizeof(mtgp_stat_result) * ctx->n_sets);
+    try {
+        StateGuard guard(ctx);
+        switch (spec->test) {
+            case MTGP_STAT_GAP: run_gap(ctx, *spec, results); break;
+            case MTGP_STAT_HAMMING_INDEP: run_hamming(ctx, *spec, results); break;
+            case MTGP_STAT_COLLISION_OVER: run_opso(ctx, *spec, results); break;
+            case MTGP_STAT_RANDOM_WALK: run_walk(ctx, *spec, results); break;
+        }
+    } catch (const Failure& f) {
+        return f.code;
+    } catch (const std::invalid_argument& x) {
+        return set_error(MTGP_EINVAL, "%s", x.what());
+    }
+    return MTGP_OK;
+}

@@ -33,7 +33,10 @@ EXPORTS = (
     "mtgp_skip", "mtgp_state_save", "mtgp_state_restore", "mtgp_checksums",
     "mtgp_checksums_reset", "mtgp_sync", "mtgp_kernel_timing", "mtgp_kernel_timing_reset",
     "mtgp_last_plan", "mtgp_launch_count", "mtgp_mt_validate_params", "mtgp_mt_ctx_create",
-    "mtgp_charpoly_sha1",
+    "mtgp_charpoly_sha1", "mtgp_stat_validate", "mtgp_stat_run", "mtgp_stat_counts_len", "mtgp_stat_finish",
+    "mtgp_ln_gamma", "mtgp_gamma_p", "mtgp_gamma_q", "mtgp_chi_square_pvalue", "mtgp_poisson_cdf",
+    "mtgp_poisson_sf", "mtgp_poisson_pmf", "mtgp_binomial_log_pmf", "mtgp_binomial_upper_tail",
+    "mtgp_classify_pvalue",
 )
 
 
@@ -57,6 +60,19 @@ class MtgpParamsC(C.Structure):
 
 class MtgpCksumC(C.Structure):
     _fields_ = [("sum64", C.c_uint64), ("words", C.c_uint64), ("xor32", C.c_uint32), ("pad", C.c_uint32)]
+
+
+class StatSpecC(C.Structure):
+    """mtgp_stat_spec: TestSpec (proj/include/twistsieve/stat_tests.hpp:18-33) with an int test id."""
+    _fields_ = [("test", C.c_int32), ("N", C.c_uint32), ("n", C.c_uint64), ("r", C.c_uint32), ("s", C.c_uint32),
+                ("L", C.c_uint32), ("d", C.c_uint32), ("l", C.c_uint32), ("t", C.c_uint32),
+                ("alpha", C.c_double), ("beta", C.c_double)]
+
+
+class StatResultC(C.Structure):
+    """mtgp_stat_result: TestResult (stat_tests.hpp:35-42) + error code + words consumed."""
+    _fields_ = [("statistic", C.c_double), ("p_value", C.c_double), ("classification", C.c_int32),
+                ("degenerate", C.c_int32), ("error", C.c_int32), ("pad", C.c_int32), ("words_used", C.c_uint64)]
 
 
 class MtgpError(RuntimeError):
@@ -105,6 +121,21 @@ def load_library(path: Optional[str] = None) -> C.CDLL:
     lib.mtgp_charpoly_sha1.argtypes = [C.c_void_p, C.c_char_p]
     lib.mtgp_mt_ctx_create.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.POINTER(MtParamsC), C.c_uint32,
                                        C.POINTER(C.c_uint32), C.c_void_p]
+    lib.mtgp_stat_validate.argtypes = [C.POINTER(StatSpecC)]
+    lib.mtgp_stat_run.argtypes = [C.c_void_p, C.POINTER(StatSpecC), C.POINTER(StatResultC)]
+    lib.mtgp_stat_counts_len.argtypes = [C.POINTER(StatSpecC), C.POINTER(C.c_uint64)]
+    lib.mtgp_stat_finish.argtypes = [C.POINTER(StatSpecC), C.POINTER(C.c_uint64), C.c_uint64, C.POINTER(StatResultC)]
+    pd = C.POINTER(C.c_double)
+    lib.mtgp_ln_gamma.argtypes = [C.c_double, pd]
+    lib.mtgp_gamma_p.argtypes = [C.c_double, C.c_double, pd]
+    lib.mtgp_gamma_q.argtypes = [C.c_double, C.c_double, pd]
+    lib.mtgp_chi_square_pvalue.argtypes = [C.c_double, C.c_uint32, pd]
+    lib.mtgp_poisson_cdf.argtypes = [C.c_uint64, C.c_double, pd]
+    lib.mtgp_poisson_sf.argtypes = [C.c_uint64, C.c_double, pd]
+    lib.mtgp_poisson_pmf.argtypes = [C.c_uint64, C.c_double, pd]
+    lib.mtgp_binomial_log_pmf.argtypes = [C.c_uint64, C.c_uint64, C.c_double, pd]
+    lib.mtgp_binomial_upper_tail.argtypes = [C.c_uint64, C.c_uint64, C.c_double, pd]
+    lib.mtgp_classify_pvalue.argtypes = [C.c_double, C.POINTER(C.c_int32)]
     if path is None:
         _lib = lib
     return lib
@@ -259,6 +290,12 @@ class MtgpContext:
 
     def kernel_timing_reset(self) -> None:
         _check(self.lib, self.lib.mtgp_kernel_timing_reset(self.h))
+
+    def stat_run(self, spec) -> list:
+        """The device-side statistical test `spec` (stattests.TestSpec) on every stream, from the
+        current position; the context state is unchanged. One stattests.TestResult per stream."""
+        from . import stattests
+        return stattests.run_on_context(self, spec)
 
 
 def mt_validate(status: dict) -> None:
