@@ -262,6 +262,8 @@ int mtgp_ctx_destroy(mtgp_ctx* ctx) {
     cudaFree(ctx->d_win);
     cudaFree(ctx->d_ck);
     cudaFree(ctx->d_stage);
+    cudaFree(ctx->d_scratch[0]);
+    cudaFree(ctx->d_scratch[1]);
     for (int i = 0; i < 2; ++i) {
         cudaEventDestroy(ctx->ev_gen[i]);
         cudaEventDestroy(ctx->ev_copy[i]);

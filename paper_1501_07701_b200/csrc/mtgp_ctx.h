@@ -45,6 +45,10 @@ struct mtgp_ctx {
     // host-output staging
     void* d_stage = nullptr;
     size_t stage_bytes = 0;
+    // stat-test scratch (slot 0: saved window, slot 1: chunk + counters), kept across
+    // mtgp_stat_run calls, grown on demand, freed with the context
+    void* d_scratch[2] = {nullptr, nullptr};
+    size_t scratch_bytes[2] = {0, 0};
     cudaEvent_t ev_gen[2] = {nullptr, nullptr};
     cudaEvent_t ev_copy[2] = {nullptr, nullptr};
 

@@ -140,6 +140,11 @@ void Planner::invalidate() {
     impl_->plan_valid = false;
 }
 
+cudaError_t Planner::analyze_now(const DevParams* params, const uint32_t* win, cudaStream_t st, std::string& err) {
+    if (!impl_->v2) return cudaSuccess;
+    return impl_->analyze(params, win, st, err);
+}
+
 cudaError_t PlannerImpl::analyze(const DevParams* params, const uint32_t* win, cudaStream_t st, std::string& err) {
     if (analyzed) return cudaSuccess;
     const uint32_t len = ((t0 + 2 * M + N + 64) + 31) & ~31u;

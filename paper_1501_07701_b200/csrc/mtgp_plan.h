@@ -41,6 +41,9 @@ public:
     bool v2_supported() const;
     // forget per-stream algebra and cached plans (after a state restore)
     void invalidate();
+    // run the per-stream annihilator analysis now, at the current window (no-op if done). An
+    // analysis made at window w stays valid for w and every later window of the same streams.
+    cudaError_t analyze_now(const DevParams* params, const uint32_t* win, cudaStream_t st, std::string& err);
     cudaError_t run(PlanRun& r, std::string& err);
     cudaError_t skip(const DevParams* params, uint32_t* win, uint64_t words, cudaStream_t st,
                      std::string& err);

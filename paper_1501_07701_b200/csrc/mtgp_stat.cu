@@ -113,25 +113,38 @@ __global__ void __launch_bounds__(kThreads) hamming_kernel(const uint32_t* __res
     for (uint32_t j = threadIdx.x; j < tile_words; j += kThreads) let[j] = letter_of(__ldg(src + j), r, sb);
     __syncthreads();
 
-    // block-wide exclusive scan over contiguous per-thread segments
-    const uint32_t ipt = (tile_words + kThreads - 1) / kThreads;
-    const uint32_t j0 = min(threadIdx.x * ipt, tile_words), j1 = min(j0 + ipt, tile_words);
+    // block-wide exclusive scan: warp w owns a contiguous range of 32-word strips; lanes walk a
+    // strip side by side (conflict-free shared-memory access), one warp total pass then one
+    // scanned pass
+    const uint32_t strips = (tile_words + 31) / 32;
+    const uint32_t spw = (strips + kWarps - 1) / kWarps;
+    const uint32_t s0 = min(warp * spw, strips), s1 = min(s0 + spw, strips);
     uint32_t own = 0;
-    for (uint32_t j = j0; j < j1; ++j) own += __popc(let[j]);
-    uint32_t incl = own;
-    for (uint32_t d = 1; d < 32; d <<= 1) {
-        const uint32_t v = __shfl_up_sync(kFull, incl, d);
-        if (lane >= d) incl += v;
+    for (uint32_t q = s0; q < s1; ++q) {
+        const uint32_t j = q * 32 + lane;
+        own += j < tile_words ? __popc(let[j]) : 0u;
     }
-    if (lane == 31) warp_tot[warp] = incl;
+    for (int d = 16; d > 0; d >>= 1) own += __shfl_xor_sync(kFull, own, d);
+    if (lane == 0) warp_tot[warp] = own;
     __syncthreads();
-    uint32_t run = incl - own;
-    for (uint32_t i = 0; i < warp; ++i) run += warp_tot[i];
-    for (uint32_t j = j0; j < j1; ++j) {
-        pre[j] = run;
-        run += __popc(let[j]);
+    uint32_t carry = 0;
+    for (uint32_t i = 0; i < warp; ++i) carry += warp_tot[i];
+    for (uint32_t q = s0; q < s1; ++q) {
+        const uint32_t j = q * 32 + lane;
+        const uint32_t v = j < tile_words ? __popc(let[j]) : 0u;
+        uint32_t incl = v;
+        for (uint32_t d = 1; d < 32; d <<= 1) {
+            const uint32_t u = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += u;
+        }
+        if (j < tile_words) pre[j] = carry + incl - v;
+        carry += __shfl_sync(kFull, incl, 31);
     }
-    if (threadIdx.x == kThreads - 1) pre[tile_words] = run;
+    if (warp == kWarps - 1 && lane == 0) {
+        uint32_t tot = 0;
+        for (uint32_t i = 0; i < kWarps; ++i) tot += warp_tot[i];
+        pre[tile_words] = tot;
+    }
     __syncthreads();
 
     const uint32_t half = L / 2;
@@ -194,6 +207,7 @@ __global__ void __launch_bounds__(kThreads) opso_kernel(const uint32_t* __restri
 // then the tile's gaps, (3) per-stream state update.
 constexpr uint32_t kGapTile = 4096;                   // words per CTA
 constexpr uint32_t kGapGroups = kGapTile / kThreads;  // 32-word groups per warp (16)
+constexpr uint32_t kGapHistCtas = 24;                 // histogram CTAs per stream
 
 struct GapTile {
     uint32_t count;
@@ -216,7 +230,8 @@ __device__ __forceinline__ uint32_t gap_ballot(const uint32_t* src, uint64_t j, 
 __global__ void __launch_bounds__(kThreads) gap_count_kernel(const uint32_t* __restrict__ w, uint64_t C, uint64_t P,
                                                              uint32_t mask, uint64_t lo, uint64_t hi, uint64_t budget,
                                                              const GapState* __restrict__ state,
-                                                             GapTile* __restrict__ tiles, uint32_t T) {
+                                                             GapTile* __restrict__ tiles, uint32_t T,
+                                                             uint32_t* __restrict__ hits) {
     __shared__ uint32_t wc[kWarps];
     __shared__ int32_t wf[kWarps], wl[kWarps];
     const uint32_t st = blockIdx.y, tile = blockIdx.x;
@@ -227,17 +242,21 @@ __global__ void __launch_bounds__(kThreads) gap_count_kernel(const uint32_t* __r
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint32_t* src = w + (size_t)st * C;
     const uint32_t base = tile * kGapTile + warp * (kGapGroups * 32);
-    uint32_t cnt = 0;
+    uint32_t cnt = 0, mine = 0;
     int32_t first = -1, last = -1;
+#pragma unroll
     for (uint32_t g = 0; g < kGapGroups; ++g) {
         const uint32_t j = base + g * 32;
         const uint32_t m = gap_ballot(src, j + lane, P + j + lane, mask, lo, hi, budget);
+        if (lane == g) mine = m;
         if (m) {
             cnt += __popc(m);
             if (first < 0) first = (int32_t)(j + __ffs(m) - 1);
             last = (int32_t)(j + 31 - __clz(m));
         }
     }
+    // hit bitmap (1 bit per word) for the histogram pass: 64 B per warp, coalesced
+    if (lane < kGapGroups) hits[(size_t)st * (C / 32) + base / 32 + lane] = mine;
     if (lane == 0) {
         wc[warp] = cnt;
         wf[warp] = first;
@@ -255,115 +274,156 @@ __global__ void __launch_bounds__(kThreads) gap_count_kernel(const uint32_t* __r
     }
 }
 
+// Per stream: exclusive scan of the chunk's tile counts -> the ordinal of each tile's first hit
+// and the hit before it; advances the carried {hits, last_hit} (done is set by gap_update_kernel
+// after the histogram pass, which still needs the old value).
+struct GapPre {
+    unsigned long long ord0;  // ordinal k of the tile's first hit (it is h_k)
+    long long prev;           // global index of the hit before it, -1 if none
+};
+
+__global__ void __launch_bounds__(kThreads) gap_scan_kernel(const GapTile* __restrict__ tiles, uint32_t T, uint64_t P,
+                                                            GapState* __restrict__ state, GapPre* __restrict__ pre) {
+    __shared__ unsigned long long wsum[kWarps];
+    __shared__ long long wlast[kWarps];
+    const uint32_t st = blockIdx.x;
+    const GapState g = state[st];
+    if (g.done) return;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const GapTile* tl = tiles + (size_t)st * T;
+    const uint32_t seg = (T + kThreads - 1) / kThreads;
+    const uint32_t t0 = min(threadIdx.x * seg, T), t1 = min(t0 + seg, T);
+    unsigned long long sum = 0;
+    long long last = -1;  // chunk-local, positions grow with t so max == most recent
+    for (uint32_t t = t0; t < t1; ++t) {
+        sum += tl[t].count;
+        if (tl[t].count) last = tl[t].last;
+    }
+    unsigned long long isum = sum;
+    long long ilast = last;
+    for (uint32_t d = 1; d < 32; d <<= 1) {
+        const unsigned long long u = __shfl_up_sync(kFull, isum, d);
+        const long long v = __shfl_up_sync(kFull, ilast, d);
+        if (lane >= d) {
+            isum += u;
+            ilast = max(ilast, v);
+        }
+    }
+    if (lane == 31) {
+        wsum[warp] = isum;
+        wlast[warp] = ilast;
+    }
+    __syncthreads();
+    unsigned long long ord = g.hits + isum - sum;
+    long long before = -1;
+    {
+        const long long v = __shfl_up_sync(kFull, ilast, 1);
+        before = lane ? v : -1;
+    }
+    for (uint32_t i = 0; i < warp; ++i) {
+        ord += wsum[i];
+        before = max(before, wlast[i]);
+    }
+    long long prev = before >= 0 ? (long long)P + before : g.last_hit;
+    for (uint32_t t = t0; t < t1; ++t) {
+        pre[(size_t)st * T + t] = GapPre{ord, prev};
+        ord += tl[t].count;
+        if (tl[t].count) prev = (long long)P + tl[t].last;
+    }
+    if (threadIdx.x == kThreads - 1) {  // its running values end at the chunk totals
+        state[st].hits = ord;
+        state[st].last_hit = prev;
+    }
+}
+
+// Histogram pass: a CTA walks tiles blockIdx.x, +gridDim.x, ... of one stream (from the hit
+// bitmap, not the words), so each CTA zeroes and flushes its shared histogram once.
 template <bool SMEM_HIST>
-__global__ void __launch_bounds__(kThreads) gap_hist_kernel(const uint32_t* __restrict__ w, uint64_t C, uint64_t P,
-                                                            uint32_t mask, uint64_t lo, uint64_t hi, uint64_t budget,
+__global__ void __launch_bounds__(kThreads) gap_hist_kernel(const uint32_t* __restrict__ hits, uint64_t C, uint64_t P,
                                                             const GapState* __restrict__ state,
-                                                            const GapTile* __restrict__ tiles, uint32_t T, uint64_t n,
+                                                            const GapTile* __restrict__ tiles,
+                                                            const GapPre* __restrict__ pre, uint32_t T, uint64_t n,
                                                             uint32_t tcut, unsigned long long* __restrict__ counts,
                                                             unsigned long long* __restrict__ end_pos) {
     extern __shared__ uint32_t hist[];
-    __shared__ unsigned long long s_base;
-    __shared__ long long s_prev;
     __shared__ uint32_t wc[kWarps];
     __shared__ int32_t wl[kWarps];
-    const uint32_t st = blockIdx.y, tile = blockIdx.x;
-    const GapState S0 = state[st];
-    if (S0.done || tiles[(size_t)st * T + tile].count == 0) return;
+    const uint32_t st = blockIdx.y;
+    if (state[st].done) return;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    if (warp == 0) {
-        // ordinal of this tile's first hit, and the hit before it
-        unsigned long long sum = 0;
-        long long prev = -1;
-        for (uint32_t t = lane; t < tile; t += 32) {
-            const GapTile g = tiles[(size_t)st * T + t];
-            sum += g.count;
-            if (g.count) prev = max(prev, (long long)g.last);
-        }
-        for (int d = 16; d > 0; d >>= 1) {
-            sum += __shfl_xor_sync(kFull, sum, d);
-            prev = max(prev, (long long)__shfl_xor_sync(kFull, prev, d));
-        }
-        if (lane == 0) {
-            s_base = S0.hits + sum;
-            s_prev = prev >= 0 ? (long long)P + prev : S0.last_hit;
-        }
-    }
     if (SMEM_HIST)
         for (uint32_t i = threadIdx.x; i <= tcut; i += kThreads) hist[i] = 0;
-    const uint32_t* src = w + (size_t)st * C;
-    const uint32_t base = tile * kGapTile + warp * (kGapGroups * 32);
-    uint32_t masks[kGapGroups];
-    uint32_t cnt = 0;
-    int32_t last = -1;
-#pragma unroll
-    for (uint32_t g = 0; g < kGapGroups; ++g) {
-        const uint32_t j = base + g * 32;
-        masks[g] = gap_ballot(src, j + lane, P + j + lane, mask, lo, hi, budget);
-        cnt += __popc(masks[g]);
-        if (masks[g]) last = (int32_t)(j + 31 - __clz(masks[g]));
-    }
-    if (lane == 0) {
-        wc[warp] = cnt;
-        wl[warp] = last;
-    }
-    __syncthreads();
-    unsigned long long ord = s_base;
-    long long prev = s_prev;
-    for (uint32_t i = 0; i < warp; ++i) {
-        ord += wc[i];
-        if (wl[i] >= 0) prev = (long long)P + wl[i];
-    }
     unsigned long long* cs = counts + (size_t)st * (tcut + 1);
-    const uint32_t below_me = (1u << lane) - 1u;
-    if (ord <= n) {
-#pragma unroll
-        for (uint32_t g = 0; g < kGapGroups; ++g) {
-            const uint32_t m = masks[g];
-            if (!m) continue;
-            const long long pos0 = (long long)P + base + g * 32;
-            if (m >> lane & 1u) {
-                const uint32_t below = m & below_me;
-                const unsigned long long k = ord + __popc(below);  // this hit is h_k
-                const long long pv = below ? pos0 + 31 - __clz(below) : prev;
-                if (k >= 1 && k <= n) {
-                    const unsigned long long gap = (unsigned long long)(pos0 + lane - pv - 1);
-                    const uint32_t bin = gap < tcut ? (uint32_t)gap : tcut;
-                    if (SMEM_HIST)
-                        atomicAdd(hist + bin, 1u);
-                    else
-                        atomicAdd(cs + bin, 1ull);
-                    if (k == n) end_pos[st] = (unsigned long long)(pos0 + lane);
-                }
+    bool touched = false;
+    for (uint32_t tile = blockIdx.x; tile < T; tile += gridDim.x) {
+        if (tiles[(size_t)st * T + tile].count == 0) continue;
+        const GapPre tp = pre[(size_t)st * T + tile];
+        if (tp.ord0 > n) break;  // ordinals only grow with the tile index
+        touched = true;
+        const uint32_t base = tile * kGapTile + warp * (kGapGroups * 32);
+        // lane g < 16 owns group g (32 words) of the warp's 512: its hit mask, the number of hits
+        // before it (exclusive scan) and the last hit before it (exclusive max scan)
+        const uint32_t m = lane < kGapGroups ? __ldg(hits + (size_t)st * (C / 32) + base / 32 + lane) : 0u;
+        const uint32_t c = __popc(m);
+        const int32_t lst = m ? (int32_t)(base + lane * 32 + 31 - __clz(m)) : -1;
+        uint32_t ic = c;
+        int32_t il = lst;
+        for (uint32_t d = 1; d < 32; d <<= 1) {
+            const uint32_t u = __shfl_up_sync(kFull, ic, d);
+            const int32_t v = __shfl_up_sync(kFull, il, d);
+            if (lane >= d) {
+                ic += u;
+                il = max(il, v);
             }
-            ord += __popc(m);
-            prev = pos0 + 31 - __clz(m);
+        }
+        const uint32_t warp_cnt = __shfl_sync(kFull, ic, 31);
+        const int32_t warp_last = __shfl_sync(kFull, il, 31);
+        int32_t before = __shfl_up_sync(kFull, il, 1);
+        if (lane == 0) before = -1;
+        __syncthreads();  // previous tile's readers of wc / wl are done
+        if (lane == 0) {
+            wc[warp] = warp_cnt;
+            wl[warp] = warp_last;
+        }
+        __syncthreads();
+        unsigned long long ord = tp.ord0;
+        long long prev = tp.prev;
+        for (uint32_t i = 0; i < warp; ++i) {
+            ord += wc[i];
+            if (wl[i] >= 0) prev = (long long)P + wl[i];
+        }
+        if (ord > n || !m) continue;
+        unsigned long long k = ord + ic - c;  // ordinal of this group's first hit
+        long long pv = before >= 0 ? (long long)P + before : prev;
+        const long long pos0 = (long long)P + base + lane * 32;
+        for (uint32_t mm = m; mm && k <= n; mm &= mm - 1, ++k) {
+            const long long pos = pos0 + __ffs(mm) - 1;  // this hit is h_k
+            if (k >= 1) {
+                const unsigned long long gap = (unsigned long long)(pos - pv - 1);
+                const uint32_t bin = gap < tcut ? (uint32_t)gap : tcut;
+                if (SMEM_HIST)
+                    atomicAdd(hist + bin, 1u);
+                else
+                    atomicAdd(cs + bin, 1ull);
+                if (k == n) end_pos[st] = (unsigned long long)pos;
+            }
+            pv = pos;
         }
     }
-    if (SMEM_HIST) {
+    if (SMEM_HIST && touched) {
         __syncthreads();
         for (uint32_t i = threadIdx.x; i <= tcut; i += kThreads)
             if (hist[i]) atomicAdd(cs + i, (unsigned long long)hist[i]);
     }
 }
 
-__global__ void gap_update_kernel(const GapTile* __restrict__ tiles, uint32_t T, uint32_t S, uint64_t P, uint64_t C,
-                                  uint64_t budget, uint64_t n, const unsigned long long* __restrict__ end_pos,
-                                  GapState* __restrict__ state) {
+__global__ void gap_update_kernel(uint32_t S, uint64_t P, uint64_t C, uint64_t budget, uint64_t n,
+                                  const unsigned long long* __restrict__ end_pos, GapState* __restrict__ state) {
     const uint32_t st = blockIdx.x * blockDim.x + threadIdx.x;
     if (st >= S) return;
     GapState g = state[st];
     if (g.done) return;
-    unsigned long long sum = 0;
-    long long last = -1;
-    for (uint32_t t = 0; t < T; ++t) {
-        const GapTile x = tiles[(size_t)st * T + t];
-        sum += x.count;
-        if (x.count) last = x.last;
-    }
-    g.hits += sum;
-    if (last >= 0) g.last_hit = (long long)P + last;
-    if (g.hits >= n + 1) {
+    if (g.hits >= n + 1) {  // hits already advanced by gap_scan_kernel
         g.done = 1;
         g.end = end_pos[st];
     } else if (P + C >= budget) {
@@ -376,11 +436,9 @@ __global__ void gap_update_kernel(const GapTile* __restrict__ tiles, uint32_t T,
 // ---------------------------------------------------------------------------------------------
 // host driver
 
+// A device sub-buffer of the context's scratch (non-owning).
 struct DevBuf {
     void* p = nullptr;
-    ~DevBuf() {
-        if (p) cudaFree(p);
-    }
     template <class T>
     T* as() const {
         return static_cast<T*>(p);
@@ -395,33 +453,75 @@ void check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw Failure{cuda_error(e, what)};
 }
 
-void alloc(DevBuf& b, size_t bytes, const char* what) { check(cudaMalloc(&b.p, std::max<size_t>(bytes, 16)), what); }
+// Context-owned scratch slot, grown on demand: a stat run makes no cudaMalloc / cudaFree after
+// the first one of its size (cudaFree synchronises the device and can stall for a long time).
+void* scratch(mtgp_ctx* ctx, int slot, size_t bytes) {
+    if (ctx->scratch_bytes[slot] < bytes) {
+        check(cudaStreamSynchronize(ctx->stream), "sync");
+        cudaFree(ctx->d_scratch[slot]);
+        ctx->d_scratch[slot] = nullptr;
+        ctx->scratch_bytes[slot] = 0;
+        check(cudaMalloc(&ctx->d_scratch[slot], bytes), "cudaMalloc stat scratch");
+        ctx->scratch_bytes[slot] = bytes;
+    }
+    return ctx->d_scratch[slot];
+}
+
+// Carves the chunk buffer and a run's counters out of scratch slot 1.
+struct Arena {
+    std::vector<std::pair<DevBuf*, size_t>> parts;
+    void add(DevBuf& b, size_t bytes) { parts.push_back({&b, (std::max<size_t>(bytes, 16) + 255) & ~size_t(255)}); }
+    uint32_t* commit(mtgp_ctx* ctx, size_t chunk_bytes) {
+        size_t total = (chunk_bytes + 255) & ~size_t(255);
+        for (auto& pb : parts) total += pb.second;
+        char* base = static_cast<char*>(scratch(ctx, 1, total));
+        size_t off = (chunk_bytes + 255) & ~size_t(255);
+        for (auto& pb : parts) {
+            pb.first->p = base + off;
+            off += pb.second;
+        }
+        return reinterpret_cast<uint32_t*>(base);
+    }
+};
 
 // Saves the context's stream state and restores it on scope exit: the stat run consumes the
-// streams from their current position but leaves them (and the checksums) untouched.
+// streams from their current position but leaves them (and the checksums) untouched. The jump
+// planner's annihilator analysis is made up front at the saved window, so it stays valid after
+// the restore (an analysis holds for its window and every later one) and is not redone per run.
 struct StateGuard {
     mtgp_ctx* ctx;
-    DevBuf win;
+    void* win;
     std::vector<uint64_t> pos;
     bool cksum;
     explicit StateGuard(mtgp_ctx* c) : ctx(c), pos(c->position), cksum(c->cksum) {
         const size_t bytes = (size_t)ctx->n_sets * ctx->N * 4;
-        alloc(win, bytes, "cudaMalloc state copy");
-        check(cudaMemcpyAsync(win.p, ctx->d_win, bytes, cudaMemcpyDeviceToDevice, ctx->stream), "state copy");
+        win = scratch(ctx, 0, bytes);
+        check(cudaMemcpyAsync(win, ctx->d_win, bytes, cudaMemcpyDeviceToDevice, ctx->stream), "state copy");
+        if (ctx->engine == 0 && ctx->planner) {
+            std::string err;
+            check(ctx->planner->analyze_now(ctx->d_params, ctx->d_win, ctx->stream, err), "annihilator analysis");
+        }
         ctx->cksum = false;
     }
     ~StateGuard() {
-        cudaMemcpyAsync(ctx->d_win, win.p, (size_t)ctx->n_sets * ctx->N * 4, cudaMemcpyDeviceToDevice, ctx->stream);
+        cudaMemcpyAsync(ctx->d_win, win, (size_t)ctx->n_sets * ctx->N * 4, cudaMemcpyDeviceToDevice, ctx->stream);
         cudaStreamSynchronize(ctx->stream);
         ctx->position = pos;
         ctx->cksum = cksum;
-        if (ctx->planner) ctx->planner->invalidate();
     }
 };
 
 uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
-constexpr uint64_t kChunkTarget = 1ull << 20;  // words per stream per chunk (S = 200: 0.8 GB)
+
+
+// Words per stream per chunk: ~2^30 words (4 GB) per chunk over all streams, 2^16..2^24 per
+// stream. Big chunks let the generator split streams into jump-ahead pieces across all SMs and
+// amortise the per-call planning; the chunk is the stat pass's only large allocation.
+uint64_t chunk_target(uint32_t S) {
+    const uint64_t c = (1ull << 30) / std::max<uint32_t>(S, 1);
+    return std::min<uint64_t>(std::max<uint64_t>(c, 1ull << 16), 1ull << 24);
+}
 
 void generate_chunk(mtgp_ctx* ctx, uint32_t* buf, uint64_t C) {
     const int rc = ctx_generate_device(ctx, MTGP_U32, buf, C);
@@ -445,21 +545,22 @@ void run_walk(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res) {
     if (l > (1u << 20)) throw std::invalid_argument("walk length l > 2^20 is not supported on the device path");
     const uint32_t wpt = std::max<uint32_t>(1, 8192 / l);
     const uint32_t tile_words = wpt * l;
-    uint32_t tpc = (uint32_t)std::max<uint64_t>(2, kChunkTarget / tile_words);
+    uint32_t tpc = (uint32_t)std::max<uint64_t>(2, chunk_target(S) / tile_words);
     tpc += tpc & 1;  // even: C % 4 == 0 (l is even) keeps the register-ring generator eligible
     const uint64_t C = (uint64_t)tpc * tile_words;
     const uint64_t chunks = ceil_div(sp.n, (uint64_t)tpc * wpt);
     const bool smem_hist = l + 1 <= 16384;
     const size_t smem = 4 * ((size_t)(tile_words + 31) / 32 + (smem_hist ? l + 1 : 0));
-    DevBuf buf, counts;
-    alloc(buf, (size_t)S * C * 4, "cudaMalloc stat chunk");
-    alloc(counts, (size_t)S * (l + 1) * 8, "cudaMalloc counts");
+    DevBuf counts;
+    Arena ar;
+    ar.add(counts, (size_t)S * (l + 1) * 8);
+    uint32_t* const wbuf = ar.commit(ctx, (size_t)S * C * 4);
     check(cudaMemsetAsync(counts.p, 0, (size_t)S * (l + 1) * 8, ctx->stream), "memset");
     auto k = smem_hist ? walk_kernel<true> : walk_kernel<false>;
     check(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attribute");
     for (uint64_t c = 0; c < chunks; ++c) {
-        generate_chunk(ctx, buf.as<uint32_t>(), C);
-        k<<<dim3(tpc, S), kThreads, smem, ctx->stream>>>(buf.as<uint32_t>(), C, l, wpt, c * tpc * wpt, sp.n,
+        generate_chunk(ctx, wbuf, C);
+        k<<<dim3(tpc, S), kThreads, smem, ctx->stream>>>(wbuf, C, l, wpt, c * tpc * wpt, sp.n,
                                                          counts.as<unsigned long long>());
         launched(ctx, "walk kernel");
     }
@@ -491,20 +592,21 @@ void run_hamming(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res)
     const uint32_t units = std::max<uint32_t>(1, 8192 / (uint32_t)unit);
     const uint32_t tile_words = units * (uint32_t)unit;
     const uint32_t ppt = units * (sp.s / g);  // pairs per tile
-    uint32_t tpc = (uint32_t)std::max<uint64_t>(4, kChunkTarget / tile_words);
+    uint32_t tpc = (uint32_t)std::max<uint64_t>(4, chunk_target(S) / tile_words);
     tpc = (tpc + 3) & ~3u;  // C % 4 == 0
     const uint64_t C = (uint64_t)tpc * tile_words;
     const uint64_t npairs = sp.n / 2;
     const uint64_t chunks = ceil_div(npairs, (uint64_t)tpc * ppt);
     const size_t smem = 4 * (2 * (size_t)tile_words + 1);
-    DevBuf buf, table;
-    alloc(buf, (size_t)S * C * 4, "cudaMalloc stat chunk");
-    alloc(table, (size_t)S * 4 * 8, "cudaMalloc table");
+    DevBuf table;
+    Arena ar;
+    ar.add(table, (size_t)S * 4 * 8);
+    uint32_t* const wbuf = ar.commit(ctx, (size_t)S * C * 4);
     check(cudaMemsetAsync(table.p, 0, (size_t)S * 4 * 8, ctx->stream), "memset");
     check(cudaFuncSetAttribute(hamming_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attribute");
     for (uint64_t c = 0; c < chunks; ++c) {
-        generate_chunk(ctx, buf.as<uint32_t>(), C);
-        hamming_kernel<<<dim3(tpc, S), kThreads, smem, ctx->stream>>>(buf.as<uint32_t>(), C, sp.r, sp.s, sp.L, ppt,
+        generate_chunk(ctx, wbuf, C);
+        hamming_kernel<<<dim3(tpc, S), kThreads, smem, ctx->stream>>>(wbuf, C, sp.r, sp.s, sp.L, ppt,
                                                                       tile_words, c * tpc * ppt, npairs,
                                                                       table.as<unsigned long long>());
         launched(ctx, "hamming kernel");
@@ -521,21 +623,22 @@ void run_opso(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res) {
     const uint64_t cells = 1ull << (2 * sp.s);
     const uint64_t bm_words = std::max<uint64_t>(1, cells / 32);
     const uint64_t W = sp.n + 1;
-    const uint64_t C = std::min<uint64_t>(kChunkTarget, (W + 3) & ~3ull);
+    const uint64_t C = std::min<uint64_t>(chunk_target(S), (W + 3) & ~3ull);
     const uint64_t chunks = ceil_div(W, C);
-    DevBuf buf, bitmap, prev, coll;
-    alloc(buf, (size_t)S * C * 4, "cudaMalloc stat chunk");
-    alloc(bitmap, (size_t)S * bm_words * 4, "cudaMalloc cell bitmap");
-    alloc(prev, (size_t)S * 2 * 4, "cudaMalloc carry");
-    alloc(coll, (size_t)S * 8, "cudaMalloc collisions");
+    DevBuf bitmap, prev, coll;
+    Arena ar;
+    ar.add(bitmap, (size_t)S * bm_words * 4);
+    ar.add(prev, (size_t)S * 2 * 4);
+    ar.add(coll, (size_t)S * 8);
+    uint32_t* const wbuf = ar.commit(ctx, (size_t)S * C * 4);
     check(cudaMemsetAsync(bitmap.p, 0, (size_t)S * bm_words * 4, ctx->stream), "memset");
     check(cudaMemsetAsync(prev.p, 0, (size_t)S * 2 * 4, ctx->stream), "memset");
     check(cudaMemsetAsync(coll.p, 0, (size_t)S * 8, ctx->stream), "memset");
     const uint32_t gx = (uint32_t)std::min<uint64_t>(ceil_div(C, kThreads), 64);
     for (uint64_t c = 0; c < chunks; ++c) {
-        generate_chunk(ctx, buf.as<uint32_t>(), C);
+        generate_chunk(ctx, wbuf, C);
         uint32_t* carry = prev.as<uint32_t>();
-        opso_kernel<<<dim3(gx, S), kThreads, 0, ctx->stream>>>(buf.as<uint32_t>(), C, c * C, sp.r, sp.s, sp.n,
+        opso_kernel<<<dim3(gx, S), kThreads, 0, ctx->stream>>>(wbuf, C, c * C, sp.r, sp.s, sp.n,
                                                                bitmap.as<uint32_t>(), bm_words,
                                                                carry + (c & 1) * S, carry + ((c + 1) & 1) * S,
                                                                coll.as<unsigned long long>());
@@ -552,19 +655,22 @@ void run_gap(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res) {
     const uint32_t S = ctx->n_sets;
     const stat::GapShape g = stat::gap_shape(sp);
     const uint32_t tcut = (uint32_t)g.tcut;
-    const uint64_t C = kChunkTarget;  // multiple of kGapTile
+    const uint64_t C = (chunk_target(S) + kGapTile - 1) / kGapTile * kGapTile;
     const uint32_t T = (uint32_t)(C / kGapTile);
     const uint64_t max_chunks = ceil_div(g.budget, C);
     const double p = sp.beta - sp.alpha;
     const uint64_t expected_chunks = std::max<uint64_t>(1, (uint64_t)((double)(sp.n + 1) / p / (double)C));
     const bool smem_hist = tcut + 1 <= 12288;
     const size_t smem = smem_hist ? 4 * ((size_t)tcut + 1) : 0;
-    DevBuf buf, counts, tiles, state, end;
-    alloc(buf, (size_t)S * C * 4, "cudaMalloc stat chunk");
-    alloc(counts, (size_t)S * (tcut + 1) * 8, "cudaMalloc counts");
-    alloc(tiles, (size_t)S * T * sizeof(GapTile), "cudaMalloc tiles");
-    alloc(state, (size_t)S * sizeof(GapState), "cudaMalloc gap state");
-    alloc(end, (size_t)S * 8, "cudaMalloc end");
+    DevBuf counts, tiles, pre, state, end, hits;
+    Arena ar;
+    ar.add(hits, (size_t)S * (C / 32) * 4);
+    ar.add(counts, (size_t)S * (tcut + 1) * 8);
+    ar.add(tiles, (size_t)S * T * sizeof(GapTile));
+    ar.add(pre, (size_t)S * T * sizeof(GapPre));
+    ar.add(state, (size_t)S * sizeof(GapState));
+    ar.add(end, (size_t)S * 8);
+    uint32_t* const wbuf = ar.commit(ctx, (size_t)S * C * 4);
     check(cudaMemsetAsync(counts.p, 0, (size_t)S * (tcut + 1) * 8, ctx->stream), "memset");
     std::vector<GapState> hs(S, GapState{0, -1, 0, 0, 0});
     check(cudaMemcpyAsync(state.p, hs.data(), S * sizeof(GapState), cudaMemcpyHostToDevice, ctx->stream), "H2D state");
@@ -573,15 +679,20 @@ void run_gap(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res) {
         check(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attribute");
     for (uint64_t c = 0; c < max_chunks; ++c) {
         const uint64_t P = c * C;
-        generate_chunk(ctx, buf.as<uint32_t>(), C);
-        gap_count_kernel<<<dim3(T, S), kThreads, 0, ctx->stream>>>(buf.as<uint32_t>(), C, P, g.mask, g.lo, g.hi,
-                                                                   g.budget, state.as<GapState>(), tiles.as<GapTile>(), T);
+        generate_chunk(ctx, wbuf, C);
+        gap_count_kernel<<<dim3(T, S), kThreads, 0, ctx->stream>>>(wbuf, C, P, g.mask, g.lo, g.hi, g.budget,
+                                                                   state.as<GapState>(), tiles.as<GapTile>(), T,
+                                                                   hits.as<uint32_t>());
         launched(ctx, "gap count kernel");
-        hk<<<dim3(T, S), kThreads, smem, ctx->stream>>>(buf.as<uint32_t>(), C, P, g.mask, g.lo, g.hi, g.budget,
-                                                        state.as<GapState>(), tiles.as<GapTile>(), T, sp.n, tcut,
+        gap_scan_kernel<<<S, kThreads, 0, ctx->stream>>>(tiles.as<GapTile>(), T, P, state.as<GapState>(),
+                                                         pre.as<GapPre>());
+        launched(ctx, "gap scan kernel");
+        hk<<<dim3(std::min<uint32_t>(T, kGapHistCtas), S), kThreads, smem, ctx->stream>>>(
+                                                        hits.as<uint32_t>(), C, P, state.as<GapState>(),
+                                                        tiles.as<GapTile>(), pre.as<GapPre>(), T, sp.n, tcut,
                                                         counts.as<unsigned long long>(), end.as<unsigned long long>());
         launched(ctx, "gap hist kernel");
-        gap_update_kernel<<<(S + 127) / 128, 128, 0, ctx->stream>>>(tiles.as<GapTile>(), T, S, P, C, g.budget, sp.n,
+        gap_update_kernel<<<(S + 127) / 128, 128, 0, ctx->stream>>>(S, P, C, g.budget, sp.n,
                                                                     end.as<unsigned long long>(), state.as<GapState>());
         launched(ctx, "gap update kernel");
         // poll for completion around the expected length, sparsely before it
