@@ -1,5 +1,6 @@
 """Build and run the C++ drop-in layer's tests (tests/cpp/test_twistsieve_b200.cpp) and the
 jump-ahead algebra test (tests/cpp/test_gf2.cpp)."""
+import json
 import subprocess
 from pathlib import Path
 
@@ -63,3 +64,51 @@ def test_gf2_jump_algebra(tmp_path):
     # the characteristic polynomials of the certified sets digest to the table's poly_sha1
     digests = [line.split()[1] for line in r.stdout.splitlines() if line.strip().startswith("digest")]
     assert digests[:2] == [sets[0].poly_sha1, sets[1].poly_sha1]
+
+
+# ---------------- stat-test layer (include/twistsieve_b200/stat_tests.hpp) ----------------
+
+@pytest.fixture(scope="module")
+def stat_exe(tmp_path_factory):
+    d = tmp_path_factory.mktemp("cpp_stat")
+    return _build(d, "test_stat_b200", [ROOT / "tests/cpp/test_stat_b200.cpp"],
+                  ["-L", str(PKG), "-ltwistsieve_b200", "-lmtgp_b200", f"-Wl,-rpath,{PKG}"])
+
+
+def _stat_cases(tmp_path):
+    """Flatten tests/golden/stat_reference.json (the reference's own results) for the C++ test."""
+    g = json.loads((ROOT / "tests/golden/stat_reference.json").read_text())
+    lines = [f"math {m['fn']} {m['a']} {m['b']} {m['k']} {m['n']} {m['value']}" for m in g["math"] if m["rc"] == 0]
+    for c in g["cases"]:
+        sp = c["spec"]
+        f = [sp["test_id"], sp.get("n", 0), sp.get("r", 0), float(sp.get("alpha", 0.0)).hex(),
+             float(sp.get("beta", 0.0)).hex(), sp.get("s", 0), sp.get("L", 0), sp.get("d", 0), sp.get("l", 0),
+             sp.get("t", 0), c["set"], c["seed"], c["statistic"], c["p_value"], c["classification"], c["degenerate"]]
+        lines.append("case " + " ".join(str(x) for x in f))
+    for c in g["cells"]:
+        lines.append(f"cell {c['spec']['test_id']} {c['seed']} {c['statistic']} {c['p_value']} {c['classification']}")
+    f = tmp_path / "stat_cases.txt"
+    f.write_text("\n".join(lines) + "\n")
+    return f
+
+
+def _curand_header():
+    for d in tables._cuda_include_dirs():
+        if (d / "curand_mtgp32dc_p_11213.h").exists():
+            return d / "curand_mtgp32dc_p_11213.h"
+    pytest.skip("curand_mtgp32dc_p_11213.h not found")
+
+
+def test_cpp_stat_layer_cpu(stat_exe, tmp_path):
+    """Specs, messages, classify and the numerics (bit-exact vs the reference's values), no GPU."""
+    r = subprocess.run([str(stat_exe), str(_stat_cases(tmp_path)), str(_curand_header())],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_stat_layer_gpu(stat_exe, tmp_path):
+    """run_test on MTGP32 streams and run_grid on Engine::mt == the reference's results."""
+    r = subprocess.run([str(stat_exe), str(_stat_cases(tmp_path)), str(_curand_header()), "--gpu"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
