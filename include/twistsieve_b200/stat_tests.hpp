@@ -3,7 +3,7 @@
 //
 // Mirrors proj/include/twistsieve/stat_tests.hpp (TestSpec :18-33, TestResult :35-42, desk specs /
 // named_spec, run_test :313-319), classify.hpp (PValueClass, classify_pvalue) and the campaign
-// grid of proj/include/twistsieve/sieve.hpp (ResultRow, run_grid = sieve.cpp:111-168). The
+// grid of proj/include/twistsieve/sieve.hpp (ResultRow, run_grid = sieve.cpp:116-183). The
 // reference runs one test per fresh stream on one CPU core; here run_test tests every stream of a
 // StreamBatch at once on the GPU (words never leave HBM) and returns what the reference template
 // would return for each stream, bit for bit (statistic, p-value, class, degenerate flag).
@@ -94,7 +94,7 @@ struct ResultRow {
 };
 
 /// Every (status, seed, test) cell on fresh streams, rows ordered (status, seed, test) like
-/// run_grid (sieve.cpp:111-168); all status x seed streams share one GPU context.
+/// run_grid (sieve.cpp:116-183); all status x seed streams share one GPU context.
 std::vector<ResultRow> run_grid(const std::vector<MtStatus>& statuses, const std::vector<std::uint32_t>& seeds,
                                 const std::vector<TestSpec>& specs, int device = 0);
 std::vector<ResultRow> run_grid(const std::vector<MtgpStatus>& statuses, const std::vector<std::uint32_t>& seeds,

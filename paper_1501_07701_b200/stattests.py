@@ -2,7 +2,7 @@
 
 Mirrors proj/include/twistsieve/stat_tests.hpp (TestSpec :18-33, TestResult :35-42, the desk
 specs and named_spec of proj/src/stat_tests.cpp:52-103, run_test :313-319) and the campaign cell
-of proj/src/sieve.cpp:140-168 (one fresh stream per (status, seed, test), rows ordered
+of proj/src/sieve.cpp:116-183 (one fresh stream per (status, seed, test), rows ordered
 (status, seed, test), per-row errors). The words are generated and counted on the GPU
 (csrc/mtgp_stat.cu); the counts -> statistic / p-value step and the numerics are the C-ABI's
 host half (csrc/stat_host.cpp). Everything goes through libmtgp_b200.so; nothing here computes a
@@ -197,7 +197,7 @@ def classify_pvalue(p: float) -> str:
     return CLASSES[out.value]
 
 
-# -- campaign grid (sieve.cpp:140-168 run_grid, GPU-fed)
+# -- campaign grid (sieve.cpp:116-183 run_grid, GPU-fed)
 @dataclass
 class ResultRow:
     """sieve.hpp ResultRow: one (status, seed, test) cell."""
