@@ -189,13 +189,19 @@ def cpu_reference(words_per_thread: int, threads: int):
     return threads * words_per_thread / secs / 1e9, secs
 
 
-def cpu_mtgp_port(sets, seeds, threads: int, n: int = 1 << 24):
+def cpu_mtgp_port(sets, seeds, threads: int, n: int = 1 << 24, min_secs: float = 1.0):
+    """The oracle's MTGP32 bulk fill, one set per thread, repeated into the same buffer until
+    about `min_secs` of wall time (a bounded sample: ~threads x min_secs of CPU work)."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle_py
     k = min(threads, len(sets))
     out = np.empty((k, n), dtype=np.uint32)
-    _, secs = oracle_py.mtgp_bulk(sets[:k], seeds[:k], n, threads=k, out=out)
-    return k * n / secs / 1e9, secs, n
+    secs, reps = 0.0, 0
+    while secs < min_secs and reps < 64:
+        _, s = oracle_py.mtgp_bulk(sets[:k], seeds[:k], n, threads=k, out=out)
+        secs += s
+        reps += 1
+    return k * n * reps / secs / 1e9, secs, n * reps
 
 
 def run_reference(args, rank, world):
