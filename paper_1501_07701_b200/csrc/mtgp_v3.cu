@@ -39,6 +39,12 @@ namespace mtgpb {
 #ifndef MTGP3_CK_WIDE
 #define MTGP3_CK_WIDE 0
 #endif
+// Operand select on the FMA pipe: send = hi * m + lo * (1 - m) with a per-lane 0/1 multiplier
+// (two IMADs instead of one SEL on the ALU pipe). 0: SEL everywhere, 1: IMAD for the A and C
+// streams, 2: A only, 3: C only.
+#ifndef MTGP3_SEL_IMAD
+#define MTGP3_SEL_IMAD 0
+#endif
 
 namespace {
 
@@ -49,6 +55,8 @@ struct V3Ctx {
     uint32_t mask, sh1, sh2, mul1, mulhi2, m16, m24, m23, one, tblr, tmpr;
     uint32_t srcA0, srcA1, srcC0, srcC1;  // source lanes for carry e = 0 / 1
     bool pA0, pA1, pC0, pC1;              // "take the newer half-step" predicates
+    uint32_t mA0, mA1, mC0, mC1;          // the same as 0/1 multipliers (MTGP3_SEL_IMAD)
+    uint32_t nA0, nA1, nC0, nC1;          // 1 - m
 };
 
 __device__ __forceinline__ uint32_t comp4(const uint4& g, int c) {
@@ -99,17 +107,24 @@ __device__ __forceinline__ uint32_t conv3(const V3Ctx& p, uint32_t o) {
 
 // Five consecutive operand words for half-step U from the history half-steps
 // h1 = (k=1), h2 = (k=2), h3 = (k=3); residue R; per-carry source lanes / predicates.
-template <int R, int U>
+template <int R, int U, bool IMAD_SEL>
 __device__ __forceinline__ void fetch5(uint32_t W[5], const uint4& h1, const uint4& h2, const uint4& h3, uint32_t src0,
-                                       uint32_t src1, bool p0, bool p1) {
+                                       uint32_t src1, bool p0, bool p1, uint32_t m0, uint32_t m1, uint32_t n0,
+                                       uint32_t n1) {
 #pragma unroll
     for (int j = 0; j < 5; ++j) {
         const int c = (R + j) & 3;
         const int e = (R + j) >> 2;
         const uint4& lo = U == 0 ? h1 : h2;  // k = 1 + U
         const uint4& hi = U == 0 ? h2 : h3;  // k = 2 + U
-        const bool take_hi = e ? p1 : p0;
-        const uint32_t send = take_hi ? comp4(hi, c) : comp4(lo, c);
+        uint32_t send;
+        if (IMAD_SEL) {
+            // inline PTX keeps the compiler from turning the 0/1 products back into a select
+            uint32_t t;
+            asm("mul.lo.u32 %0, %1, %2;" : "=r"(t) : "r"(comp4(lo, c)), "r"(e ? n1 : n0));
+            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(send) : "r"(comp4(hi, c)), "r"(e ? m1 : m0), "r"(t));
+        } else
+            send = (e ? p1 : p0) ? comp4(hi, c) : comp4(lo, c);
         W[j] = __shfl_sync(FULL, send, e ? src1 : src0);
     }
 }
@@ -121,10 +136,12 @@ __device__ __forceinline__ void step3(const V3Ctx& p, const uint4& h1, const uin
                                       uint4& n1, uint32_t* optr, uint32_t n, uint32_t len, uint32_t* win_out,
                                       uint32_t win_lo, unsigned long long& sum, uint32_t& xr) {
     uint32_t WA[2][5], WC[2][5];
-    fetch5<1, 0>(WA[0], h1, h2, h3, p.srcA0, p.srcA1, p.pA0, p.pA1);
-    fetch5<1, 1>(WA[1], h1, h2, h3, p.srcA0, p.srcA1, p.pA0, p.pA1);
-    fetch5<RC, 0>(WC[0], h1, h2, h3, p.srcC0, p.srcC1, p.pC0, p.pC1);
-    fetch5<RC, 1>(WC[1], h1, h2, h3, p.srcC0, p.srcC1, p.pC0, p.pC1);
+    constexpr bool kImadA = MTGP3_SEL_IMAD == 1 || MTGP3_SEL_IMAD == 2;
+    constexpr bool kImadC = MTGP3_SEL_IMAD == 1 || MTGP3_SEL_IMAD == 3;
+    fetch5<1, 0, kImadA>(WA[0], h1, h2, h3, p.srcA0, p.srcA1, p.pA0, p.pA1, p.mA0, p.mA1, p.nA0, p.nA1);
+    fetch5<1, 1, kImadA>(WA[1], h1, h2, h3, p.srcA0, p.srcA1, p.pA0, p.pA1, p.mA0, p.mA1, p.nA0, p.nA1);
+    fetch5<RC, 0, kImadC>(WC[0], h1, h2, h3, p.srcC0, p.srcC1, p.pC0, p.pC1, p.mC0, p.mC1, p.nC0, p.nC1);
+    fetch5<RC, 1, kImadC>(WC[1], h1, h2, h3, p.srcC0, p.srcC1, p.pC0, p.pC1, p.mC0, p.mC1, p.nC0, p.nC1);
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
         uint32_t r[4], o[4];
@@ -206,6 +223,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MTGP3_MIN_CTAS) gen3_kernel
     p.srcA1 = (lane + 9) & 31;
     p.pA0 = lane < 8;
     p.pA1 = lane < 9;
+    p.mA0 = p.pA0;
+    p.mA1 = p.pA1;
+    p.nA0 = 1u - p.mA0;
+    p.nA1 = 1u - p.mA1;
     const TeamWork tw = a.teams[team];
     for (uint32_t pi = tw.first; pi < tw.first + tw.count; ++pi) {
         const Piece pc = a.pieces[pi];
@@ -227,6 +248,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MTGP3_MIN_CTAS) gen3_kernel
         p.srcC1 = (lane + thr1) & 31;
         p.pC0 = lane < thr0;
         p.pC1 = lane < thr1;
+        p.mC0 = p.pC0;
+        p.mC1 = p.pC1;
+        p.nC0 = 1u - p.mC0;
+        p.nC1 = 1u - p.mC1;
         uint32_t* optr = reinterpret_cast<uint32_t*>(a.out) + (size_t)pc.set * a.L + pc.offset;
         const uint32_t len = (uint32_t)pc.len;
         const uint32_t* w0 = a.piece_win[pi];

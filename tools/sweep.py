@@ -4,7 +4,10 @@ Variants are measured in interleaved rounds (A B C A B C ...) so power-cap clock
 favour whichever ran first; the SM clock is sampled through NVML during each measurement and
 the result is reported both as GB/s and as SM cycles per launch (clock-independent).
 
-    python tools/sweep.py [words_per_stream] [kind] [mexp] [rounds]
+    python tools/sweep.py [words_per_stream] [kind] [mexp] [rounds] [cksum] [sustain_seconds]
+
+sustain_seconds > 0: instead of best-of short bursts, each variant generates back to back for
+that long per round (the power-capped regime the bench runs in) and the AVERAGE rate is kept.
 """
 import json
 import statistics
@@ -24,6 +27,7 @@ kind = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 mexp = int(sys.argv[3]) if len(sys.argv) > 3 else 11213
 rounds = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 cksum = int(sys.argv[5]) if len(sys.argv) > 5 else 1
+sustain = float(sys.argv[6]) if len(sys.argv) > 6 else 0.0
 
 try:
     import pynvml
@@ -64,8 +68,13 @@ for r in range(rounds):
         clk = Clock()
         th = threading.Thread(target=clk.run)
         th.start()
-        for _ in range(2):
+        t_end = time.perf_counter() + sustain
+        calls = 0
+        while calls < 2 or time.perf_counter() < t_end:
             ctx.generate_device(kind, out.data_ptr(), words)
+            calls += 1
+            if sustain:
+                ctx.sync()
         g, gn, j, jn = ctx.kernel_timing()
         clk.stop = True
         th.join()
@@ -74,11 +83,16 @@ for r in range(rounds):
         res[name].append((g / gn, j / max(1, jn), mhz))
 for name, ctx in ctxs:
     pieces, _, kv = ctx.last_plan()
-    ms = min(x[0] for x in res[name])
-    best = min(res[name], key=lambda x: x[0])
+    if sustain:  # the average over the sustained rounds, not the best
+        ms = statistics.mean(x[0] for x in res[name])
+        best = (ms, statistics.mean(x[1] for x in res[name]), statistics.median(x[2] for x in res[name]))
+    else:
+        ms = min(x[0] for x in res[name])
+        best = min(res[name], key=lambda x: x[0])
     cycles = min(x[0] * 1e-3 * x[2] * 1e6 for x in res[name])
     print(json.dumps({"variant": name, "gen_ms": round(ms, 4), "gen_GBps": round(4.0 * 200 * words / (ms / 1e3) / 1e9, 1),
                       "mcycles_per_launch": round(cycles / 1e6, 3), "mhz_at_best": best[2],
-                      "jump_ms": round(best[1], 4), "pieces": pieces, "kernel": kv, "kind": kind, "mexp": mexp, "cksum": cksum}),
+                      "jump_ms": round(best[1], 4), "pieces": pieces, "kernel": kv, "kind": kind, "mexp": mexp, "cksum": cksum,
+                      "sustain_s": sustain}),
           flush=True)
     ctx.close()

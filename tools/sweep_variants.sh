@@ -7,7 +7,7 @@ ROOT=$(cd "$(dirname "$0")/.." && pwd)
 CS=$ROOT/paper_1501_07701_b200/csrc
 OUT=$ROOT/paper_1501_07701_b200/variants
 mkdir -p $OUT
-OBJS="$CS/build/mtgp_capi.o $CS/build/mtgp_v1.o $CS/build/mtgp_plan.o $CS/build/mtgp_mt.o $CS/build/gf2.o $CS/build/sha1.o"
+OBJS="$CS/build/mtgp_capi.o $CS/build/mtgp_v1.o $CS/build/mtgp_plan.o $CS/build/mtgp_mt.o $CS/build/mtgp_stat.o $CS/build/gf2.o $CS/build/sha1.o $CS/build/stat_host.o"
 NV="nvcc -gencode arch=compute_100a,code=sm_100a -std=c++17 -O3 -lineinfo -Xcompiler -fPIC -I$ROOT/include -I$CS"
 build() {
   name=$1; shift
