@@ -417,9 +417,14 @@ int mtgp_generate(mtgp_ctx* ctx, int kind, void* out, uint64_t L, int out_is_dev
         ctx->stage_bytes = 2 * chunk_bytes;
     }
     char* host = static_cast<char*>(out);
+    // Chunk sizes ramp up 16x per chunk from a small first chunk: the copy engine starts after
+    // ~1/64 of a chunk's generation instead of a whole one (generation outruns PCIe ~20x, so
+    // the ramp never starves the copy). Lengths stay multiples of 4 words (v3 eligibility).
+    uint64_t next_len = std::max<uint64_t>(std::min<uint64_t>(Lc, 4096), (Lc >> 6) & ~3ull);
     int c = 0;
-    for (uint64_t done = 0; done < L; done += Lc, ++c) {
-        const uint64_t len = std::min<uint64_t>(Lc, L - done);
+    for (uint64_t done = 0, len = 0; done < L; done += len, ++c) {
+        len = std::min<uint64_t>(next_len, L - done);
+        next_len = std::min<uint64_t>(Lc, next_len * 16);
         const int b = c & 1;
         char* stage = static_cast<char*>(ctx->d_stage) + b * chunk_bytes;
         // buffer b is free once its previous copy finished
