@@ -292,3 +292,18 @@ def test_short_skip_generates(curand_sets):
         o = oracle_py.MtgpOracle(sets[s], 3 + s)
         o.skip(103)
         assert np.array_equal(w[s], o.fill(1000))
+
+
+@pytest.mark.parametrize("host_chunk,L", [(1, 37), (3, 1000), (4096, 4095), (4097, 100003), (1 << 18, 1 << 20),
+                                          (1 << 18, (1 << 20) + 6), (65536, 300001)])
+def test_host_output_chunk_ramp(curand_sets, host_chunk, L):
+    """Host-memory output goes through ramped device chunks (first chunk small, then x16 up to
+    OPT_HOST_CHUNK): every chunking must give the same words, and the stream must continue."""
+    sets = curand_sets[10:13]
+    with _ctx(sets, [7, 8, 9], 0, {mtgp.OPT_HOST_CHUNK: host_chunk}) as ctx:
+        a = ctx.fill_u32(L)
+        b = ctx.fill_u32(5)
+        ck = ctx.checksums()
+    ref, _ = oracle_py.mtgp_bulk(sets, [7, 8, 9], L + 5, threads=3)
+    assert np.array_equal(a, ref[:, :L]) and np.array_equal(b, ref[:, L:])
+    assert all(c[2] == L + 5 for c in ck)
