@@ -2,6 +2,8 @@
 //   1. HBM write-only peak: coalesced STG.128 grid-stride stores, and cudaMemsetAsync
 //   2. MIO pipe: SHFL.IDX and LDS.128 / LDS.32 throughput per SM per clock
 //   3. STG.128 with a 32-byte lane stride (a lane owning 8 consecutive words) vs contiguous
+//   4. TMA bulk stores (cp.async.bulk.global.shared::cta, 16 KB per op) from a double-buffered
+//      shared-memory stage -- the store path north_star names, against direct STG.128
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench tools/microbench.cu
 #include <cuda_runtime.h>
@@ -35,6 +37,32 @@ __global__ void store_stride32(uint4* __restrict__ p, size_t n4, uint32_t v) {
         __stcs(q, make_uint4(v, lane, v, v));
         __stcs(q + 1, make_uint4(v, lane, v + 1, v));
     }
+}
+
+// Each CTA fills a 16 KB shared-memory stage (STS.128) and one thread bulk-stores it with TMA;
+// two stages, so filling one overlaps the bulk store of the other.
+constexpr uint32_t kTmaChunk = 16384;
+__global__ void __launch_bounds__(256) store_tma(char* __restrict__ p, size_t bytes, uint32_t v) {
+    extern __shared__ __align__(128) uint4 stage[];
+    const size_t nch = bytes / kTmaChunk;
+    uint32_t b = 0;
+    for (size_t c = blockIdx.x; c < nch; c += gridDim.x, b ^= 1u) {
+        uint4* s = stage + b * (kTmaChunk / 16);
+        // the bulk store issued two chunks ago (same stage) must have finished reading it
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < kTmaChunk / 16; i += blockDim.x) s[i] = make_uint4(v, i, v + 1, (uint32_t)c);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const uint32_t saddr = static_cast<uint32_t>(__cvta_generic_to_shared(s));
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(p + c * kTmaChunk),
+                         "r"(saddr), "r"(kTmaChunk)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 __global__ void shfl_tput(uint32_t* out, int iters) {
@@ -126,6 +154,20 @@ int main() {
             if (ms < best) best = ms;
         }
         printf(", \"memset_GBps\": %.1f", bytes / (best * 1e6));
+    }
+    // 4. TMA bulk stores, 2..6 CTAs (32 KB stage each) per SM
+    CK(cudaFuncSetAttribute(store_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kTmaChunk));
+    for (int per_sm : {2, 4, 6}) {
+        float best = 1e30f;
+        for (int r = 0; r < 5; ++r) {
+            CK(cudaEventRecord(a));
+            store_tma<<<sms * per_sm, 256, 2 * kTmaChunk>>>(reinterpret_cast<char*>(buf), bytes, r);
+            CK(cudaEventRecord(b));
+            CK(cudaEventSynchronize(b));
+            CK(cudaEventElapsedTime(&ms, a, b));
+            if (ms < best) best = ms;
+        }
+        printf(", \"tma_bulk_store_%dcta_GBps\": %.1f", per_sm, bytes / (best * 1e6));
     }
     // 2. MIO throughput; report per-SM ops per ns (divide by GHz for per-clock)
     const int iters = 20000;
