@@ -84,7 +84,8 @@ typedef struct mtgp_ctx mtgp_ctx;
 /* Options for mtgp_set_option */
 #define MTGP_OPT_CHECKSUM 1        /* 0/1: accumulate mtgp_cksum in-kernel (default 1)              */
 #define MTGP_OPT_KERNEL 2          /* 0 = auto, 1 = reference-shaped v1 (one CTA per set), 2 = v2 */
-                                   /* (shared-memory ring), 3 = v3 (register ring, mexp 11213)    */
+                                   /* (shared-memory ring), 3 = v3 (register ring, mexp 11213),   */
+                                   /* 4 = v4 (register ring for any supported exponent)           */
 #define MTGP_OPT_MAX_PIECES 3      /* cap on jump-ahead pieces per call (0 = auto)                  */
 #define MTGP_OPT_MIN_PIECE_WORDS 4 /* minimum words per jump-ahead piece (default 1<<21)            */
 #define MTGP_OPT_TIMING 5          /* 0/1: record CUDA events around every generation kernel        */

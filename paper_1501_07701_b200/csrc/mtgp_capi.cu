@@ -300,7 +300,7 @@ int mtgp_set_option(mtgp_ctx* ctx, int option, int64_t value) {
     switch (option) {
         case MTGP_OPT_CHECKSUM: ctx->cksum = value != 0; return MTGP_OK;
         case MTGP_OPT_KERNEL:
-            if (value < 0 || value > 3) return fail(MTGP_EINVAL, "kernel must be 0 (auto), 1, 2 or 3");
+            if (value < 0 || value > 4) return fail(MTGP_EINVAL, "kernel must be 0 (auto), 1, 2, 3 or 4");
             ctx->kernel = (int)value;
             return MTGP_OK;
         case MTGP_OPT_MAX_PIECES:

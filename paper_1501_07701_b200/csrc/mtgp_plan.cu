@@ -360,13 +360,26 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     }
     // v3 (register-resident ring) serves MTGP32-11213 when every piece starts 16-byte aligned:
     // 16-byte aligned output, L % 4 == 0 (piece offsets are multiples of 4 by construction)
-    const bool v3_ok = I.M == 11213 && r.L % 4 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 15) == 0;
+    const bool reg_ok = r.L % 4 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 15) == 0;
+    const bool v3_ok = I.M == 11213 && reg_ok;
+    const bool v4_ok = v4_supports(I.M, r.kind) && reg_ok;
     if (r.want_kernel == 3 && !v3_ok) {
         err = "kernel v3 needs mexp 11213, words_per_stream % 4 == 0 and 16-byte aligned output";
         return cudaSuccess;
     }
-    const bool use_v3 = v3_ok && r.want_kernel != 2;
-    const int cps = use_v3 ? gen3_ctas_per_sm(r.kind, r.cksum) : gen_ctas_per_sm(I.M, r.kind, r.cksum);
+    if (r.want_kernel == 4 && !v4_ok) {
+        err = "kernel v4 needs mexp 11213/23209/44497, u32 output, words_per_stream % 4 == 0 and 16-byte aligned output";
+        return cudaSuccess;
+    }
+    // auto: v3 for 11213; v4 (the same register-resident design, templated on N) for 23209, where
+    // it beats the shared-memory ring by 13-17%; v2 for 44497 (v4's 36 C-stream variants of a
+    // 12-half-step history thrash the instruction cache there: 93.6 vs 60.5 M cycles per launch,
+    // profiles/r1_v4_sweep.jsonl) and for request shapes the register kernels do not take
+    const bool use_v3 = v3_ok && (r.want_kernel == 3 || (r.want_kernel == 0 && I.M == 11213));
+    const bool use_v4 = !use_v3 && v4_ok && (r.want_kernel == 4 || (r.want_kernel == 0 && I.M == 23209));
+    const int cps = use_v3   ? gen3_ctas_per_sm(r.kind, r.cksum)
+                    : use_v4 ? gen4_ctas_per_sm(I.M, r.kind, r.cksum)
+                             : gen_ctas_per_sm(I.M, r.kind, r.cksum);
     if (cps <= 0) {
         err = "generation kernel cannot be resident";
         return cudaSuccess;
@@ -430,10 +443,11 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     ga.L = r.L;
     ga.ck = r.ck;
     if (r.timing) r.timing->record(r.stream, &g0);
-    if ((e = use_v3 ? launch_gen3(r.kind, r.cksum, ga, r.stream) : launch_gen(I.M, r.kind, r.cksum, ga, r.stream)) !=
-        cudaSuccess)
-        return e;
-    r.version = use_v3 ? 3 : 2;
+    e = use_v3   ? launch_gen3(r.kind, r.cksum, ga, r.stream)
+        : use_v4 ? launch_gen4(I.M, r.kind, r.cksum, ga, r.stream)
+                 : launch_gen(I.M, r.kind, r.cksum, ga, r.stream);
+    if (e != cudaSuccess) return e;
+    r.version = use_v3 ? 3 : use_v4 ? 4 : 2;
     if (r.timing) {
         r.timing->record(r.stream, &g1);
         r.timing->gen.push_back({g0, g1});

@@ -409,7 +409,10 @@ cudaError_t launch_prefix(const DevParams* params, const uint32_t* win, const ui
 // prefix is staged in shared memory; each warp takes one job (piece) at a time; lane l keeps
 // a sliding window of J consecutive j's in registers and walks q two bits at a time.
 // ------------------------------------------------------------------------------------------
-constexpr int kJumpJ = 12;
+#ifndef MTGP_JUMP_J
+#define MTGP_JUMP_J 12
+#endif
+constexpr int kJumpJ = MTGP_JUMP_J;  // outputs per lane per pass (multiple of 4)
 constexpr int kJumpWarps = 8;
 
 template <uint32_t MEXP>
@@ -484,13 +487,18 @@ __global__ void __launch_bounds__(kJumpFlatWarps * 32) jump_flat_kernel(JumpArgs
     constexpr uint32_t N = MEXP / 32 + 1;
     constexpr int J = kJumpJ;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t job = blockIdx.x * kJumpFlatWarps + warp;
+    // one warp per (job, pass): a pass is 32*J consecutive outputs of the job's window, so a
+    // 44497 window (4 passes) runs on 4 warps instead of 4 sequential passes of one warp
+    constexpr uint32_t kPasses = (N + 32 * J - 1) / (32 * J);
+    const uint32_t unit = blockIdx.x * kJumpFlatWarps + warp;
+    const uint32_t job = unit / kPasses;
     if (job >= a.n_jobs) return;
     const JumpJob jb = a.jobs[job];
     const uint4* x4 = reinterpret_cast<const uint4*>(a.pre + (size_t)jb.row * a.pre_stride + a.pre_off);
     const uint32_t* q = a.q + (size_t)jb.q * a.q_words;
     uint32_t* dst = a.piece_win + (size_t)jb.piece * N;
-    for (uint32_t j0 = 0; j0 < N; j0 += 32 * J) {
+    {
+        const uint32_t j0 = (unit % kPasses) * 32 * J;
         const uint32_t jl = j0 + J * lane;  // multiple of 4
         uint32_t acc[J];
 #pragma unroll
@@ -541,7 +549,9 @@ template <uint32_t MEXP>
 static cudaError_t launch_jump_t(const JumpArgs& a, uint32_t n_rows, cudaStream_t st) {
     if (MTGP_JUMP_FLAT) {
         if (a.n_jobs == 0) return cudaSuccess;
-        jump_flat_kernel<MEXP><<<(a.n_jobs + kJumpFlatWarps - 1) / kJumpFlatWarps, kJumpFlatWarps * 32, 0, st>>>(a);
+        constexpr uint32_t N = MEXP / 32 + 1, kPasses = (N + 32 * kJumpJ - 1) / (32 * kJumpJ);
+        const uint32_t units = a.n_jobs * kPasses;
+        jump_flat_kernel<MEXP><<<(units + kJumpFlatWarps - 1) / kJumpFlatWarps, kJumpFlatWarps * 32, 0, st>>>(a);
         return cudaGetLastError();
     }
     const size_t smem = (size_t)a.pre_len * 4;

@@ -307,3 +307,39 @@ def test_host_output_chunk_ramp(curand_sets, host_chunk, L):
     ref, _ = oracle_py.mtgp_bulk(sets, [7, 8, 9], L + 5, threads=3)
     assert np.array_equal(a, ref[:, :L]) and np.array_equal(b, ref[:, L:])
     assert all(c[2] == L + 5 for c in ck)
+
+
+def _sets_for(mexp, k, curand_sets):
+    return curand_sets[:k] if mexp == 11213 else tables.synthetic_sets(mexp, k)
+
+
+@pytest.mark.parametrize("mexp", [11213, 23209, 44497])
+def test_v4_bit_exact_with_jumps(curand_sets, mexp):
+    """v4 (gen3's register-resident design templated on N) over jump-ahead pieces."""
+    sets = _sets_for(mexp, 8, curand_sets)
+    seeds = list(range(31, 39))
+    L = (1 << 18) + 12
+    with _ctx(sets, seeds, 4, {mtgp.OPT_MIN_PIECE_WORDS: 1 << 13}) as ctx:
+        a = ctx.fill_u32(L)
+        pieces, _, kv = ctx.last_plan()
+        b = ctx.fill_u32(4096)
+        ck = ctx.checksums()
+    assert kv == 4 and pieces > 8
+    ref, _ = oracle_py.mtgp_bulk(sets, seeds, L + 4096, threads=8)
+    assert np.array_equal(a, ref[:, :L]) and np.array_equal(b, ref[:, L:])
+    for s in range(8):
+        c = oracle_py.cksum(ref[s])
+        assert ck[s] == (c["sum64"], c["xor32"], L + 4096)
+
+
+@pytest.mark.parametrize("mexp", [11213, 23209, 44497])
+@pytest.mark.parametrize("L", [4, 256, 260, 728, 1024, 1392, 3000, 65536 + 12])
+def test_v4_short_and_edge_lengths(curand_sets, mexp, L):
+    """Tail steps and the end-window hand-off at lengths around N and the step size; the
+    next call must continue the stream exactly."""
+    sets = _sets_for(mexp, 3, curand_sets)
+    with _ctx(sets, [5, 6, 7], 4) as ctx:
+        a = ctx.fill_u32(L)
+        b = ctx.fill_u32(1000 + 4 * (L % 3))
+    ref, _ = oracle_py.mtgp_bulk(sets, [5, 6, 7], L + b.shape[1], threads=3)
+    assert np.array_equal(a, ref[:, :L]) and np.array_equal(b, ref[:, L:])

@@ -4,7 +4,9 @@ Variants are measured in interleaved rounds (A B C A B C ...) so power-cap clock
 favour whichever ran first; the SM clock is sampled through NVML during each measurement and
 the result is reported both as GB/s and as SM cycles per launch (clock-independent).
 
-    python tools/sweep.py [words_per_stream] [kind] [mexp] [rounds] [cksum] [sustain_seconds]
+    python tools/sweep.py [words_per_stream] [kind] [mexp] [rounds] [cksum] [sustain_seconds] [kernels]
+
+kernels: comma-separated MTGP_OPT_KERNEL values to compare within each library (default 0 = auto).
 
 sustain_seconds > 0: instead of best-of short bursts, each variant generates back to back for
 that long per round (the power-capped regime the bench runs in) and the AVERAGE rate is kept.
@@ -28,6 +30,7 @@ mexp = int(sys.argv[3]) if len(sys.argv) > 3 else 11213
 rounds = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 cksum = int(sys.argv[5]) if len(sys.argv) > 5 else 1
 sustain = float(sys.argv[6]) if len(sys.argv) > 6 else 0.0
+kernels = [int(k) for k in sys.argv[7].split(",")] if len(sys.argv) > 7 else [0]  # MTGP_OPT_KERNEL values
 
 try:
     import pynvml
@@ -55,11 +58,13 @@ libs.insert(0, mtgp.LIB_PATH)
 ctxs = []
 for path in libs:
     lib = mtgp.load_library(str(path))
-    ctx = mtgp.MtgpContext(sets, [1] * 200, lib=lib)
-    ctx.set_option(mtgp.OPT_CHECKSUM, cksum)
-    ctx.generate_device(kind, out.data_ptr(), words)  # plan + warm
-    ctx.sync()
-    ctxs.append((path.stem, ctx))
+    for kern in kernels:
+        ctx = mtgp.MtgpContext(sets, [1] * 200, lib=lib)
+        ctx.set_option(mtgp.OPT_CHECKSUM, cksum)
+        ctx.set_option(mtgp.OPT_KERNEL, kern)
+        ctx.generate_device(kind, out.data_ptr(), words)  # plan + warm
+        ctx.sync()
+        ctxs.append((path.stem + ("" if kernels == [0] else f"/k{kern}"), ctx))
 res = {name: [] for name, _ in ctxs}
 for r in range(rounds):
     for name, ctx in ctxs:

@@ -7,14 +7,24 @@ ROOT=$(cd "$(dirname "$0")/.." && pwd)
 CS=$ROOT/paper_1501_07701_b200/csrc
 OUT=$ROOT/paper_1501_07701_b200/variants
 mkdir -p $OUT
-OBJS="$CS/build/mtgp_capi.o $CS/build/mtgp_v1.o $CS/build/mtgp_plan.o $CS/build/mtgp_mt.o $CS/build/mtgp_stat.o $CS/build/gf2.o $CS/build/sha1.o $CS/build/stat_host.o"
+OBJS=$(ls $CS/build/*.o)
 NV="nvcc -gencode arch=compute_100a,code=sm_100a -std=c++17 -O3 -lineinfo -Xcompiler -fPIC -I$ROOT/include -I$CS"
+# VARIANT_SRCS (default: the v2 + v3 kernels) are rebuilt with the variant's flags and replace
+# their objects from the main build.
+VARIANT_SRCS=${VARIANT_SRCS:-"mtgp_v2 mtgp_v3"}
 build() {
   name=$1; shift
-  $NV "$@" -c $CS/mtgp_v2.cu -o $OUT/$name.v2.o
-  $NV "$@" -c $CS/mtgp_v3.cu -o $OUT/$name.v3.o
-  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT/$name.so $OBJS $OUT/$name.v2.o $OUT/$name.v3.o -lpthread
-  rm -f $OUT/$name.v2.o $OUT/$name.v3.o
+  objs=""
+  for f in $OBJS; do
+    b=$(basename $f .o)
+    case " $VARIANT_SRCS " in *" $b "*) ;; *) objs="$objs $f";; esac
+  done
+  for v in $VARIANT_SRCS; do
+    $NV "$@" -c $CS/$v.cu -o $OUT/$name.$v.o
+    objs="$objs $OUT/$name.$v.o"
+  done
+  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT/$name.so $objs -lpthread
+  for v in $VARIANT_SRCS; do rm -f $OUT/$name.$v.o; done
 }
 for v in "$@"; do
   IFS=: read name flags <<< "$v"
