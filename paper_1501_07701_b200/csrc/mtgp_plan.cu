@@ -371,12 +371,11 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         err = "kernel v4 needs mexp 11213/23209/44497, u32 output, words_per_stream % 4 == 0 and 16-byte aligned output";
         return cudaSuccess;
     }
-    // auto: v3 for 11213; v4 (the same register-resident design, templated on N) for 23209, where
-    // it beats the shared-memory ring by 13-17%; v2 for 44497 (v4's 36 C-stream variants of a
-    // 12-half-step history thrash the instruction cache there: 93.6 vs 60.5 M cycles per launch,
-    // profiles/r1_v4_sweep.jsonl) and for request shapes the register kernels do not take
+    // auto: v3 for 11213; v4 (the same register-resident design, templated on N) for 23209 and
+    // 44497, where it beats the shared-memory ring by 18% / 27% (profiles/r1_v4_sweep.jsonl);
+    // v2 for request shapes the register kernels do not take (float kinds, L % 4 != 0, ...)
     const bool use_v3 = v3_ok && (r.want_kernel == 3 || (r.want_kernel == 0 && I.M == 11213));
-    const bool use_v4 = !use_v3 && v4_ok && (r.want_kernel == 4 || (r.want_kernel == 0 && I.M == 23209));
+    const bool use_v4 = !use_v3 && v4_ok && (r.want_kernel == 4 || (r.want_kernel == 0 && I.M != 11213));
     const int cps = use_v3   ? gen3_ctas_per_sm(r.kind, r.cksum)
                     : use_v4 ? gen4_ctas_per_sm(I.M, r.kind, r.cksum)
                              : gen_ctas_per_sm(I.M, r.kind, r.cksum);

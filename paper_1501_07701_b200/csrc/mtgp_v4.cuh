@@ -29,6 +29,9 @@ namespace mtgpb {
 #ifndef MTGP4_UNROLL
 #define MTGP4_UNROLL 1
 #endif
+#ifndef MTGP4_BIG_CTA
+#define MTGP4_BIG_CTA 1
+#endif
 #ifndef MTGP4_MIN_CTAS
 #define MTGP4_MIN_CTAS 0  // 0: by history depth (6 / 5 / 4 CTAs for K = 2 / 3 / >= 4)
 #endif
@@ -49,6 +52,10 @@ struct S4 {
     static constexpr uint32_t AC_MAX = H - 3;            // pos <= N - 256
     static constexpr int MIN_CTAS = MTGP4_MIN_CTAS ? MTGP4_MIN_CTAS : (K == 2 ? 6 : K == 3 ? 5 : 4);
     static constexpr uint32_t U = MTGP4_UNROLL ? MTGP4_UNROLL : K;  // steps per main-loop trip
+    // One CTA per SM holding all of the SM's warps (MIN_CTAS x 4): teams are ordered by stream,
+    // so a CTA's warps share one or two streams -- one or two C-stream variants per SM instead of
+    // one per 4-warp CTA (the variants otherwise thrash the instruction cache).
+    static constexpr uint32_t WARPS = MTGP4_BIG_CTA ? 4u * MIN_CTAS : kWarpsPerCta;
 };
 
 struct V4Ctx {
@@ -196,11 +203,12 @@ __device__ __forceinline__ void run_ac(int ac, int rc, const V4Ctx& p, uint4 (&H
 }  // namespace
 
 template <uint32_t MEXP, int KIND, bool CK>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, S4<MEXP>::MIN_CTAS) gen4_kernel(GenArgs a) {
+__global__ void __launch_bounds__(S4<MEXP>::WARPS * 32, S4<MEXP>::MIN_CTAS * kWarpsPerCta / S4<MEXP>::WARPS)
+    gen4_kernel(GenArgs a) {
     using S = S4<MEXP>;
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t team = blockIdx.x * kWarpsPerCta + warp;
+    const uint32_t team = blockIdx.x * S::WARPS + warp;
     if (team >= a.n_teams) return;
     V4Ctx p;
     p.lane = lane;
@@ -267,18 +275,19 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, S4<MEXP>::MIN_CTAS) gen4_ke
 
 template <uint32_t MEXP, int KIND, bool CK>
 static cudaError_t launch4_t(const GenArgs& a, cudaStream_t st) {
-    const uint32_t grid = (a.n_teams + kWarpsPerCta - 1) / kWarpsPerCta;
-    gen4_kernel<MEXP, KIND, CK><<<grid, kWarpsPerCta * 32, 0, st>>>(a);
+    constexpr uint32_t W = S4<MEXP>::WARPS;
+    const uint32_t grid = (a.n_teams + W - 1) / W;
+    gen4_kernel<MEXP, KIND, CK><<<grid, W * 32, 0, st>>>(a);
     return cudaGetLastError();
 }
 
 template <uint32_t MEXP, int KIND, bool CK>
 static int occ4_t() {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gen4_kernel<MEXP, KIND, CK>, kWarpsPerCta * 32, 0) !=
-        cudaSuccess)
+    constexpr uint32_t W = S4<MEXP>::WARPS;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gen4_kernel<MEXP, KIND, CK>, W * 32, 0) != cudaSuccess)
         return 0;
-    return n;
+    return n * (int)(W / kWarpsPerCta);  // in the planner's unit: resident 4-warp teams groups
 }
 
 // Per-exponent entry points (one translation unit each: mtgp_v4_<mexp>.cu), u32 output only.
