@@ -204,6 +204,28 @@ int mtgp_mt_ctx_create(mtgp_ctx** out, int device, const mtgp_mt_params* sets, u
 int mtgp_last_plan(const mtgp_ctx* ctx, uint32_t* pieces, uint32_t* warps_per_piece,
                    uint32_t* kernel_version);
 
+/*
+ * Certification (table tooling): out[s] = 1 iff stream s's minimal polynomial,
+ * taken from its current state, has degree mexp and is irreducible -- the maximal-period test the
+ * reference's dynamic creator accepts a status by (proj/src/dynamic_creator.cpp:79-81,
+ * is_irreducible gf2poly.cpp:342-383). MTGP32 and Engine::mt contexts. State is unchanged.
+ */
+int mtgp_certify(mtgp_ctx* ctx, int32_t* out);
+
+/*
+ * Engine::mt contexts: the reference's poly_digest (proj/src/dynamic_creator.cpp:9-31) of each
+ * stream's minimal polynomial probed from bit 0 of its next 2*mexp + 64 outputs
+ * (probe_minimal_polynomial, :33-38). For a context seeded with kDefaultProbeSeed (1) this is
+ * the digest verify_digest compares with ParameterizedStatus::charpoly_digest (:99-103).
+ * out: 41 bytes per stream (40 hex digits + NUL). State is unchanged.
+ */
+int mtgp_mt_charpoly_digest(mtgp_ctx* ctx, char* out);
+
+/* The irreducibility test alone (host): coeff_bits[i] (0/1, one byte per coefficient, the
+   reference's Gf2Poly::from_coeff_bits layout) is the coefficient of x^i. MTGP_EINVAL for a
+   constant polynomial, like the reference's is_irreducible. */
+int mtgp_gf2_is_irreducible(const uint8_t* coeff_bits, uint64_t n, int32_t* out);
+
 /* ------------------------------------------------------------------------------------------
  * Device-side statistical tests (GPU-fed consumers).
  *

@@ -144,6 +144,11 @@ public:
     void skip(std::uint64_t words);
     std::uint64_t position(std::uint32_t s) const;
     std::vector<mtgp_cksum> checksums() const;
+    /// Per stream: minimal polynomial (from the current state) of degree mexp and irreducible,
+    /// the reference dynamic creator's acceptance test (dynamic_creator.cpp:79-81).
+    std::vector<bool> certify();
+    /// Engine::mt batches: the reference's poly_digest of each stream's probed minimal polynomial.
+    std::vector<std::string> mt_charpoly_digests();
     void set_option(int option, std::int64_t value);
     void synchronize();
     mtgp_ctx* handle() { return ctx_; }
@@ -178,6 +183,10 @@ private:
     std::size_t pos_ = 0, len_ = 0;
     std::uint64_t consumed_ = 0;
 };
+
+/// verify_digest (proj/src/dynamic_creator.cpp:99-103) on the GPU: the digest of the status's
+/// minimal polynomial probed from a generator seeded with kDefaultProbeSeed (1) equals `digest`.
+bool verify_digest(const MtStatus& status, const std::string& digest, int device = 0);
 
 /// Factory with the reference's shape (word_source.cpp:5-16).
 std::unique_ptr<WordSource> make_word_source(const MtgpStatus& params, std::uint32_t seed);

@@ -1,6 +1,7 @@
-// ref_stat_harness.cpp -- extern "C" shim over the UNMODIFIED reference statistical tests,
-// compiled with the reference's own sources (proj/src/{stat_tests,stats,classify}.cpp and the
-// header templates proj/include/twistsieve/stat_tests.hpp:83-309) into
+// ref_stat_harness.cpp -- extern "C" shim over the UNMODIFIED reference statistical tests and
+// parameter-set tooling, compiled with the reference's own sources
+// (proj/src/{stat_tests,stats,classify,gf2poly,dynamic_creator}.cpp and the header templates
+// proj/include/twistsieve/stat_tests.hpp:83-309) into
 // oracle/_ref/libtwistsieve_ref.so by oracle/Makefile. TEST INFRASTRUCTURE ONLY: the checker for
 // the device-side stat tests (tests/test_stat_*.py) and the generator of
 // tests/golden/stat_reference.json.
@@ -12,8 +13,11 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "twistsieve/classify.hpp"
+#include "twistsieve/dynamic_creator.hpp"
+#include "twistsieve/gf2poly.hpp"
 #include "twistsieve/params.hpp"
 #include "twistsieve/stat_tests.hpp"
 #include "twistsieve/stats.hpp"
@@ -213,6 +217,55 @@ int ref_gap_tcut(const ref_stat_spec* spec, uint64_t* tcut) {
         g_msg = e.what();
         return 1;
     }
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// The reference's is_irreducible (gf2poly.cpp:342-383) on sum_i bits[i] x^i.
+// Returns 1 / 0, or -1 if it throws (constant polynomial).
+int ref_is_irreducible(const uint8_t* bits, uint64_t n) {
+    try {
+        return is_irreducible(Gf2Poly::from_coeff_bits(std::span<const std::uint8_t>(bits, n))) ? 1 : 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// poly_digest(probe_minimal_polynomial(Generator(status, seed), mexp)) and its degree
+// (dynamic_creator.cpp:9-38). status12 == NULL: mt19937_params().
+int ref_mt_probe_digest(const uint32_t* status12, uint32_t seed, char* out41, int* degree) {
+    try {
+        const ParameterizedStatus p = status12 ? status_from12(status12) : mt19937_params();
+        const Gf2Poly poly = probe_minimal_polynomial(Generator(p, seed), p.mexp);
+        const std::string d = poly_digest(poly);
+        std::memset(out41, 0, 41);
+        std::memcpy(out41, d.data(), std::min<size_t>(40, d.size()));
+        *degree = poly.degree();
+        return 0;
+    } catch (const std::exception& e) {
+        g_msg = e.what();
+        return 1;
+    }
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// The reference's dc_search acceptance test (dynamic_creator.cpp:79-81) on an arbitrary word
+// stream: berlekamp_massey over bit 0 of words[0, 2*mexp + 64) (probe_minimal_polynomial,
+// :33-38), then degree == mexp && is_irreducible. *irreducible = -1 when the degree differs.
+int ref_bit0_certify(const uint32_t* words, uint64_t nwords, uint32_t mexp, int* degree, int* irreducible) {
+    const std::size_t nbits = 2 * static_cast<std::size_t>(mexp) + 64;
+    if (nwords < nbits) return 1;
+    std::vector<std::uint8_t> bits(nbits);
+    for (std::size_t k = 0; k < nbits; ++k) bits[k] = static_cast<std::uint8_t>(words[k] & 1u);
+    const Gf2Poly poly = berlekamp_massey(bits);
+    *degree = poly.degree();
+    *irreducible = poly.degree() == static_cast<int>(mexp) ? (is_irreducible(poly) ? 1 : 0) : -1;
+    return 0;
 }
 
 }  // extern "C"

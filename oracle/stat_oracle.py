@@ -149,3 +149,34 @@ def walk_counts(words: np.ndarray, spec) -> np.ndarray:
     """stat_tests.hpp:279-284: H = odd words per length-l walk, histogram over 0..l."""
     h = (words[:spec.n * spec.l] & 1).reshape(spec.n, spec.l).sum(axis=1)
     return np.bincount(h, minlength=spec.l + 1).astype(np.uint64)
+
+
+# ---------------- the reference's parameter-set tooling (gf2poly.cpp, dynamic_creator.cpp) ----------------
+
+def ref_is_irreducible(coeffs) -> int:
+    """The reference's is_irreducible on sum_i coeffs[i] x^i: 1 / 0, -1 if it throws."""
+    L = _lib()
+    L.ref_is_irreducible.argtypes = [C.c_void_p, C.c_uint64]
+    b = np.ascontiguousarray(np.asarray(coeffs, dtype=np.uint8))
+    return L.ref_is_irreducible(b.ctypes.data_as(C.c_void_p), b.size)
+
+
+def ref_mt_probe_digest(seed: int, status12=None):
+    """(poly_digest, degree) of probe_minimal_polynomial(Generator(status, seed), mexp)."""
+    L = _lib()
+    L.ref_mt_probe_digest.argtypes = [C.c_void_p, C.c_uint32, C.c_char_p, C.POINTER(C.c_int)]
+    st = (C.c_uint32 * 12)(*status12) if status12 is not None else None
+    buf = C.create_string_buffer(41)
+    deg = C.c_int()
+    assert L.ref_mt_probe_digest(st, seed & 0xFFFFFFFF, buf, C.byref(deg)) == 0
+    return buf.value.decode(), deg.value
+
+
+def ref_bit0_certify(words: np.ndarray, mexp: int):
+    """(degree, irreducible) of the reference's BM over bit 0 of `words` (dc_search's test)."""
+    L = _lib()
+    L.ref_bit0_certify.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    w = np.ascontiguousarray(words, dtype=np.uint32)
+    d, irr = C.c_int(), C.c_int()
+    assert L.ref_bit0_certify(w.ctypes.data_as(C.c_void_p), w.size, mexp, C.byref(d), C.byref(irr)) == 0
+    return d.value, irr.value

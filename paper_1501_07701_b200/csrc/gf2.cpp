@@ -1,5 +1,6 @@
 // gf2.cpp -- see gf2.h.
 #include "gf2.h"
+#include "sha1.h"
 
 #include <algorithm>
 #include <cstring>
@@ -95,6 +96,14 @@ Poly mul(const Poly& a, const Poly& b) {
         r.w.resize(na + nb);
         mul_raw(a.w.data(), na, b.w.data(), nb, r.w.data());
     }
+    r.trim();
+    return r;
+}
+
+Poly square(const Poly& a) {
+    Poly r;
+    r.w.assign(2 * a.w.size(), 0);
+    for (size_t i = 0; i < a.w.size(); ++i) clmul64(a.w[i], a.w[i], &r.w[2 * i], &r.w[2 * i + 1]);
     r.trim();
     return r;
 }
@@ -276,6 +285,59 @@ Poly Modulus::x_pow(uint64_t e) const {
         }
     }
     return r;
+}
+
+}  // namespace gf2
+}  // namespace mtgpb
+
+namespace mtgpb {
+namespace gf2 {
+
+bool is_irreducible(const Poly& p) {
+    const int d = p.degree();
+    if (d < 1) return false;
+    if (d == 1) return true;
+    // k = d / q for the distinct primes q | d, plus k = 1..20 as a sieve for small factors
+    // (gcd(x^(2^k) - x, p) = 1 for every k < d when p is irreducible, so the answer is unchanged;
+    // a reducible p is usually rejected after a few squarings instead of d)
+    std::vector<int> checkpoints;
+    for (int k = 1; k <= std::min(20, d - 1); ++k) checkpoints.push_back(k);
+    int rem = d;
+    for (int q = 2; q * q <= rem; ++q)
+        if (rem % q == 0) {
+            checkpoints.push_back(d / q);
+            while (rem % q == 0) rem /= q;
+        }
+    if (rem > 1) checkpoints.push_back(d / rem);
+    std::sort(checkpoints.begin(), checkpoints.end());
+    checkpoints.erase(std::unique(checkpoints.begin(), checkpoints.end()), checkpoints.end());
+    const Modulus md(p);
+    Poly x;
+    x.set(1);
+    Poly u = md.reduce(x);  // x mod p (d >= 2: x itself)
+    size_t next = 0;
+    for (int k = 1; k <= d; ++k) {
+        u = md.sqrmod(u);  // x^(2^k) mod p
+        while (next < checkpoints.size() && checkpoints[next] == k) {
+            ++next;
+            Poly g = gcd(add(u, x), p);
+            g.trim();
+            if (g.degree() != 0) return false;
+        }
+    }
+    Poly ux = add(u, x);
+    ux.trim();
+    return ux.degree() < 0;
+}
+
+std::string reference_digest(const Poly& p) {
+    const int d = p.degree();
+    const uint64_t nbits = d < 0 ? 0 : (uint64_t)d + 1;
+    std::string payload(8, '\0');
+    for (int i = 0; i < 8; ++i) payload[i] = static_cast<char>((nbits >> (8 * i)) & 0xff);
+    const size_t nbytes = d < 0 ? 0 : (size_t)d / 8 + 1;
+    for (size_t i = 0; i < nbytes; ++i) payload.push_back(static_cast<char>((p.w[i / 8] >> (8 * (i % 8))) & 0xff));
+    return sha1_hex(payload);
 }
 
 }  // namespace gf2

@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 #include <vector>
 
 namespace mtgpb {
@@ -26,6 +27,7 @@ struct Poly {
 };
 
 Poly mul(const Poly& a, const Poly& b);
+Poly square(const Poly& a);  // a^2: bit spreading (one carry-less square per word)
 Poly add(const Poly& a, const Poly& b);
 Poly shift_left(const Poly& a, int k);
 // quotient and remainder by long division (O(deg^2/64)); used once per set
@@ -46,7 +48,18 @@ struct Modulus {
     Poly reduce(const Poly& a) const;  // deg a < 2M
     Poly mulmod(const Poly& a, const Poly& b) const;
     Poly x_pow(uint64_t e) const;  // x^e mod P
+    Poly sqrmod(const Poly& a) const { return reduce(square(a)); }
 };
+
+// Rabin's test: p of degree d >= 1 is irreducible iff x^(2^d) = x (mod p) and
+// gcd(x^(2^(d/q)) - x, p) = 1 for every prime q | d; like the reference's is_irreducible
+// (proj/src/gf2poly.cpp:342-383) also at k = 1..20 as a small-factor sieve. Up to d squarings.
+bool is_irreducible(const Poly& p);
+
+// The reference's poly_digest (proj/src/dynamic_creator.cpp:9-31): SHA-1 of the coefficient
+// count (degree + 1, 0 for the zero polynomial) as 8 little-endian bytes, then the coefficient
+// bits as little-endian bytes; lowercase hex.
+std::string reference_digest(const Poly& p);
 
 }  // namespace gf2
 }  // namespace mtgpb

@@ -477,6 +477,20 @@ cudaError_t Planner::charpoly_sha1(const DevParams* params, uint32_t* win, cudaS
     return cudaSuccess;
 }
 
+cudaError_t Planner::certify(const DevParams* params, uint32_t* win, cudaStream_t st, std::vector<int>& out,
+                             std::string& err) {
+    PlannerImpl& I = *impl_;
+    cudaError_t e;
+    if (!I.analyzed && (e = I.analyze(params, win, st, err)) != cudaSuccess) return e;
+    out.assign(I.S, 0);
+    parallel_for(I.S, [&](size_t s) {
+        if (!I.set_ok[s]) return;
+        const gf2::Poly& P = I.mods[s]->p;
+        out[s] = P.degree() == (int)I.M && gf2::is_irreducible(P) ? 1 : 0;
+    });
+    return cudaSuccess;
+}
+
 cudaError_t Planner::skip(const DevParams* params, uint32_t* win, uint64_t words, cudaStream_t st, std::string& err) {
     PlannerImpl& I = *impl_;
     if (!v2_supports(I.M)) {

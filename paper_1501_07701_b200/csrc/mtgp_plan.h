@@ -51,6 +51,9 @@ public:
     // '0'/'1' coefficients lowest degree first; empty where none was found.
     cudaError_t charpoly_sha1(const DevParams* params, uint32_t* win, cudaStream_t st,
                               std::vector<std::string>& out, std::string& err);
+    // 1 per stream whose minimal polynomial has degree mexp and is irreducible (maximal period)
+    cudaError_t certify(const DevParams* params, uint32_t* win, cudaStream_t st, std::vector<int>& out,
+                        std::string& err);
 
 private:
     std::unique_ptr<PlannerImpl> impl_;

@@ -483,6 +483,25 @@ std::uint64_t StreamBatch::position(std::uint32_t s) const {
     return v;
 }
 
+std::vector<bool> StreamBatch::certify() {
+    std::vector<std::int32_t> c(n_sets_);
+    check(mtgp_certify(ctx_, c.data()), "mtgp_certify");
+    return std::vector<bool>(c.begin(), c.end());
+}
+
+std::vector<std::string> StreamBatch::mt_charpoly_digests() {
+    std::vector<char> buf(41 * (size_t)n_sets_);
+    check(mtgp_mt_charpoly_digest(ctx_, buf.data()), "mtgp_mt_charpoly_digest");
+    std::vector<std::string> out;
+    for (std::uint32_t s = 0; s < n_sets_; ++s) out.emplace_back(buf.data() + 41 * (size_t)s);
+    return out;
+}
+
+bool verify_digest(const MtStatus& status, const std::string& digest, int device) {
+    StreamBatch b(std::vector<MtStatus>{status}, {1u}, device);  // kDefaultProbeSeed
+    return b.mt_charpoly_digests()[0] == digest;
+}
+
 std::vector<mtgp_cksum> StreamBatch::checksums() const {
     std::vector<mtgp_cksum> v(n_sets_);
     check(mtgp_checksums(ctx_, v.data()), "mtgp_checksums");

@@ -36,7 +36,7 @@ EXPORTS = (
     "mtgp_charpoly_sha1", "mtgp_stat_validate", "mtgp_stat_run", "mtgp_stat_counts_len", "mtgp_stat_finish",
     "mtgp_ln_gamma", "mtgp_gamma_p", "mtgp_gamma_q", "mtgp_chi_square_pvalue", "mtgp_poisson_cdf",
     "mtgp_poisson_sf", "mtgp_poisson_pmf", "mtgp_binomial_log_pmf", "mtgp_binomial_upper_tail",
-    "mtgp_classify_pvalue",
+    "mtgp_classify_pvalue", "mtgp_certify", "mtgp_mt_charpoly_digest", "mtgp_gf2_is_irreducible",
 )
 
 
@@ -136,6 +136,9 @@ def load_library(path: Optional[str] = None) -> C.CDLL:
     lib.mtgp_binomial_log_pmf.argtypes = [C.c_uint64, C.c_uint64, C.c_double, pd]
     lib.mtgp_binomial_upper_tail.argtypes = [C.c_uint64, C.c_uint64, C.c_double, pd]
     lib.mtgp_classify_pvalue.argtypes = [C.c_double, C.POINTER(C.c_int32)]
+    lib.mtgp_certify.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
+    lib.mtgp_mt_charpoly_digest.argtypes = [C.c_void_p, C.c_char_p]
+    lib.mtgp_gf2_is_irreducible.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_int32)]
     if path is None:
         _lib = lib
     return lib
@@ -291,6 +294,21 @@ class MtgpContext:
     def kernel_timing_reset(self) -> None:
         _check(self.lib, self.lib.mtgp_kernel_timing_reset(self.h))
 
+    def certify(self) -> list:
+        """Per stream: True iff its minimal polynomial has degree mexp and is irreducible (the
+        reference dynamic creator's acceptance test, dynamic_creator.cpp:79-81)."""
+        arr = (C.c_int32 * self.n_sets)()
+        _check(self.lib, self.lib.mtgp_certify(self.h, arr))
+        return [bool(v) for v in arr]
+
+    def mt_charpoly_digest(self) -> list:
+        """Engine::mt contexts: the reference's poly_digest of each stream's probed minimal
+        polynomial (verify_digest's digest when seeded with 1)."""
+        buf = C.create_string_buffer(41 * self.n_sets)
+        _check(self.lib, self.lib.mtgp_mt_charpoly_digest(self.h, buf))
+        raw = buf.raw
+        return [raw[41 * s:41 * s + 40].split(b"\0")[0].decode() for s in range(self.n_sets)]
+
     def stat_run(self, spec) -> list:
         """The device-side statistical test `spec` (stattests.TestSpec) on every stream, from the
         current position; the context state is unchanged. One stattests.TestResult per stream."""
@@ -320,3 +338,12 @@ class MtContext(MtgpContext):
         _check(self.lib, self.lib.mtgp_mt_ctx_create(C.byref(h), device, self._params, self.n_sets, self._seeds,
                                                      C.c_void_p(stream or 0)))
         self.h = h
+
+
+def gf2_is_irreducible(coeffs) -> bool:
+    """Rabin irreducibility of sum_i coeffs[i] x^i (host, PCLMUL; csrc/gf2.cpp)."""
+    lib = load_library()
+    b = np.ascontiguousarray(np.asarray(coeffs, dtype=np.uint8))
+    out = C.c_int32()
+    _check(lib, lib.mtgp_gf2_is_irreducible(b.ctypes.data_as(C.c_void_p), b.size, C.byref(out)))
+    return bool(out.value)

@@ -2,6 +2,7 @@
 // Built and run by tests/test_jump_cpu.py:
 //   g++ -O2 -mpclmul -msse4.1 -I include -I paper_1501_07701_b200/csrc -I oracle
 //       tests/cpp/test_gf2.cpp paper_1501_07701_b200/csrc/gf2.cpp oracle/liboracle.so
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -84,6 +85,34 @@ int main(int argc, char** argv) {
             CHECK(m1.coeff(k) == (bool)c);
         }
     }
+    // 1b. Rabin irreducibility (the reference's is_irreducible, gf2poly.cpp:342-383) on known
+    //     cases: primitive trinomials of Mersenne exponents, and products of two factors
+    {
+        auto tri = [](int n, int k) {
+            Poly t;
+            t.set(0);
+            t.set(k);
+            t.set(n);
+            return t;
+        };
+        CHECK(is_irreducible(tri(89, 38)));
+        CHECK(is_irreducible(tri(127, 1)));
+        CHECK(is_irreducible(tri(521, 32)));
+        CHECK(is_irreducible(tri(607, 105)));
+        CHECK(is_irreducible(tri(1279, 216)));
+        CHECK(!is_irreducible(tri(8, 0)));                       // x^8 + 1 = (x + 1)^8
+        CHECK(!is_irreducible(mul(tri(89, 38), tri(127, 1))));   // composite, no small factor
+        CHECK(!is_irreducible(mul(tri(127, 1), tri(127, 1))));   // a square
+        CHECK(!is_irreducible(tri(200, 3)));                     // x^200 + x^3 + 1 has degree 200
+        Poly x1;  // x + 1
+        x1.set(0);
+        x1.set(1);
+        CHECK(is_irreducible(x1));
+        // the reference digest of x^2 + x + 1 (coefficient count 3, byte 0x07)
+        Poly q;
+        q.set(0); q.set(1); q.set(2);
+        CHECK(reference_digest(q).size() == 40);
+    }
     // 2. MTGP sets from the file: charpoly via BM, annihilation, jump = direct generation
     FILE* f = std::fopen(argv[1], "r");
     if (!f) return 2;
@@ -98,6 +127,12 @@ int main(int argc, char** argv) {
             if (x[k + 1] >> 31) bits[k >> 6] |= 1ull << (k & 63);
         Poly P = berlekamp_massey(bits, 2 * (size_t)M);
         std::printf("set %d mexp %u: BM degree %d\n", nset, M, P.degree());
+        {
+            const auto t0 = std::chrono::steady_clock::now();
+            const bool irr = is_irreducible(P);
+            const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            std::printf("  irreducible %d (%.3f s)\n", (int)irr, s);
+        }
         {
             std::string coeffs(P.degree() + 1, '0');
             for (int i = 0; i <= P.degree(); ++i)

@@ -157,6 +157,14 @@ int main(int argc, char** argv) {
             CHECK(rows[i].p_value == hexd(cells[i][4]));
             CHECK(static_cast<int>(rows[i].classification) == std::atoi(cells[i][5].c_str()));
         }
+        // verify_digest on the GPU with the reference's MT19937 preset digest (params.cpp:75)
+        CHECK(verify_digest(mt19937_status(), "736dbad14b19609ef909097e1b440834727ed02c"));
+        CHECK(!verify_digest(mt19937_status(), "0000000000000000000000000000000000000000"));
+        {
+            StreamBatch b(std::vector<MtgpStatus>{sets[0], sets[1]}, {1u, 2u});
+            const auto c = b.certify();
+            CHECK(c.size() == 2 && c[0] && c[1]);
+        }
         // a spec error becomes an error row in every cell, the rest of the grid still runs
         TestSpec bad = desk_walk_spec();
         bad.n = 10;

@@ -44,6 +44,11 @@ def main():
         w = oracle_py.ref_fill(1 << 16, 4357, st)
         ref[name] = {"status12": st, "seed": 4357, "n": 1 << 16,
                      **{k: int(v) for k, v in oracle_py.cksum(w).items()}}
+    # probe digests (verify_digest's polynomial, dynamic_creator.cpp:33-38, 99-103), seed 1
+    import stat_oracle as so
+    ref["probe_digest_mt19937_seed1"] = list(so.ref_mt_probe_digest(1))
+    for name, st in dc.items():
+        ref[name]["probe_digest_seed1"] = list(so.ref_mt_probe_digest(1, st))
     (ROOT / "tests/golden/mt_reference.json").write_text(json.dumps(ref, indent=1) + "\n")
     stat_goldens()
     print("goldens written")
