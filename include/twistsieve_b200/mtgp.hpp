@@ -122,6 +122,9 @@ void write_status_file(const std::filesystem::path& path, const std::vector<Stat
 // ---- seeds (proj/src/word_source.cpp:18-27) ----
 std::uint64_t splitmix64(std::uint64_t x);
 std::uint32_t derive_seed(std::uint64_t source, std::uint32_t j);
+/// cuRAND's convention (curandMakeMTGP32KernelState, curand_mtgp32_host.h:482-510): stream i is
+/// seeded with (u32)(seed ^ (seed >> 32)) + i + 1.
+std::vector<std::uint32_t> curand_kernel_state_seeds(std::uint64_t seed, std::uint32_t n);
 
 /// RAII owner of a C-ABI context: many independent streams on one GPU.
 class StreamBatch {

@@ -423,6 +423,13 @@ std::uint64_t splitmix64(std::uint64_t x) {
     return x ^ (x >> 31);
 }
 
+std::vector<std::uint32_t> curand_kernel_state_seeds(std::uint64_t seed, std::uint32_t n) {
+    const auto base = static_cast<std::uint32_t>(seed ^ (seed >> 32));
+    std::vector<std::uint32_t> out(n);
+    for (std::uint32_t i = 0; i < n; ++i) out[i] = base + i + 1;
+    return out;
+}
+
 std::uint32_t derive_seed(std::uint64_t source, std::uint32_t j) {
     return static_cast<std::uint32_t>(splitmix64(source + j));
 }

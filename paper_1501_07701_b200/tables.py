@@ -192,6 +192,15 @@ def synthetic_sets(mexp: int, count: int, first: int = 0) -> List[MtgpParams]:
     return [synthetic_set(mexp, first + i) for i in range(count)]
 
 
+def curand_kernel_state_seeds(seed: int, n: int) -> List[int]:
+    """Per-stream seeds of curandMakeMTGP32KernelState (curand_mtgp32_host.h:482-510): stream i
+    is seeded with (u32)(seed ^ (seed >> 32)) + i + 1, so a context built with these seeds
+    reproduces a cuRAND MTGP32 device-API setup stream for stream."""
+    seed &= 0xFFFFFFFFFFFFFFFF
+    base = (seed ^ (seed >> 32)) & 0xFFFFFFFF
+    return [(base + i + 1) & 0xFFFFFFFF for i in range(n)]
+
+
 def sets_for(mexp: int, count: int, first: int = 0) -> List[MtgpParams]:
     """`count` sets for `mexp`: the certified cuRAND sets first (11213), then synthetic ones."""
     out: List[MtgpParams] = []

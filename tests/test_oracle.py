@@ -142,3 +142,13 @@ def test_derive_seed_matches_reference_formula():
     # splitmix64(0) is the published first output of the splitmix64 sequence
     assert L.oracle_splitmix64(0) == 0xE220A8397B1DCDAF
     assert L.oracle_derive_seed(10, 3) == L.oracle_splitmix64(13) & 0xFFFFFFFF
+
+
+def test_curand_kernel_state_seeds():
+    """curandMakeMTGP32KernelState's per-stream seeds (curand_mtgp32_host.h:482-510)."""
+    from paper_1501_07701_b200 import tables
+    assert tables.curand_kernel_state_seeds(1, 3) == [2, 3, 4]
+    s = 0x1234567890ABCDEF
+    assert (0x90ABCDEF ^ 0x12345678) == 0x82999997  # low word of seed ^ (seed >> 32)
+    assert tables.curand_kernel_state_seeds(s, 2) == [0x82999998, 0x82999999]
+    assert tables.curand_kernel_state_seeds(0xFFFFFFFF, 2) == [0, 1]  # u32 wrap
