@@ -149,6 +149,6 @@ def test_curand_kernel_state_seeds():
     from paper_1501_07701_b200 import tables
     assert tables.curand_kernel_state_seeds(1, 3) == [2, 3, 4]
     s = 0x1234567890ABCDEF
-    assert (0x90ABCDEF ^ 0x12345678) == 0x82999997  # low word of seed ^ (seed >> 32)
-    assert tables.curand_kernel_state_seeds(s, 2) == [0x82999998, 0x82999999]
+    # low word of seed ^ (seed >> 32) = 0x90ABCDEF ^ 0x12345678 = 0x829F9B97
+    assert tables.curand_kernel_state_seeds(s, 2) == [0x829F9B98, 0x829F9B99]
     assert tables.curand_kernel_state_seeds(0xFFFFFFFF, 2) == [0, 1]  # u32 wrap
