@@ -318,6 +318,17 @@ def main():
         t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+        # clocks of the whole job: slowest rank's median / minimum SM clock, union of reasons
+        names = [n for n, _ in ClockSampler.REASONS]
+        lo = torch.tensor([clk.get("sm_mhz") or 0.0, clk.get("sm_mhz_min") or clk.get("sm_mhz") or 0.0],
+                          device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+        bits = torch.tensor([float(n in clk.get("reasons", [])) for n in names], device=f"cuda:{local}",
+                            dtype=torch.float64)
+        dist.all_reduce(bits, op=dist.ReduceOp.MAX)
+        clk = dict(clk, sm_mhz=float(lo[0].item()), sm_mhz_min=float(lo[1].item()),
+                   reasons=[n for n, b in zip(names, bits.tolist()) if b > 0], ranks=world,
+                   note="min over ranks of each rank's median / min SM clock; union of reasons")
     # per-stream checksum gather (NCCL all_gather; the only inter-GPU traffic)
     allck = shard.gather_checksums(ctx.checksums(), device=f"cuda:{local}")
     gathered_streams = len(allck)
@@ -349,9 +360,10 @@ def main():
             cpu = {"value": None, "error": str(e)[:200]}
 
     e2e = None
-    if rank == 0 and not args.no_e2e:
+    if not args.no_e2e:
         # public API, HOST buffers: mtgp_generate(out_is_device=0) into pinned memory; the timed
-        # region contains generation plus the device->host copy of every word
+        # region contains generation plus the device->host copy of every word. Every rank runs it
+        # at once (each GPU has its own host link); whole-job samples over the slowest rank's time.
         Le = 1 << 20
         host = torch.empty((S, Le), dtype=torch.int32, pin_memory=True)
         hv = host.numpy().view(np.uint32)
@@ -359,15 +371,21 @@ def main():
         ectx.set_option(mtgp.OPT_HOST_CHUNK, 1 << 18)
         ectx.generate_host(kind, Le, out=hv)
         reps = 5
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(reps):
             ectx.generate_host(kind, Le, out=hv)
-        t1 = time.perf_counter()
+        el = time.perf_counter() - t0
         ectx.close()
-        e2e = {"value": round(S * Le * reps / (t1 - t0) / 1e9, 4), "unit": "Gsamples/s",
-               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": S * Le * 4,
+        if world > 1:
+            tt = torch.tensor([el], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            el = float(tt.item())
+        e2e = {"value": round(world * S * Le * reps / el / 1e9, 4), "unit": "Gsamples/s",
+               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": world * S * Le * 4,
                "how": f"mtgp_generate(out_is_device=0) of {Le} words x {S} streams into pinned host memory, "
-                      f"{reps} calls, wall clock"}
+                      f"{reps} calls on each of {world} GPU(s) at once, max wall clock over ranks"}
 
     if rank == 0:
         line = {
@@ -382,13 +400,15 @@ def main():
                        "checksums_fused": not args.no_checksum,
                        "checksums_gathered_streams": gathered_streams,
                        "l2": "output 4*S*L/calls bytes per call >> 126 MB L2; no flush needed",
-                       "parameter_sets": "cuRAND MTGP32-11213 (certified)" if (mexp == 11213 and rank == 0 and S <= 200)
-                       else "synthetic (uncertified period)"},
+                       "parameter_sets": ("synthetic (uncertified period)" if mexp != 11213 or S > 200
+                                          else "cuRAND MTGP32-11213 (certified)" if world == 1
+                                          else "rank 0: cuRAND MTGP32-11213 (certified); ranks 1..N-1: synthetic "
+                                               "MTGP32-11213 (uncertified period)")},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(achieved / hbm, 4), "traffic": traffic_per_launch(bytes_per_launch),
                          "traffic_source": "profiles/gen_traffic.json (ncu dram__bytes_read+write per algorithmic byte)",
                          "peak_source": hbm_src,
-                         "kernel": f"gen{kver if kver == 3 else ''}_kernel (v{kver})", "launches_timed": gen_n,
+                         "kernel": f"gen{kver if kver in (3, 4) else ''}_kernel (v{kver})", "launches_timed": gen_n,
                          "avg_launch_ms": round(gen_avg_ms, 4),
                          "algorithmic_bytes_per_launch": bytes_per_launch,
                          "step_write_GBps": round(step_gbs, 1),
