@@ -252,25 +252,7 @@ int mtgp_mt_ctx_create(mtgp_ctx** out, int device, const mtgp_mt_params* sets, u
 }
 
 int mtgp_ctx_destroy(mtgp_ctx* ctx) {
-    if (!ctx) return MTGP_OK;
-    cudaSetDevice(ctx->device);
-    cudaStreamSynchronize(ctx->stream);
-    cudaStreamSynchronize(ctx->copy_stream);
-    ctx->planner.reset();
-    cudaFree(ctx->d_params);
-    cudaFree(ctx->d_mt);
-    cudaFree(ctx->d_win);
-    cudaFree(ctx->d_ck);
-    cudaFree(ctx->d_stage);
-    cudaFree(ctx->d_scratch[0]);
-    cudaFree(ctx->d_scratch[1]);
-    for (int i = 0; i < 2; ++i) {
-        cudaEventDestroy(ctx->ev_gen[i]);
-        cudaEventDestroy(ctx->ev_copy[i]);
-    }
-    cudaStreamDestroy(ctx->copy_stream);
-    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
-    delete ctx;
+    delete ctx;  // ~mtgp_ctx releases everything (also on ctx_create's error paths)
     return MTGP_OK;
 }
 

@@ -61,6 +61,26 @@ struct mtgp_ctx {
     // v2 planner / jump-ahead state
     std::unique_ptr<Planner> planner;
     uint32_t last_pieces = 0, last_warps = 0, last_kernel = 0;
+
+    mtgp_ctx() = default;
+    mtgp_ctx(const mtgp_ctx&) = delete;
+    mtgp_ctx& operator=(const mtgp_ctx&) = delete;
+    // Releases whatever was created, so a partially built context (a failed mtgp_ctx_create)
+    // does not leak. cudaFree / cudaEventDestroy / cudaStreamDestroy accept null handles.
+    ~mtgp_ctx() {
+        cudaSetDevice(device);
+        if (stream) cudaStreamSynchronize(stream);
+        if (copy_stream) cudaStreamSynchronize(copy_stream);
+        planner.reset();
+        for (void* p : {(void*)d_params, (void*)d_mt, (void*)d_win, (void*)d_ck, d_stage, d_scratch[0], d_scratch[1]})
+            if (p) cudaFree(p);
+        for (int i = 0; i < 2; ++i) {
+            if (ev_gen[i]) cudaEventDestroy(ev_gen[i]);
+            if (ev_copy[i]) cudaEventDestroy(ev_copy[i]);
+        }
+        if (copy_stream) cudaStreamDestroy(copy_stream);
+        if (own_stream && stream) cudaStreamDestroy(stream);
+    }
 };
 
 namespace mtgpb {
