@@ -1,4 +1,4 @@
-"""Multi-GPU sharding of independent MTGP32 streams.
+"""Multi-GPU sharding of independent MTGP32 streams and of stat-test campaigns.
 
 Streams are independent by parameterization, so the path shards
 with no data-path collective: rank r owns a contiguous range of parameter-set IDs and generates
@@ -43,3 +43,43 @@ def gather_checksums(local: Sequence[Cksum], device=None) -> List[Cksum]:
         for lo, hi, x, w in p.cpu().tolist():
             out.append(((hi << 32) | lo, x, w))
     return out
+
+
+def status_range(n_statuses: int, rank: int, world: int) -> range:
+    """Contiguous, balanced status-index range of `rank` for a campaign over n_statuses
+    (strong scaling: the campaign's cells are fixed, split across ranks)."""
+    base, extra = divmod(n_statuses, world)
+    lo = rank * base + min(rank, extra)
+    return range(lo, lo + base + (1 if rank < extra else 0))
+
+
+def run_grid_distributed(statuses: Sequence, seeds: Sequence[int], specs: Sequence, runner=None, **kw):
+    """The sieve's campaign grid (sieve.cpp:116-183) over every rank's GPU: rank r runs the
+    cells of its status range on its own device (stattests.run_grid), and rank 0 returns all
+    rows in the reference's (status, seed, test) order -- the same report for any world size,
+    as run_grid is for any worker count. Other ranks return []. The row gather is the only
+    collective (all_gather_object: NCCL / gloo). `runner` replaces stattests.run_grid (tests)."""
+    import torch.distributed as dist
+
+    from . import stattests
+    dist_on = dist.is_available() and dist.is_initialized()
+    rank = dist.get_rank() if dist_on else 0
+    world = dist.get_world_size() if dist_on else 1
+    mine = status_range(len(statuses), rank, world)
+    rows = []
+    if runner is None:
+        import os
+        kw.setdefault("device", int(os.environ.get("LOCAL_RANK", "0")))  # each rank its own GPU
+    if len(mine):
+        run = runner or stattests.run_grid
+        ids = kw.pop("status_ids", None) or [str(i) for i in range(len(statuses))]
+        rows = run([statuses[i] for i in mine], seeds, specs, status_ids=[ids[i] for i in mine], **kw)
+        for r in rows:
+            r.status_index += mine.start
+    if world == 1:
+        return rows
+    parts = [None] * world
+    dist.all_gather_object(parts, rows)
+    if rank != 0:
+        return []
+    return [r for part in parts for r in part]

@@ -78,3 +78,55 @@ def test_sets_beyond_the_table_are_synthetic_and_distinct():
     assert len(keys) == 200
     r0 = shard.sets_for_rank(11213, 200, 0)
     assert all(s.certified for s in r0)
+
+
+def _grid_worker(rank, world, port, n_status, q):
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    sys.path.insert(0, str(root))
+    import torch.distributed as dist
+
+    from paper_1501_07701_b200 import shard, stattests
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    seen = []
+
+    def fake_run_grid(statuses, seeds, specs, status_ids=None, **kw):
+        # stands in for the GPU: one row per (status, seed, test), carrying its coordinates
+        seen.extend(statuses)
+        return [stattests.ResultRow(si, wi, status_ids[si], sp.test_id, seed, statistic=float(statuses[si]))
+                for si in range(len(statuses)) for wi, seed in enumerate(seeds) for sp in specs]
+
+    rows = shard.run_grid_distributed(list(range(100, 100 + n_status)), [7, 8], stattests.desk_battery()[:2],
+                                      runner=fake_run_grid)
+    q.put((rank, seen, [(r.status_index, r.seed_index, r.test_id, r.statistic, r.status_id) for r in rows]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_status", [5, 2, 1])
+def test_run_grid_distributed_order_and_coverage(n_status):
+    """Campaign cells split over 2 ranks by status; rank 0 gets every row in run_grid's
+    (status, seed, test) order, whatever the split (including a rank with no statuses)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_grid_worker, args=(r, 2, port, n_status, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in range(2):
+        rank, seen, rows = q.get(timeout=240)
+        got[rank] = (seen, rows)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    statuses = list(range(100, 100 + n_status))
+    assert sorted(got[0][0] + got[1][0]) == statuses and not set(got[0][0]) & set(got[1][0])
+    assert got[1][1] == []
+    want = [(si, wi, t, float(statuses[si]), str(si)) for si in range(n_status) for wi in range(2)
+            for t in ("gap", "hamming_indep")]
+    assert got[0][1] == want
