@@ -275,7 +275,9 @@ typedef struct mtgp_stat_result {
 int mtgp_stat_validate(const mtgp_stat_spec* spec);
 
 /* Runs the test on every stream of ctx, each from the context's current position; results[s]
-   for stream s. The context's state and checksums are left unchanged. */
+   for stream s. The context's state and checksums are left unchanged. The context keeps a
+   scratch arena for the generated chunks (about 2^32 bytes at any stream count, up to 2^26
+   bytes per stream) until it is destroyed. */
 int mtgp_stat_run(mtgp_ctx* ctx, const mtgp_stat_spec* spec, mtgp_stat_result* results);
 
 /* The host half alone: result from a test's integer counts. Layout: gap tcut+1 gap-length
