@@ -126,3 +126,28 @@ def test_mt_ragged_state_restore_skip_checksums():
         o2.fill(sum((1, 226, 227, 228, 624, 1000)) + 999 + 100003)
         assert np.array_equal(z[s], o2.fill(64))
         assert ck[s][2] == total + 64
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mexp", [89, 127, 521, 607, 1279, 2203, 2281, 3217, 19937, 23209])
+def test_mt_every_supported_shape_vs_compiled_reference(mexp):
+    """Engine::mt at every exponent the reference supports (kSupportedMexp, params.hpp:50-51),
+    shapes from shape_for_mexp (params.cpp:56-61), middle offsets m across [1, n-1] (DC draws m in
+    that range, dynamic_creator.cpp:73) -- incl. n - m = 1, a one-word parallel step."""
+    import random
+    rnd = random.Random(mexp)
+    n = (mexp + 31) // 32
+    ms = sorted({1, n - 1, max(1, n // 2), rnd.randint(1, n - 1)})
+    sts = []
+    for j, m in enumerate(ms):
+        sts.append(dict(id=7 + j, mexp=mexp, n=n, m=m, r=32 * n - mexp, a=(rnd.getrandbits(16) << 16) | (7 + j),
+                        temper_b=rnd.getrandbits(32), temper_c=rnd.getrandbits(32), temper_u=11, temper_s=7,
+                        temper_t=15, temper_l=18))
+    seeds = [rnd.getrandbits(32) for _ in sts]
+    L = 3 * n + 1000
+    with mtgp.MtContext(sts, seeds) as ctx:
+        w = ctx.fill_u32(L)
+    for s, st in enumerate(sts):
+        st12 = [st[k] for k in ("id", "mexp", "n", "m", "r", "a", "temper_b", "temper_c", "temper_u", "temper_s",
+                                "temper_t", "temper_l")]
+        assert np.array_equal(w[s], oracle_py.ref_fill(L, seeds[s], st12)), (mexp, st["m"])
