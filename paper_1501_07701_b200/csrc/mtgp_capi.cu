@@ -247,6 +247,8 @@ int mtgp_mt_ctx_create(mtgp_ctx** out, int device, const mtgp_mt_params* sets, u
     CK(cudaMemcpyAsync(ctx->d_win, win.data(), sizeof(uint32_t) * win.size(), cudaMemcpyHostToDevice, ctx->stream), "upload state");
     CK(cudaMemsetAsync(ctx->d_ck, 0, sizeof(DevCksum) * n_sets, ctx->stream), "memset checksums");
     CK(cudaStreamSynchronize(ctx->stream), "sync");
+    // jump-ahead pieces + warp teams when the statuses share one shape (Planner(mt_sets))
+    ctx->planner = std::make_unique<Planner>(ctx->mt_sets, prop.multiProcessorCount);
     *out = ctx.release();
     return MTGP_OK;
 }
@@ -309,7 +311,9 @@ namespace {
 // One device-side generation of L words per stream into device memory `out`.
 int generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
     if (L == 0) return MTGP_OK;
-    if (ctx->engine == 1) {
+    const bool mt_teams = ctx->engine == 1 && ctx->kernel != 1 && kind != MTGP_F64_01 && ctx->planner &&
+                          ctx->planner->v2_supported();
+    if (ctx->engine == 1 && !mt_teams) {
         size_t e0 = 0, e1 = 0;
         if (ctx->timing) ctx->pool.record(ctx->stream, &e0);
         cudaError_t e = launch_mt_v1(kind, ctx->cksum, ctx->d_mt, ctx->d_win, ctx->n_sets, ctx->N, out, L, ctx->d_ck,
@@ -327,7 +331,7 @@ int generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
         return MTGP_OK;
     }
     // doubles (8 B/sample, the reference's next_f64_01) are produced by the stream-per-CTA kernel
-    const bool use_v1 = ctx->kernel == 1 || !ctx->planner->v2_supported() || kind == MTGP_F64_01;
+    const bool use_v1 = !mt_teams && (ctx->kernel == 1 || !ctx->planner->v2_supported() || kind == MTGP_F64_01);
     if (use_v1) {
         size_t e0 = 0, e1 = 0;
         if (ctx->timing) ctx->pool.record(ctx->stream, &e0);
@@ -346,7 +350,7 @@ int generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
         PlanRun run;
         run.kind = kind;
         run.cksum = ctx->cksum;
-        run.params = ctx->d_params;
+        run.params = ctx->engine == 1 ? static_cast<const void*>(ctx->d_mt) : static_cast<const void*>(ctx->d_params);
         run.win = ctx->d_win;
         run.ck = ctx->d_ck;
         run.out = out;
@@ -355,7 +359,7 @@ int generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
         run.max_pieces = ctx->max_pieces;
         run.min_piece_words = ctx->min_piece_words;
         run.timing = ctx->timing ? &ctx->pool : nullptr;
-        run.want_kernel = ctx->kernel;
+        run.want_kernel = ctx->engine == 1 ? 0 : ctx->kernel;
         std::string err;
         cudaError_t e = ctx->planner->run(run, err);
         if (e != cudaSuccess) return fail(e == cudaErrorMemoryAllocation ? MTGP_ENOMEM : MTGP_ECUDA, "v2 generation: %s (%s)", err.c_str(), cudaGetErrorString(e));
@@ -438,9 +442,9 @@ int mtgp_skip(mtgp_ctx* ctx, uint64_t words) {
     if (!ctx) return fail(MTGP_EINVAL, "null context");
     if (words == 0) return MTGP_OK;
     CK(cudaSetDevice(ctx->device), "cudaSetDevice");
-    if (words < 4096 || ctx->engine == 1) {
-        // Short skips (and Engine::mt, which has no jump-ahead yet): generate into a scratch
-        // buffer in chunks; generating is cheaper than a jump for short distances.
+    if (words < 4096 || !ctx->planner || !ctx->planner->v2_supported()) {
+        // Short skips (and shapes without a planner: mixed Engine::mt statuses): generate into a
+        // scratch buffer in chunks; generating is cheaper than a jump for short distances.
         const uint64_t chunk = std::min<uint64_t>(words, 1ull << 20);
         void* scratch = nullptr;
         CK(cudaMalloc(&scratch, (size_t)chunk * ctx->n_sets * 4), "cudaMalloc skip scratch");
@@ -455,7 +459,8 @@ int mtgp_skip(mtgp_ctx* ctx, uint64_t words) {
         return rc;
     }
     std::string err;
-    cudaError_t e = ctx->planner->skip(ctx->d_params, ctx->d_win, words, ctx->stream, err);
+    const void* prm = ctx->engine == 1 ? static_cast<const void*>(ctx->d_mt) : static_cast<const void*>(ctx->d_params);
+    cudaError_t e = ctx->planner->skip(prm, ctx->d_win, words, ctx->stream, err);
     if (e != cudaSuccess) return fail(MTGP_ECUDA, "skip: %s (%s)", err.c_str(), cudaGetErrorString(e));
     if (!err.empty()) return fail(MTGP_EINVAL, "skip: %s", err.c_str());
     for (auto& p : ctx->position) p += words;

@@ -71,6 +71,7 @@ constexpr uint64_t kMaxPieceWords = 1ull << 30;
 
 struct PlannerImpl {
     std::vector<mtgp_params> sets;
+    bool mt = false;  // Engine::mt streams
     int num_sms = 148;
     uint32_t M = 0, N = 0, S = 0;
     bool v2 = false;
@@ -116,7 +117,17 @@ struct PlannerImpl {
     // words the prefix kernel generates per row (x_0 .. ), rows 128-byte aligned
     uint32_t prefix_stride() const { return (t0 + prefix_len() + 31) & ~31u; }
 
-    cudaError_t analyze(const DevParams* params, const uint32_t* win, cudaStream_t st, std::string& err);
+    cudaError_t analyze(const void* params, const uint32_t* win, cudaStream_t st, std::string& err);
+
+    // engine-specific launches: the state-word prefix of rows, and the jump itself
+    cudaError_t prefix(const void* params, const uint32_t* win, const uint32_t* rows, uint32_t n_rows, uint32_t* pre,
+                       uint32_t len, cudaStream_t st) const {
+        return mt ? launch_mt_prefix(static_cast<const DevMtParams*>(params), win, rows, n_rows, N, pre, len, st)
+                  : launch_prefix(static_cast<const DevParams*>(params), win, rows, n_rows, N, pre, len, st);
+    }
+    cudaError_t jump(const JumpArgs& a, uint32_t n_rows, cudaStream_t st) const {
+        return mt ? launch_jump_rt(a, N, st) : launch_jump(M, a, n_rows, st);
+    }
     cudaError_t build_plan(uint64_t L, uint32_t T, uint64_t min_piece, std::string& err);
 };
 
@@ -131,6 +142,17 @@ Planner::Planner(const std::vector<mtgp_params>& sets, int num_sms) : impl_(new 
     for (const auto& p : sets)
         if (p.pos + kStepWords > impl_->N) impl_->v2 = false;  // needs N - pos >= 256
 }
+Planner::Planner(const std::vector<mtgp_mt_params>& sets, int num_sms) : impl_(new PlannerImpl) {
+    impl_->mt = true;
+    impl_->num_sms = num_sms;
+    impl_->S = (uint32_t)sets.size();
+    impl_->M = sets[0].mexp;
+    impl_->N = sets[0].n;
+    impl_->t0 = (impl_->N + 8 + 3) & ~3u;
+    impl_->v2 = true;
+    for (const auto& p : sets)
+        if (p.mexp != impl_->M || p.n != impl_->N || p.n - p.m < 32) impl_->v2 = false;
+}
 Planner::~Planner() = default;
 
 bool Planner::v2_supported() const { return impl_->v2; }
@@ -140,12 +162,12 @@ void Planner::invalidate() {
     impl_->plan_valid = false;
 }
 
-cudaError_t Planner::analyze_now(const DevParams* params, const uint32_t* win, cudaStream_t st, std::string& err) {
+cudaError_t Planner::analyze_now(const void* params, const uint32_t* win, cudaStream_t st, std::string& err) {
     if (!impl_->v2) return cudaSuccess;
     return impl_->analyze(params, win, st, err);
 }
 
-cudaError_t PlannerImpl::analyze(const DevParams* params, const uint32_t* win, cudaStream_t st, std::string& err) {
+cudaError_t PlannerImpl::analyze(const void* params, const uint32_t* win, cudaStream_t st, std::string& err) {
     if (analyzed) return cudaSuccess;
     const uint32_t len = ((t0 + 2 * M + N + 64) + 31) & ~31u;
     std::vector<uint32_t> rows(S);
@@ -155,7 +177,7 @@ cudaError_t PlannerImpl::analyze(const DevParams* params, const uint32_t* win, c
     DevBuf seq;
     if ((e = seq.ensure((size_t)S * len * 4)) != cudaSuccess) return e;
     cudaMemcpyAsync(d_all_rows.p, rows.data(), S * 4, cudaMemcpyHostToDevice, st);
-    if ((e = launch_prefix(params, win, d_all_rows.as<uint32_t>(), S, N, seq.as<uint32_t>(), len, st)) != cudaSuccess) {
+    if ((e = prefix(params, win, d_all_rows.as<uint32_t>(), S, seq.as<uint32_t>(), len, st)) != cudaSuccess) {
         seq.release();
         return e;
     }
@@ -360,9 +382,13 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     }
     // v3 (register-resident ring) serves MTGP32-11213 when every piece starts 16-byte aligned:
     // 16-byte aligned output, L % 4 == 0 (piece offsets are multiples of 4 by construction)
-    const bool reg_ok = r.L % 4 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 15) == 0;
+    const bool reg_ok = !I.mt && r.L % 4 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 15) == 0;
     const bool v3_ok = I.M == 11213 && reg_ok;
     const bool v4_ok = v4_supports(I.M, r.kind) && reg_ok;
+    if (I.mt && r.kind == MTGP_F64_01) {
+        err = "the Engine::mt warp-team kernel has no f64 output";
+        return cudaSuccess;
+    }
     if (r.want_kernel == 3 && !v3_ok) {
         err = "kernel v3 needs mexp 11213, words_per_stream % 4 == 0 and 16-byte aligned output";
         return cudaSuccess;
@@ -376,7 +402,8 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     // v2 for request shapes the register kernels do not take (float kinds, L % 4 != 0, ...)
     const bool use_v3 = v3_ok && (r.want_kernel == 3 || (r.want_kernel == 0 && I.M == 11213));
     const bool use_v4 = !use_v3 && v4_ok && (r.want_kernel == 4 || (r.want_kernel == 0 && I.M != 11213));
-    const int cps = use_v3   ? gen3_ctas_per_sm(r.kind, r.cksum)
+    const int cps = I.mt     ? mt_gen2_ctas_per_sm(I.N, r.kind, r.cksum)
+                    : use_v3 ? gen3_ctas_per_sm(r.kind, r.cksum)
                     : use_v4 ? gen4_ctas_per_sm(I.M, r.kind, r.cksum)
                              : gen_ctas_per_sm(I.M, r.kind, r.cksum);
     if (cps <= 0) {
@@ -408,8 +435,8 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     size_t j0 = 0, j1 = 0, g0 = 0, g1 = 0;
     if (!I.jump_rows.empty()) {
         if (r.timing) r.timing->record(r.stream, &j0);
-        if ((e = launch_prefix(r.params, r.win, I.d_rows.as<uint32_t>(), (uint32_t)I.jump_rows.size(), I.N,
-                               I.d_pre.as<uint32_t>(), I.prefix_stride(), r.stream)) != cudaSuccess)
+        if ((e = I.prefix(r.params, r.win, I.d_rows.as<uint32_t>(), (uint32_t)I.jump_rows.size(),
+                          I.d_pre.as<uint32_t>(), I.prefix_stride(), r.stream)) != cudaSuccess)
             return e;
         JumpArgs ja;
         ja.pre = I.d_pre.as<uint32_t>();
@@ -424,29 +451,46 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         ja.piece_win = I.d_pwin.as<uint32_t>();
         ja.max_jobs_per_row = I.max_jobs_per_row;
         ja.n_jobs = (uint32_t)I.jobs.size();
-        if ((e = launch_jump(I.M, ja, (uint32_t)I.jump_rows.size(), r.stream)) != cudaSuccess) return e;
+        if ((e = I.jump(ja, (uint32_t)I.jump_rows.size(), r.stream)) != cudaSuccess) return e;
         if (r.timing) {
             r.timing->record(r.stream, &j1);
             r.timing->jump.push_back({j0, j1});
         }
         r.launches += 2;
     }
-    GenArgs ga;
-    ga.params = r.params;
-    ga.pieces = I.d_pieces.as<Piece>();
-    ga.teams = I.d_teams.as<TeamWork>();
-    ga.n_teams = (uint32_t)I.teams.size();
-    ga.piece_win = I.d_pwin_ptrs.as<const uint32_t*>();
-    ga.win_out = I.d_win_next.as<uint32_t>();
-    ga.out = r.out;
-    ga.L = r.L;
-    ga.ck = r.ck;
-    if (r.timing) r.timing->record(r.stream, &g0);
-    e = use_v3   ? launch_gen3(r.kind, r.cksum, ga, r.stream)
-        : use_v4 ? launch_gen4(I.M, r.kind, r.cksum, ga, r.stream)
-                 : launch_gen(I.M, r.kind, r.cksum, ga, r.stream);
-    if (e != cudaSuccess) return e;
-    r.version = use_v3 ? 3 : use_v4 ? 4 : 2;
+    if (I.mt) {
+        MtGenArgs ma;
+        ma.params = static_cast<const DevMtParams*>(r.params);
+        ma.pieces = I.d_pieces.as<Piece>();
+        ma.teams = I.d_teams.as<TeamWork>();
+        ma.n_teams = (uint32_t)I.teams.size();
+        ma.piece_win = I.d_pwin_ptrs.as<const uint32_t*>();
+        ma.win_out = I.d_win_next.as<uint32_t>();
+        ma.out = r.out;
+        ma.L = r.L;
+        ma.ck = r.ck;
+        ma.n = I.N;
+        if (r.timing) r.timing->record(r.stream, &g0);
+        if ((e = launch_mt_gen2(r.kind, r.cksum, ma, r.stream)) != cudaSuccess) return e;
+        r.version = 5;
+    } else {
+        GenArgs ga;
+        ga.params = static_cast<const DevParams*>(r.params);
+        ga.pieces = I.d_pieces.as<Piece>();
+        ga.teams = I.d_teams.as<TeamWork>();
+        ga.n_teams = (uint32_t)I.teams.size();
+        ga.piece_win = I.d_pwin_ptrs.as<const uint32_t*>();
+        ga.win_out = I.d_win_next.as<uint32_t>();
+        ga.out = r.out;
+        ga.L = r.L;
+        ga.ck = r.ck;
+        if (r.timing) r.timing->record(r.stream, &g0);
+        e = use_v3   ? launch_gen3(r.kind, r.cksum, ga, r.stream)
+            : use_v4 ? launch_gen4(I.M, r.kind, r.cksum, ga, r.stream)
+                     : launch_gen(I.M, r.kind, r.cksum, ga, r.stream);
+        if (e != cudaSuccess) return e;
+        r.version = use_v3 ? 3 : use_v4 ? 4 : 2;
+    }
     if (r.timing) {
         r.timing->record(r.stream, &g1);
         r.timing->gen.push_back({g0, g1});
@@ -460,7 +504,7 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     return cudaGetLastError();
 }
 
-cudaError_t Planner::charpoly_sha1(const DevParams* params, uint32_t* win, cudaStream_t st,
+cudaError_t Planner::charpoly_sha1(const void* params, uint32_t* win, cudaStream_t st,
                                    std::vector<std::string>& out, std::string& err) {
     PlannerImpl& I = *impl_;
     cudaError_t e;
@@ -477,7 +521,7 @@ cudaError_t Planner::charpoly_sha1(const DevParams* params, uint32_t* win, cudaS
     return cudaSuccess;
 }
 
-cudaError_t Planner::certify(const DevParams* params, uint32_t* win, cudaStream_t st, std::vector<int>& out,
+cudaError_t Planner::certify(const void* params, uint32_t* win, cudaStream_t st, std::vector<int>& out,
                              std::string& err) {
     PlannerImpl& I = *impl_;
     cudaError_t e;
@@ -491,10 +535,10 @@ cudaError_t Planner::certify(const DevParams* params, uint32_t* win, cudaStream_
     return cudaSuccess;
 }
 
-cudaError_t Planner::skip(const DevParams* params, uint32_t* win, uint64_t words, cudaStream_t st, std::string& err) {
+cudaError_t Planner::skip(const void* params, uint32_t* win, uint64_t words, cudaStream_t st, std::string& err) {
     PlannerImpl& I = *impl_;
-    if (!v2_supports(I.M)) {
-        err = "skip (jump-ahead) is implemented for mexp 11213, 23209 and 44497";
+    if (I.mt ? !I.v2 : !v2_supports(I.M)) {
+        err = "skip (jump-ahead) is implemented for mexp 11213, 23209 and 44497 and uniform Engine::mt shapes";
         return cudaSuccess;
     }
     cudaError_t e;
@@ -539,7 +583,7 @@ cudaError_t Planner::skip(const DevParams* params, uint32_t* win, uint64_t words
     cudaMemcpyAsync(rows.p, hrows.data(), I.S * 4, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(joff.p, hoff.data(), (I.S + 1) * 4, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(jobs.p, hjobs.data(), I.S * sizeof(JumpJob), cudaMemcpyHostToDevice, st);
-    e = launch_prefix(params, win, rows.as<uint32_t>(), I.S, I.N, pre.as<uint32_t>(), pre_stride, st);
+    e = I.prefix(params, win, rows.as<uint32_t>(), I.S, pre.as<uint32_t>(), pre_stride, st);
     if (e == cudaSuccess) {
         JumpArgs ja;
         ja.pre = pre.as<uint32_t>();
@@ -553,7 +597,7 @@ cudaError_t Planner::skip(const DevParams* params, uint32_t* win, uint64_t words
         ja.q_words = qw;
         ja.piece_win = out.as<uint32_t>();
         ja.n_jobs = I.S;
-        e = launch_jump(I.M, ja, I.S, st);
+        e = I.jump(ja, I.S, st);
     }
     if (e == cudaSuccess) e = cudaMemcpyAsync(win, out.p, (size_t)I.S * I.N * 4, cudaMemcpyDeviceToDevice, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);

@@ -10,13 +10,14 @@
 
 #include "mtgp_b200.h"
 #include "mtgp_internal.cuh"
+#include "mtgp_mt.cuh"
 
 namespace mtgpb {
 
 struct PlanRun {
     int kind = 0;
     bool cksum = true;
-    const DevParams* params = nullptr;
+    const void* params = nullptr;  // DevParams (MTGP32) or DevMtParams (Engine::mt planner)
     uint32_t* win = nullptr;
     DevCksum* ck = nullptr;
     void* out = nullptr;
@@ -26,7 +27,7 @@ struct PlanRun {
     uint64_t min_piece_words = 1ull << 21;
     EventPool* timing = nullptr;  // non-null: record event pairs around the launches
     int want_kernel = 0;          // 0 auto, 2 force v2, 3 force v3
-    int version = 0;              // kernel that ran
+    int version = 0;              // kernel that ran (2, 3, 4; 5 = Engine::mt warp teams)
     // results
     uint64_t launches = 0;        // kernels launched by this call
     uint32_t pieces = 0, warps_per_piece = 0;
@@ -37,22 +38,25 @@ struct PlannerImpl;
 class Planner {
 public:
     Planner(const std::vector<mtgp_params>& sets, int num_sms);
+    // Engine::mt streams (the reference's recurrence): same pieces and jumps, warp-team MT kernel.
+    // Supported when every status has the same mexp and n and n - m >= 32.
+    Planner(const std::vector<mtgp_mt_params>& sets, int num_sms);
     ~Planner();
     bool v2_supported() const;
     // forget per-stream algebra and cached plans (after a state restore)
     void invalidate();
     // run the per-stream annihilator analysis now, at the current window (no-op if done). An
     // analysis made at window w stays valid for w and every later window of the same streams.
-    cudaError_t analyze_now(const DevParams* params, const uint32_t* win, cudaStream_t st, std::string& err);
+    cudaError_t analyze_now(const void* params, const uint32_t* win, cudaStream_t st, std::string& err);
     cudaError_t run(PlanRun& r, std::string& err);
-    cudaError_t skip(const DevParams* params, uint32_t* win, uint64_t words, cudaStream_t st,
+    cudaError_t skip(const void* params, uint32_t* win, uint64_t words, cudaStream_t st,
                      std::string& err);
     // SHA-1 of each stream's minimal (for certified sets: characteristic) polynomial, printed as
     // '0'/'1' coefficients lowest degree first; empty where none was found.
-    cudaError_t charpoly_sha1(const DevParams* params, uint32_t* win, cudaStream_t st,
+    cudaError_t charpoly_sha1(const void* params, uint32_t* win, cudaStream_t st,
                               std::vector<std::string>& out, std::string& err);
     // 1 per stream whose minimal polynomial has degree mexp and is irreducible (maximal period)
-    cudaError_t certify(const DevParams* params, uint32_t* win, cudaStream_t st, std::vector<int>& out,
+    cudaError_t certify(const void* params, uint32_t* win, cudaStream_t st, std::vector<int>& out,
                         std::string& err);
 
 private:

@@ -497,9 +497,11 @@ struct StateGuard {
         const size_t bytes = (size_t)ctx->n_sets * ctx->N * 4;
         win = scratch(ctx, 0, bytes);
         check(cudaMemcpyAsync(win, ctx->d_win, bytes, cudaMemcpyDeviceToDevice, ctx->stream), "state copy");
-        if (ctx->engine == 0 && ctx->planner) {
+        if (ctx->planner && ctx->planner->v2_supported()) {
             std::string err;
-            check(ctx->planner->analyze_now(ctx->d_params, ctx->d_win, ctx->stream, err), "annihilator analysis");
+            const void* prm =
+                ctx->engine == 1 ? static_cast<const void*>(ctx->d_mt) : static_cast<const void*>(ctx->d_params);
+            check(ctx->planner->analyze_now(prm, ctx->d_win, ctx->stream, err), "annihilator analysis");
         }
         ctx->cksum = false;
     }

@@ -541,6 +541,64 @@ __global__ void __launch_bounds__(kJumpFlatWarps * 32) jump_flat_kernel(JumpArgs
     }
 }
 
+// Same kernel with the window length N a runtime argument (Engine::mt: n per status shape).
+__global__ void __launch_bounds__(kJumpFlatWarps * 32) jump_flat_rt_kernel(JumpArgs a, uint32_t N) {
+    constexpr int J = kJumpJ;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // one warp per (job, pass): a pass is 32*J consecutive outputs of the job's window, so a
+    // 44497 window (4 passes) runs on 4 warps instead of 4 sequential passes of one warp
+    const uint32_t kPasses = (N + 32 * J - 1) / (32 * J);
+    const uint32_t unit = blockIdx.x * kJumpFlatWarps + warp;
+    const uint32_t job = unit / kPasses;
+    if (job >= a.n_jobs) return;
+    const JumpJob jb = a.jobs[job];
+    const uint4* x4 = reinterpret_cast<const uint4*>(a.pre + (size_t)jb.row * a.pre_stride + a.pre_off);
+    const uint32_t* q = a.q + (size_t)jb.q * a.q_words;
+    uint32_t* dst = a.piece_win + (size_t)jb.piece * N;
+    {
+        const uint32_t j0 = (unit % kPasses) * 32 * J;
+        const uint32_t jl = j0 + J * lane;  // multiple of 4
+        uint32_t acc[J];
+#pragma unroll
+        for (int k = 0; k < J; ++k) acc[k] = 0;
+        for (uint32_t iw0 = 0; iw0 < a.q_words; iw0 += 32) {
+            const uint32_t qmine = iw0 + lane < a.q_words ? __ldg(q + iw0 + lane) : 0u;
+            const uint32_t nw = min(32u, a.q_words - iw0);
+            for (uint32_t k32 = 0; k32 < nw; ++k32) {
+                const uint32_t qw = __shfl_sync(FULL, qmine, k32);
+                if (qw == 0) continue;
+                const uint32_t base4 = ((iw0 + k32) * 32 + jl) >> 2;
+                uint32_t w[J + 32];
+#pragma unroll
+                for (int v = 0; v < (J + 32) / 4; ++v) {
+                    const uint4 g = __ldg(x4 + base4 + v);
+                    w[4 * v] = g.x;
+                    w[4 * v + 1] = g.y;
+                    w[4 * v + 2] = g.z;
+                    w[4 * v + 3] = g.w;
+                }
+#pragma unroll
+                for (int b = 0; b < 32; b += 2) {
+                    const uint32_t pat = (qw >> b) & 3u;
+                    if (pat == 1) {
+#pragma unroll
+                        for (int k = 0; k < J; ++k) acc[k] ^= w[b + k];
+                    } else if (pat == 2) {
+#pragma unroll
+                        for (int k = 0; k < J; ++k) acc[k] ^= w[b + 1 + k];
+                    } else if (pat == 3) {
+#pragma unroll
+                        for (int k = 0; k < J; ++k) acc[k] ^= w[b + k] ^ w[b + 1 + k];
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < J; ++k)
+            if (jl + k < N) dst[jl + k] = acc[k];
+    }
+}
+
 #ifndef MTGP_JUMP_FLAT
 #define MTGP_JUMP_FLAT 1
 #endif
@@ -559,6 +617,14 @@ static cudaError_t launch_jump_t(const JumpArgs& a, uint32_t n_rows, cudaStream_
     if (e != cudaSuccess) return e;
     const dim3 grid(n_rows, (a.max_jobs_per_row + kJumpWarps - 1) / kJumpWarps);
     jump_kernel<MEXP><<<grid, kJumpWarps * 32, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_jump_rt(const JumpArgs& a, uint32_t N, cudaStream_t st) {
+    if (a.n_jobs == 0) return cudaSuccess;
+    const uint32_t passes = (N + 32 * kJumpJ - 1) / (32 * kJumpJ);
+    const uint32_t units = a.n_jobs * passes;
+    jump_flat_rt_kernel<<<(units + kJumpFlatWarps - 1) / kJumpFlatWarps, kJumpFlatWarps * 32, 0, st>>>(a, N);
     return cudaGetLastError();
 }
 

@@ -49,6 +49,8 @@ bool v2_supports(uint32_t mexp);
 cudaError_t launch_prefix(const DevParams* params, const uint32_t* win, const uint32_t* sets, uint32_t n_rows,
                           uint32_t N, uint32_t* pre, uint32_t len, cudaStream_t st);
 cudaError_t launch_jump(uint32_t mexp, const JumpArgs& a, uint32_t n_jump_sets, cudaStream_t st);
+// the same jump with a runtime window length N (Engine::mt)
+cudaError_t launch_jump_rt(const JumpArgs& a, uint32_t N, cudaStream_t st);
 cudaError_t launch_gen(uint32_t mexp, int kind, bool cksum, const GenArgs& a, cudaStream_t st);
 int gen_ctas_per_sm(uint32_t mexp, int kind, bool cksum);
 // v3: register-resident ring, MTGP32-11213 only (mtgp_v3.cu)

@@ -151,3 +151,72 @@ def test_mt_every_supported_shape_vs_compiled_reference(mexp):
         st12 = [st[k] for k in ("id", "mexp", "n", "m", "r", "a", "temper_b", "temper_c", "temper_u", "temper_s",
                                 "temper_t", "temper_l")]
         assert np.array_equal(w[s], oracle_py.ref_fill(L, seeds[s], st12)), (mexp, st["m"])
+
+
+def _rand_status(mexp, m, seed):
+    import random
+    rnd = random.Random(seed)
+    n = (mexp + 31) // 32
+    return dict(id=9, mexp=mexp, n=n, m=m, r=32 * n - mexp, a=(rnd.getrandbits(16) << 16) | 9,
+                temper_b=rnd.getrandbits(32), temper_c=rnd.getrandbits(32), temper_u=11, temper_s=7, temper_t=15,
+                temper_l=18)
+
+
+def _st12(st):
+    return [st[k] for k in ("id", "mexp", "n", "m", "r", "a", "temper_b", "temper_c", "temper_u", "temper_s",
+                            "temper_t", "temper_l")]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("which", ["mt19937", "m23209", "dc3217"])
+def test_mt_warp_teams_with_jumps_vs_reference(mt_golden, which):
+    """Engine::mt through the jump-ahead planner (warp teams, kernel version 5), many pieces per
+    stream, bit-exact against the reference compiled from its sources; the next call continues."""
+    if which == "mt19937":
+        sts = [mtgp.mt19937_status()] * 3
+    elif which == "m23209":
+        sts = [_rand_status(23209, 300, 1), _rand_status(23209, 300, 2), _rand_status(23209, 300, 3)]
+    else:
+        sts = [_dc(mt_golden, "dc3217_id7")] * 3
+    seeds = [5489, 1, 0xC0FFEE]
+    L = (1 << 17) + 36
+    with mtgp.MtContext(sts, seeds) as ctx:
+        ctx.set_option(mtgp.OPT_MIN_PIECE_WORDS, 1 << 12)
+        a = ctx.fill_u32(L)
+        pieces, _, kv = ctx.last_plan()
+        b = ctx.fill_u32(5000)
+        ck = ctx.checksums()
+    assert kv == 5 and pieces > 3
+    for s in range(3):
+        ref = oracle_py.ref_fill(L + 5000, seeds[s], _st12(sts[s]))
+        assert np.array_equal(a[s], ref[:L]) and np.array_equal(b[s], ref[L:])
+        c = oracle_py.cksum(ref)
+        assert ck[s] == (c["sum64"], c["xor32"], L + 5000)
+
+
+@pytest.mark.gpu
+def test_mt_warp_teams_float_kinds_and_jump_skip():
+    st = mtgp.mt19937_status()
+    with mtgp.MtContext([st, st], [11, 12]) as ctx:
+        f = ctx.generate_host(mtgp.F32_01OC, 40000)
+        ctx.skip(1_000_003)  # jump-ahead for Engine::mt
+        u = ctx.fill_u32(3000)
+    for s in range(2):
+        o = oracle_py.MtOracle(None, 11 + s)
+        w = o.fill(40000)
+        v = ((w >> 9) | 0x3F800000).astype(np.uint32)
+        assert np.array_equal(f[s], (np.float32(2.0) - v.view(np.float32)).view(np.uint32))
+        o.fill(1_000_003)
+        assert np.array_equal(u[s], o.fill(3000))
+
+
+@pytest.mark.gpu
+def test_mt_shapes_without_teams_fall_back(mt_golden):
+    """n - m < 32 (dc521: 10) and mixed shapes keep the CTA-per-stream kernel, still bit-exact."""
+    sts = [_dc(mt_golden, "dc521_id7"), mtgp.mt19937_status()]
+    with mtgp.MtContext(sts, [4357, 5489]) as ctx:
+        w = ctx.fill_u32(70000)
+        _, _, kv = ctx.last_plan()
+    assert kv == 1
+    assert np.array_equal(w[0], oracle_py.ref_fill(70000, 4357, mt_golden["dc521_id7"]["status12"]))
+    assert np.array_equal(w[1], oracle_py.ref_fill(70000, 5489))
