@@ -195,12 +195,16 @@ int mtgp_mt_validate_params(const mtgp_mt_params* p);
  * Context of n_sets Engine::mt streams (= n_sets make_word_source(status, seed) calls,
  * proj/src/word_source.cpp:5-16). Seeds expand as Generator::Generator (generator.cpp:37-52).
  * Supports mtgp_generate (all kinds; u32 = next_u32 order), state save/restore (window of n
- * words, stride = max n), checksums, positions and mtgp_skip (by generation).
+ * words, stride = max n), checksums, positions, mtgp_skip, mtgp_certify,
+ * mtgp_mt_charpoly_digest and mtgp_stat_run. When every status has the same mexp and n and
+ * n - m >= 32, generation and long skips use the jump-ahead planner with warp teams (kernel
+ * version 5 in mtgp_last_plan); otherwise (and for MTGP_F64_01) one CTA per stream.
  */
 int mtgp_mt_ctx_create(mtgp_ctx** out, int device, const mtgp_mt_params* sets, uint32_t n_sets,
                        const uint32_t* seeds, void* stream);
 
-/* Launch plan of the last generation call: pieces (jump-ahead segments) and warps per piece. */
+/* Launch plan of the last generation call: pieces (jump-ahead segments), warps per piece and the
+   kernel (1 CTA per stream, 2 shared-memory ring, 3 / 4 register ring, 5 Engine::mt warp teams). */
 int mtgp_last_plan(const mtgp_ctx* ctx, uint32_t* pieces, uint32_t* warps_per_piece,
                    uint32_t* kernel_version);
 
