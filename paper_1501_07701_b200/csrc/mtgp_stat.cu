@@ -169,6 +169,52 @@ __global__ void __launch_bounds__(kThreads) hamming_kernel(const uint32_t* __res
         atomicAdd(table + (size_t)st * 4 + threadIdx.x, (unsigned long long)cat[threadIdx.x]);
 }
 
+// Long blocks (>= 32 letters): one warp per block, no shared-memory scan. Lanes stride the
+// block's letters (coalesced loads straight from the chunk), the partial first / last letters
+// are masked, popcounts are warp-reduced; the two blocks of a pair run back to back on the
+// same warp.
+__global__ void __launch_bounds__(kThreads) hamming_warp_kernel(const uint32_t* __restrict__ w, uint64_t C, uint32_t r,
+                                                                uint32_t sb, uint32_t L, uint64_t pairs_chunk,
+                                                                uint64_t pair0, uint64_t npairs,
+                                                                unsigned long long* __restrict__ table) {
+    __shared__ uint32_t cat[4];
+    const uint32_t st = blockIdx.y;
+    const uint32_t* src = w + (size_t)st * C;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    if (threadIdx.x < 4) cat[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t half = L / 2;
+    const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
+    for (uint64_t pp = (uint64_t)blockIdx.x * kWarps + warp; pp < pairs_chunk && pair0 + pp < npairs; pp += nwarps) {
+        uint32_t sign[2];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const uint64_t B = (2 * pp + b) * (uint64_t)L, E = B + L;  // chunk-local bit range
+            const uint32_t jf = (uint32_t)(B / sb), jl = (uint32_t)((E - 1) / sb);  // letters (< C)
+            const uint32_t of = (uint32_t)(B - (uint64_t)jf * sb), eo = (uint32_t)(E - (uint64_t)jl * sb);
+            // interior letters whole: popc of the letter = popc of the word under the letter mask
+            const uint32_t lmask = ((1u << sb) - 1u) << (32u - r - sb);
+            uint32_t cnt = 0;
+            for (uint32_t j = jf + 1 + lane; j < jl; j += 32) cnt += __popc(__ldg(src + j) & lmask);
+            if (lane == 0) {  // the partial first / last letters
+                const uint32_t vf = letter_of(__ldg(src + jf), r, sb);
+                if (jf == jl) {
+                    cnt += __popc((vf >> (sb - eo)) & low_mask(eo - of));
+                } else {
+                    cnt += __popc(vf & low_mask(sb - of));  // skips the `of` bits the previous block took
+                    cnt += __popc(letter_of(__ldg(src + jl), r, sb) >> (sb - eo));  // top eo bits
+                }
+            }
+            for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(kFull, cnt, d);
+            sign[b] = cnt > half ? 1u : 0u;
+        }
+        if (lane == 0) atomicAdd(&cat[sign[0] * 2 + sign[1]], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 4 && cat[threadIdx.x])
+        atomicAdd(table + (size_t)st * 4 + threadIdx.x, (unsigned long long)cat[threadIdx.x]);
+}
+
 // ---------------------------------------------------------------------------------------------
 // Overlapping-pairs collisions (stat_tests.hpp:214-248): cell i = letter(w_i) << s | letter(w_i+1),
 // i < n; a collision is a visit to an occupied cell. The count n - |distinct cells| does not
@@ -606,11 +652,20 @@ void run_hamming(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res)
     uint32_t* const wbuf = ar.commit(ctx, (size_t)S * C * 4);
     check(cudaMemsetAsync(table.p, 0, (size_t)S * 4 * 8, ctx->stream), "memset");
     check(cudaFuncSetAttribute(hamming_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attribute");
+    const bool long_blocks = sp.L >= 32u * sp.s;  // >= 32 letters per block: warp per block
+    const uint64_t pairs_chunk = (uint64_t)tpc * ppt;
     for (uint64_t c = 0; c < chunks; ++c) {
         generate_chunk(ctx, wbuf, C);
-        hamming_kernel<<<dim3(tpc, S), kThreads, smem, ctx->stream>>>(wbuf, C, sp.r, sp.s, sp.L, ppt,
-                                                                      tile_words, c * tpc * ppt, npairs,
-                                                                      table.as<unsigned long long>());
+        if (long_blocks) {
+            const uint32_t gx = (uint32_t)std::min<uint64_t>(ceil_div(pairs_chunk, kWarps), 1024);
+            hamming_warp_kernel<<<dim3(gx, S), kThreads, 0, ctx->stream>>>(wbuf, C, sp.r, sp.s, sp.L, pairs_chunk,
+                                                                           c * pairs_chunk, npairs,
+                                                                           table.as<unsigned long long>());
+        } else {
+            hamming_kernel<<<dim3(tpc, S), kThreads, smem, ctx->stream>>>(wbuf, C, sp.r, sp.s, sp.L, ppt,
+                                                                          tile_words, c * tpc * ppt, npairs,
+                                                                          table.as<unsigned long long>());
+        }
         launched(ctx, "hamming kernel");
     }
     const auto h = fetch(ctx, table, (size_t)S * 4);
