@@ -211,6 +211,73 @@ __device__ __forceinline__ void mt_piece(const DevMtParams& p, uint32_t* ring, u
     }
 }
 
+// Two consecutive words per lane (64-word strips, D = 64 K2): the pair shares q[1] and the
+// address arithmetic, reads (q0, q1) as one LDS.64, writes the pair to the ring as STS.64 when n
+// is even (EVEN_N) and to HBM as one STG.64. Needs even piece lengths and 8-byte aligned output
+// (L even: the planner cuts pieces at multiples of 4).
+template <int KIND, bool CK, int K2, bool EVEN_N>
+__device__ __forceinline__ void mt_piece2(const DevMtParams& p, uint32_t* ring, uint32_t ring_mask, uint32_t n,
+                                          uint32_t lane, uint32_t* optr, uint32_t len, unsigned long long& sum,
+                                          uint32_t& xr) {
+    const uint32_t m = p.m, R = ring_mask + 1;
+    const uint32_t upper = p.r ? (0xFFFFFFFFu << p.r) : 0xFFFFFFFFu, lower = ~upper;
+    auto temper = [&](uint32_t v) {
+        v ^= v >> p.u;
+        v ^= (v << p.s) & p.b;
+        v ^= (v << p.t) & p.c;
+        v ^= v >> p.l;
+        if (KIND != MTGP_U32) {
+            v = (v >> 9) | 0x3F800000u;
+            if (KIND == MTGP_F32_01OC) v = __float_as_uint(2.0f - __uint_as_float(v));
+        }
+        return v;
+    };
+    auto pair = [&](uint32_t i, bool store) {  // words i, i + 1 (i even)
+        const uint32_t* q = ring + (i & ring_mask);
+        const uint2 q01 = *reinterpret_cast<const uint2*>(q);
+        const uint32_t q2 = q[2], qm0 = q[m], qm1 = q[m + 1];
+        const uint32_t y0 = (q01.x & upper) | (q01.y & lower);
+        const uint32_t y1 = (q01.y & upper) | (q2 & lower);
+        const uint32_t x0 = qm0 ^ (y0 >> 1) ^ ((y0 & 1u) ? p.a : 0u);
+        const uint32_t x1 = qm1 ^ (y1 >> 1) ^ ((y1 & 1u) ? p.a : 0u);
+        if (EVEN_N) {
+            const uint32_t w = (i + n) & ring_mask;  // even: the pair does not wrap
+            *reinterpret_cast<uint2*>(ring + w) = make_uint2(x0, x1);
+            *reinterpret_cast<uint2*>(ring + w + R) = make_uint2(x0, x1);
+        } else {
+            const uint32_t w0 = (i + n) & ring_mask, w1 = (i + n + 1) & ring_mask;
+            ring[w0] = x0;
+            ring[w0 + R] = x0;
+            ring[w1] = x1;
+            ring[w1 + R] = x1;
+        }
+        if (store) {
+            const uint32_t v0 = temper(x0), v1 = temper(x1);
+            __stcs(reinterpret_cast<uint2*>(optr + i), make_uint2(v0, v1));
+            if (CK) {
+                sum += v0;
+                sum += v1;
+                xr ^= v0 ^ v1;
+            }
+        }
+    };
+    constexpr uint32_t D = 64 * K2;
+    uint32_t base = 0;
+    for (; base + D <= len; base += D) {
+#pragma unroll
+        for (int k = 0; k < K2; ++k) pair(base + 64 * k + 2 * lane, true);
+        __syncwarp();
+    }
+    if (base < len) {
+#pragma unroll
+        for (int k = 0; k < K2; ++k) {
+            const uint32_t i = base + 64 * k + 2 * lane;
+            pair(i, i < len);  // len is even, so i < len covers both words
+        }
+        __syncwarp();
+    }
+}
+
 template <int KIND, bool CK>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) mt_gen2_kernel(MtGenArgs a, uint32_t ring_mask) {
     extern __shared__ uint32_t smem[];
@@ -231,7 +298,20 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) mt_gen2_kernel(MtGenArgs a,
         const uint32_t len = (uint32_t)pc.len;
         unsigned long long sum = 0;
         uint32_t xr = 0;
-        switch (min(8u, (n - p.m) >> 5)) {  // K = D / 32
+        const uint32_t k2 = min(4u, (n - p.m) >> 6);  // 64-word strips for the pair path
+        if (a.pairs && k2 > 0) {
+            const bool even = (n & 1u) == 0;
+            switch (k2 * 2 + (even ? 1 : 0)) {
+                case 2: mt_piece2<KIND, CK, 1, false>(p, ring, ring_mask, n, lane, optr, len, sum, xr); break;
+                case 3: mt_piece2<KIND, CK, 1, true>(p, ring, ring_mask, n, lane, optr, len, sum, xr); break;
+                case 4: mt_piece2<KIND, CK, 2, false>(p, ring, ring_mask, n, lane, optr, len, sum, xr); break;
+                case 5: mt_piece2<KIND, CK, 2, true>(p, ring, ring_mask, n, lane, optr, len, sum, xr); break;
+                case 6: mt_piece2<KIND, CK, 3, false>(p, ring, ring_mask, n, lane, optr, len, sum, xr); break;
+                case 7: mt_piece2<KIND, CK, 3, true>(p, ring, ring_mask, n, lane, optr, len, sum, xr); break;
+                case 8: mt_piece2<KIND, CK, 4, false>(p, ring, ring_mask, n, lane, optr, len, sum, xr); break;
+                default: mt_piece2<KIND, CK, 4, true>(p, ring, ring_mask, n, lane, optr, len, sum, xr); break;
+            }
+        } else switch (min(8u, (n - p.m) >> 5)) {  // K = D / 32
             case 1: mt_piece<KIND, CK, 1>(p, ring, ring_mask, n, lane, optr, len, sum, xr); break;
             case 2: mt_piece<KIND, CK, 2>(p, ring, ring_mask, n, lane, optr, len, sum, xr); break;
             case 3: mt_piece<KIND, CK, 3>(p, ring, ring_mask, n, lane, optr, len, sum, xr); break;

@@ -470,6 +470,7 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         ma.L = r.L;
         ma.ck = r.ck;
         ma.n = I.N;
+        ma.pairs = r.L % 2 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 7) == 0;
         if (r.timing) r.timing->record(r.stream, &g0);
         if ((e = launch_mt_gen2(r.kind, r.cksum, ma, r.stream)) != cudaSuccess) return e;
         r.version = 5;
