@@ -37,7 +37,11 @@ CONFIGS = {
     "c3-f01": (11213, 2, 1 << 28, "MTGP32-11213 x200 sets, 2^28 f32 (0,1]/set/step (BASELINE config 3)"),
     "c4-23209": (23209, 0, 1 << 28, "MTGP32-23209 x200 synthetic sets, 2^28 u32/set/step (BASELINE config 4)"),
     "c4-44497": (44497, 0, 1 << 28, "MTGP32-44497 x200 synthetic sets, 2^28 u32/set/step (BASELINE config 4)"),
+    # the reference's own recurrence (Engine::mt) on the GPU: like for like with --impl reference
+    "mt19937": (19937, 0, 1 << 28, "Engine::mt MT19937 x200 streams (seeds 5489+i), 2^28 u32/stream/step "
+                                   "(the reference arm's generator, on the GPU)"),
 }
+MT_CONFIGS = {"mt19937"}
 
 
 def parse():
@@ -250,11 +254,19 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     mexp, kind, L_step, label = CONFIGS[args.config]
     S = args.sets
-    sets = shard.sets_for_rank(mexp, S, rank)
-    seeds = [1] * S
+    is_mt = args.config in MT_CONFIGS
+    if is_mt:  # MT19937 statuses, distinct seeds per stream (and per rank)
+        sets = [mtgp.mt19937_status()] * S
+        seeds = [5489 + rank * S + i for i in range(S)]
+    else:
+        sets = shard.sets_for_rank(mexp, S, rank)
+        seeds = [1] * S
+
+    def make_ctx(ss, sd):
+        return mtgp.MtContext(ss, sd, device=local) if is_mt else mtgp.MtgpContext(ss, sd, device=local)
     calls = max(1, args.calls)
     Lc = L_step // calls
-    ctx = mtgp.MtgpContext(sets, seeds, device=local)
+    ctx = make_ctx(sets, seeds)
     ctx.set_option(mtgp.OPT_CHECKSUM, 0 if args.no_checksum else 1)
     ext = torch.cuda.ExternalStream(ctx.stream_handle(), device=torch.device("cuda", local))
     out = torch.empty((S, Lc), dtype=torch.int32, device=f"cuda:{local}")
@@ -263,10 +275,11 @@ def main():
     if rank == 0:
         sys.path.insert(0, str(ROOT / "oracle"))
         import oracle_py
-        probe = mtgp.MtgpContext(sets[:2], seeds[:2], device=local)
+        probe = make_ctx(sets[:2], seeds[:2])
         w = probe.generate_host(kind, 4096)
         probe.close()
-        ref = oracle_py.MtgpOracle(sets[0], seeds[0]).fill(4096, kind=kind)
+        ref = (oracle_py.MtOracle(None, seeds[0]).fill(4096) if is_mt
+               else oracle_py.MtgpOracle(sets[0], seeds[0]).fill(4096, kind=kind))
         if not np.array_equal(w[0], ref):
             raise SystemExit("parity gate failed: GPU stream 0 differs from the oracle")
 
@@ -352,10 +365,11 @@ def main():
                              f"{args.cpu_words_per_thread} words, {secs:.2f} s wall; the reference has no MTGP32"}
             # the CPU MTGP32 restatement (oracle port) timed the same way, one
             # certified set per core, so the MTGP32-vs-MT19937 CPU cost is visible next to the GPU
-            pv, psecs, pn = cpu_mtgp_port(sets, seeds, cores)
-            cpu["mtgp32_port"] = {"value": round(pv, 4), "unit": "Gsamples/s", "cores": cores, "kind": "port",
-                                  "sample": f"oracle/mtgp32_oracle.c bulk fill, {cores} sets x {pn} words "
-                                            f"(one thread per set), {psecs:.2f} s wall"}
+            if not is_mt:  # the reference itself is the MT19937 baseline; add the MTGP32 port's cost
+                pv, psecs, pn = cpu_mtgp_port(sets, seeds, cores)
+                cpu["mtgp32_port"] = {"value": round(pv, 4), "unit": "Gsamples/s", "cores": cores, "kind": "port",
+                                      "sample": f"oracle/mtgp32_oracle.c bulk fill, {cores} sets x {pn} words "
+                                                f"(one thread per set), {psecs:.2f} s wall"}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "error": str(e)[:200]}
 
@@ -367,7 +381,7 @@ def main():
         Le = 1 << 20
         host = torch.empty((S, Le), dtype=torch.int32, pin_memory=True)
         hv = host.numpy().view(np.uint32)
-        ectx = mtgp.MtgpContext(sets, seeds, device=local)
+        ectx = make_ctx(sets, seeds)
         ectx.set_option(mtgp.OPT_HOST_CHUNK, 1 << 18)
         ectx.generate_host(kind, Le, out=hv)
         reps = 5
@@ -400,7 +414,8 @@ def main():
                        "checksums_fused": not args.no_checksum,
                        "checksums_gathered_streams": gathered_streams,
                        "l2": "output 4*S*L/calls bytes per call >> 126 MB L2; no flush needed",
-                       "parameter_sets": ("synthetic (uncertified period)" if mexp != 11213 or S > 200
+                       "parameter_sets": ("MT19937 (mt19937_params, proj/src/params.cpp:63-77)" if is_mt
+                                          else "synthetic (uncertified period)" if mexp != 11213 or S > 200
                                           else "cuRAND MTGP32-11213 (certified)" if world == 1
                                           else "rank 0: cuRAND MTGP32-11213 (certified); ranks 1..N-1: synthetic "
                                                "MTGP32-11213 (uncertified period)")},
@@ -408,7 +423,8 @@ def main():
                          "frac": round(achieved / hbm, 4), "traffic": traffic_per_launch(bytes_per_launch),
                          "traffic_source": "profiles/gen_traffic.json (ncu dram__bytes_read+write per algorithmic byte)",
                          "peak_source": hbm_src,
-                         "kernel": f"gen{kver if kver in (3, 4) else ''}_kernel (v{kver})", "launches_timed": gen_n,
+                         "kernel": ("mt_gen2_kernel (v5, Engine::mt warp teams)" if kver == 5 else
+                                    f"gen{kver if kver in (3, 4) else ''}_kernel (v{kver})"), "launches_timed": gen_n,
                          "avg_launch_ms": round(gen_avg_ms, 4),
                          "algorithmic_bytes_per_launch": bytes_per_launch,
                          "step_write_GBps": round(step_gbs, 1),
