@@ -392,7 +392,9 @@ int mtgp_generate(mtgp_ctx* ctx, int kind, void* out, uint64_t L, int out_is_dev
     // and copy each chunk out with one strided 2-D copy, overlapping generation of chunk c+1
     // with the copy of chunk c.
     const size_t es = kind == MTGP_F64_01 ? 8 : 4;  // bytes per sample
-    const uint64_t Lc = std::min<uint64_t>(L, ctx->host_chunk);
+    // chunk lengths are multiples of 4 (the register-resident kernels need L % 4 == 0 per call),
+    // so the device path a request takes does not depend on the staging size
+    const uint64_t Lc = std::min<uint64_t>(L, std::max<uint64_t>(4, ctx->host_chunk & ~3ull));
     const size_t chunk_bytes = (size_t)Lc * ctx->n_sets * es;
     if (ctx->stage_bytes < 2 * chunk_bytes) {
         CK(cudaStreamSynchronize(ctx->copy_stream), "sync");
@@ -449,11 +451,14 @@ int mtgp_skip(mtgp_ctx* ctx, uint64_t words) {
         void* scratch = nullptr;
         CK(cudaMalloc(&scratch, (size_t)chunk * ctx->n_sets * 4), "cudaMalloc skip scratch");
         const bool ck = ctx->cksum;
+        const int kern = ctx->kernel;
         ctx->cksum = false;
+        ctx->kernel = 0;  // internal scratch generation: any kernel that takes the shape
         int rc = MTGP_OK;
         for (uint64_t done = 0; done < words && rc == MTGP_OK; done += chunk)
             rc = generate_device(ctx, MTGP_U32, scratch, std::min<uint64_t>(chunk, words - done));
         ctx->cksum = ck;
+        ctx->kernel = kern;
         cudaStreamSynchronize(ctx->stream);
         cudaFree(scratch);
         return rc;
