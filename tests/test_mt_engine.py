@@ -220,3 +220,31 @@ def test_mt_shapes_without_teams_fall_back(mt_golden):
     assert kv == 1
     assert np.array_equal(w[0], oracle_py.ref_fill(70000, 4357, mt_golden["dc521_id7"]["status12"]))
     assert np.array_equal(w[1], oracle_py.ref_fill(70000, 5489))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("engine", ["mt", "mtgp"])
+def test_zero_state_emits_zero_forever(engine, curand_sets):
+    """proj/tests/test_generator.cpp:52-57: an all-zero state is a fixed point (from_state with a
+    zero state). Restoring a zero window must give 0 words on every path, incl. jumped pieces."""
+    if engine == "mt":
+        ctx = mtgp.MtContext([mtgp.mt19937_status()] * 2, [1, 2])
+    else:
+        ctx = mtgp.MtgpContext(curand_sets[:2], [1, 2])
+    with ctx:
+        win, pos = ctx.state_save()
+        ctx.state_restore(np.zeros_like(win), pos)
+        ctx.set_option(mtgp.OPT_MIN_PIECE_WORDS, 1 << 12)
+        w = ctx.fill_u32(100000)
+    assert not w.any()
+
+
+@pytest.mark.gpu
+def test_mt_seed0_state_and_first_words():
+    """test_generator.cpp:27-50: seed 0 seeds a non-zero state with
+    st[1] = 1812433253 * (0 ^ (0 >> 30)) + 1 = 1; the words equal the reference's."""
+    with mtgp.MtContext([mtgp.mt19937_status()], [0]) as ctx:
+        win, _ = ctx.state_save()
+        w = ctx.fill_u32(2000)
+    assert win[0, 0] == 0 and win[0, 1] == 1 and win[0].any()
+    assert np.array_equal(w[0], oracle_py.ref_fill(2000, 0))
