@@ -343,3 +343,25 @@ def test_v4_short_and_edge_lengths(curand_sets, mexp, L):
         b = ctx.fill_u32(1000 + 4 * (L % 3))
     ref, _ = oracle_py.mtgp_bulk(sets, [5, 6, 7], L + b.shape[1], threads=3)
     assert np.array_equal(a, ref[:, :L]) and np.array_equal(b, ref[:, L:])
+
+
+@pytest.mark.parametrize("mexp", [3217, 4253, 4423, 9689, 9941, 19937, 21701])
+def test_other_mtgp_exponents_cta_per_stream(mexp):
+    """The remaining MTGP32 exponents (mtgp_validate_params' list) run on the CTA-per-stream
+    kernel: bit-exact across calls, skips and save/restore."""
+    sets = tables.synthetic_sets(mexp, 3)
+    seeds = [3, 5, 7]
+    with mtgp.MtgpContext(sets, seeds) as ctx:
+        a = ctx.fill_u32(5001)
+        _, _, kv = ctx.last_plan()
+        win, pos = ctx.state_save()
+        b = ctx.fill_u32(999)
+        ctx.state_restore(win, pos)
+        b2 = ctx.fill_u32(999)
+        ctx.skip(12345)
+        c = ctx.fill_u32(100)
+    assert kv == 1
+    ref, _ = oracle_py.mtgp_bulk(sets, seeds, 5001 + 999 + 12345 + 100, threads=3)
+    assert np.array_equal(a, ref[:, :5001])
+    assert np.array_equal(b, ref[:, 5001:6000]) and np.array_equal(b2, b)
+    assert np.array_equal(c, ref[:, 6000 + 12345:])
