@@ -24,10 +24,12 @@
 namespace mtgpb {
 
 // Steps per main-loop trip: 0 = K (the history shift is pure register renaming, but the code is
-// K times larger -- 16 C-stream variants at 23209 overflow the instruction cache); otherwise the
-// shift costs register moves (IMAD.MOV, FMA pipe) at the loop back-edge.
+// K times larger); otherwise the shift costs register moves (IMAD.MOV, FMA pipe) at the loop
+// back-edge. -1 (default) = per history depth, measured (profiles/r1_v4_unroll_sweep.jsonl):
+// K <= 3 (11213, 23209): K; K >= 4 (44497, K = 6): 2 -- full unrolling there spills at the
+// 128-register cap and U = 3 is slower than U = 2.
 #ifndef MTGP4_UNROLL
-#define MTGP4_UNROLL 1
+#define MTGP4_UNROLL -1
 #endif
 #ifndef MTGP4_BIG_CTA
 #define MTGP4_BIG_CTA 1
@@ -51,7 +53,7 @@ struct S4 {
     static constexpr uint32_t AC_MIN = (BASE + 1) >> 7;  // pos >= 2
     static constexpr uint32_t AC_MAX = H - 3;            // pos <= N - 256
     static constexpr int MIN_CTAS = MTGP4_MIN_CTAS ? MTGP4_MIN_CTAS : (K == 2 ? 6 : K == 3 ? 5 : 4);
-    static constexpr uint32_t U = MTGP4_UNROLL ? MTGP4_UNROLL : K;  // steps per main-loop trip
+    static constexpr uint32_t U = MTGP4_UNROLL > 0 ? MTGP4_UNROLL : MTGP4_UNROLL == 0 || K <= 3 ? K : 2;  // steps/trip
     // One CTA per SM holding all of the SM's warps (MIN_CTAS x 4): teams are ordered by stream,
     // so a CTA's warps share one or two streams -- one or two C-stream variants per SM instead of
     // one per 4-warp CTA (the variants otherwise thrash the instruction cache).
