@@ -423,8 +423,10 @@ def main():
                          "frac": round(achieved / hbm, 4), "traffic": traffic_per_launch(bytes_per_launch),
                          "traffic_source": "profiles/gen_traffic.json (ncu dram__bytes_read+write per algorithmic byte)",
                          "peak_source": hbm_src,
-                         "kernel": ("mt_gen2_kernel (v5, Engine::mt warp teams)" if kver == 5 else
-                                    f"gen{kver if kver in (3, 4) else ''}_kernel (v{kver})"), "launches_timed": gen_n,
+                         "kernel": {5: "mt_gen2_kernel (v5, Engine::mt warp teams, shared-memory rings)",
+                                    6: "mt_gen3_kernel (v6, Engine::mt register-resident warp teams)"}.get(
+                                        kver, f"gen{kver if kver in (3, 4) else ''}_kernel (v{kver})"),
+                         "launches_timed": gen_n,
                          "avg_launch_ms": round(gen_avg_ms, 4),
                          "algorithmic_bytes_per_launch": bytes_per_launch,
                          "step_write_GBps": round(step_gbs, 1),

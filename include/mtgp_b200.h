@@ -85,7 +85,9 @@ typedef struct mtgp_ctx mtgp_ctx;
 #define MTGP_OPT_CHECKSUM 1        /* 0/1: accumulate mtgp_cksum in-kernel (default 1)              */
 #define MTGP_OPT_KERNEL 2          /* 0 = auto, 1 = reference-shaped v1 (one CTA per set), 2 = v2 */
                                    /* (shared-memory ring), 3 = v3 (register ring, mexp 11213),   */
-                                   /* 4 = v4 (register ring for any supported exponent)           */
+                                   /* 4 = v4 (register ring for any supported exponent);          */
+                                   /* Engine::mt contexts: 5 = warp teams, shared-memory rings,   */
+                                   /* 6 = warp teams, register-resident (n = 624)                 */
 #define MTGP_OPT_MAX_PIECES 3      /* cap on jump-ahead pieces per call (0 = auto)                  */
 #define MTGP_OPT_MIN_PIECE_WORDS 4 /* minimum words per jump-ahead piece (default 1<<21)            */
 #define MTGP_OPT_TIMING 5          /* 0/1: record CUDA events around every generation kernel        */
@@ -198,13 +200,17 @@ int mtgp_mt_validate_params(const mtgp_mt_params* p);
  * words, stride = max n), checksums, positions, mtgp_skip, mtgp_certify,
  * mtgp_mt_charpoly_digest and mtgp_stat_run. When every status has the same mexp and n and
  * n - m >= 32, generation and long skips use the jump-ahead planner with warp teams (kernel
- * version 5 in mtgp_last_plan); otherwise (and for MTGP_F64_01) one CTA per stream.
+ * version 5 in mtgp_last_plan; version 6, the register-resident team kernel, for n = 624 with
+ * every n - m >= 129, u32 output, words_per_stream % 4 == 0 and 16-byte aligned output);
+ * otherwise (and for MTGP_F64_01) one CTA per stream. MTGP_OPT_KERNEL 5 / 6 force the team
+ * kernel, 1 the CTA-per-stream one.
  */
 int mtgp_mt_ctx_create(mtgp_ctx** out, int device, const mtgp_mt_params* sets, uint32_t n_sets,
                        const uint32_t* seeds, void* stream);
 
 /* Launch plan of the last generation call: pieces (jump-ahead segments), warps per piece and the
-   kernel (1 CTA per stream, 2 shared-memory ring, 3 / 4 register ring, 5 Engine::mt warp teams). */
+   kernel (1 CTA per stream, 2 shared-memory ring, 3 / 4 register ring, 5 Engine::mt warp teams
+   with shared-memory rings, 6 Engine::mt register-resident warp teams). */
 int mtgp_last_plan(const mtgp_ctx* ctx, uint32_t* pieces, uint32_t* warps_per_piece,
                    uint32_t* kernel_version);
 

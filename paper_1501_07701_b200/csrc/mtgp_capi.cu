@@ -235,7 +235,8 @@ int mtgp_mt_ctx_create(mtgp_ctx** out, int device, const mtgp_mt_params* sets, u
     std::vector<uint32_t> win((size_t)n_sets * nmax, 0);
     for (uint32_t s = 0; s < n_sets; ++s) {
         const mtgp_mt_params& p = sets[s];
-        dp[s] = DevMtParams{p.n, p.m, p.r, p.a, p.temper_b, p.temper_c, p.temper_u, p.temper_s, p.temper_t, p.temper_l, 0, 0};
+        dp[s] = DevMtParams{p.n, p.m, p.r, p.a, p.temper_b, p.temper_c, p.temper_u, p.temper_s, p.temper_t, p.temper_l,
+                            1u << p.temper_s, 1u << p.temper_t};  // shifts validated in [1, 31]
         uint32_t* x = win.data() + (size_t)s * nmax;
         x[0] = seeds[s];
         for (uint32_t i = 1; i < p.n; ++i) x[i] = 1812433253u * (x[i - 1] ^ (x[i - 1] >> 30)) + i;
@@ -284,7 +285,7 @@ int mtgp_set_option(mtgp_ctx* ctx, int option, int64_t value) {
     switch (option) {
         case MTGP_OPT_CHECKSUM: ctx->cksum = value != 0; return MTGP_OK;
         case MTGP_OPT_KERNEL:
-            if (value < 0 || value > 4) return fail(MTGP_EINVAL, "kernel must be 0 (auto), 1, 2, 3 or 4");
+            if (value < 0 || value > 6) return fail(MTGP_EINVAL, "kernel must be 0 (auto) or 1 .. 6");
             ctx->kernel = (int)value;
             return MTGP_OK;
         case MTGP_OPT_MAX_PIECES:
@@ -359,7 +360,8 @@ int generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
         run.max_pieces = ctx->max_pieces;
         run.min_piece_words = ctx->min_piece_words;
         run.timing = ctx->timing ? &ctx->pool : nullptr;
-        run.want_kernel = ctx->engine == 1 ? 0 : ctx->kernel;
+        // Engine::mt contexts: 5 / 6 pick the warp-team kernel, the MTGP kernel numbers mean auto
+        run.want_kernel = ctx->engine == 1 ? (ctx->kernel >= 5 ? ctx->kernel : 0) : ctx->kernel;
         std::string err;
         cudaError_t e = ctx->planner->run(run, err);
         if (e != cudaSuccess) return fail(e == cudaErrorMemoryAllocation ? MTGP_ENOMEM : MTGP_ECUDA, "v2 generation: %s (%s)", err.c_str(), cudaGetErrorString(e));

@@ -6,7 +6,8 @@
 namespace mtgpb {
 
 struct alignas(16) DevMtParams {
-    uint32_t n, m, r, a, b, c, u, s, t, l, pad0, pad1;
+    uint32_t n, m, r, a, b, c, u, s, t, l;
+    uint32_t mul_s, mul_t;  // 2^s, 2^t: the left shifts of the tempering as IMADs (mt_gen3)
 };
 
 cudaError_t launch_mt_v1(int kind, bool cksum, const DevMtParams* params, uint32_t* win, uint32_t n_sets,
@@ -32,5 +33,10 @@ cudaError_t launch_mt_prefix(const DevMtParams* params, const uint32_t* win, con
                              uint32_t n, uint32_t* pre, uint32_t len, cudaStream_t st);
 cudaError_t launch_mt_gen2(int kind, bool cksum, const MtGenArgs& a, cudaStream_t st);
 int mt_gen2_ctas_per_sm(uint32_t n, int kind, bool cksum);
+// Register-resident warp teams (csrc/mtgp_mt3.cu, kernel version 6): n = 624, every status
+// n - m >= 129 (min_gap), u32 output, L % 4 == 0, 16-byte aligned output.
+bool mt_gen3_supports(uint32_t n, uint32_t min_gap, int kind);
+cudaError_t launch_mt_gen3(uint32_t n, bool cksum, const MtGenArgs& a, cudaStream_t st);
+int mt_gen3_ctas_per_sm(uint32_t n, bool cksum);
 
 }  // namespace mtgpb

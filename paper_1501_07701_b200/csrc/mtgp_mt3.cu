@@ -1,0 +1,292 @@
+// mtgp_mt3.cu -- register-resident Engine::mt generation (kernel version 6, mt_gen3_kernel):
+// gen4's design (csrc/mtgp_v4.cuh) applied to the reference's classic MT recurrence
+// (proj/src/generator.cpp:68-88, temper :7-13), for the MT19937 state shape n = 624.
+//
+// The recurrences have the same operand structure -- MTGP32 reads x_k, x_{k+1}, x_{k+pos}; MT
+// reads x_k, x_{k+1}, x_{k+m} -- so the A stream (x_k, x_{k+1}) and the C stream (x_{k+m}) are
+// fetched exactly as in gen4: every operand word is ONE shfl.idx from a fixed source lane of ONE
+// SEL-chosen history register. What differs:
+//   * step = one 128-word half-step (lane t makes words 4t..4t+3, one STG.128): n - m = 227
+//     for MT19937, below gen4's 256-word step; any n - m >= 129 works here;
+//   * history = H = ceil(n / 128) half-steps (5 for n = 624, 20 registers), BASE = 128 H - n;
+//     operand x_{g-n+off} of the word at step position p is history position BASE + off + p;
+//   * the C stream's register pair a_C = (BASE + m) / 128 and residue (BASE + m) mod 4 are
+//     template parameters (4 x 4 variants for n = 624, one per status m class);
+//   * no table lookups: the tempering is four shift/mask steps on the new word itself, the left
+//     shifts as IMAD by 2^s / 2^t (FMA pipe), the right shifts and masks on the ALU pipe;
+//   * the step loop is unrolled by H, so the history shift is register renaming.
+// u32 output; pieces come from the shared planner / jump-ahead (csrc/mtgp_plan.cu), windows in
+// the same n-word window model as every other kernel.
+#include "mtgp_mt.cuh"
+#include "mtgp_v2.cuh"
+
+#ifndef MTGP6_MIN_CTAS
+#define MTGP6_MIN_CTAS 5  // 6: 19% more pieces (jumps) for the same cycles
+#endif
+// Right shifts of the tempering on the FMA pipe as IMAD.HI by 2^(32-k): 0 none, 1 the last
+// (v >> l), 2 both (v >> u too).
+#ifndef MTGP6_SHR_IMAD
+#define MTGP6_SHR_IMAD 0
+#endif
+#ifndef MTGP6_CK_WIDE
+#define MTGP6_CK_WIDE 0
+#endif
+
+namespace mtgpb {
+
+namespace {
+
+constexpr uint32_t kFull6 = 0xffffffffu;
+constexpr uint32_t kHalfWords = 128;
+
+template <uint32_t NW>
+struct S6 {
+    static constexpr uint32_t N = NW;
+    static constexpr uint32_t H = (N + kHalfWords - 1) / kHalfWords;  // half-steps of history
+    static constexpr uint32_t BASE = kHalfWords * H - N;               // history position of x_{g-n}, p = 0
+    static constexpr uint32_t QA = BASE >> 2, RA = BASE & 3;
+    static constexpr uint32_t AA = QA >> 5, BA = QA & 31;
+    static constexpr uint32_t AC_MAX = H - 2;  // n - m >= 129
+};
+
+struct M6Ctx {
+    uint32_t lane;
+    uint32_t upper, a, b, c, u, l, mul_s, mul_t, hi_u, hi_l, one;
+    uint32_t srcA0, srcA1, srcC0, srcC1;  // source lanes for carry e = 0 / 1
+    bool pA0, pA1, pC0, pC1;              // "send the newer half-step of the pair"
+};
+
+__device__ __forceinline__ uint32_t comp6(const uint4& g, int c) {
+    return c == 0 ? g.x : c == 1 ? g.y : c == 2 ? g.z : g.w;
+}
+
+// v >> k on the ALU pipe, or as the high word of v * 2^(32-k) on the FMA pipe
+template <bool IMAD>
+__device__ __forceinline__ uint32_t shr6(uint32_t v, uint32_t k, uint32_t hi) {
+    if (!IMAD) return v >> k;
+    uint32_t r;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(v), "r"(hi));
+    return r;
+}
+
+// CNT consecutive operand words: residue R, register pair (Hs[LO], Hs[LO + 1]).
+template <int R, int LO, int CNT, int NH>
+__device__ __forceinline__ void fetch6(uint32_t* W, const uint4 (&Hs)[NH], uint32_t src0, uint32_t src1, bool p0,
+                                       bool p1) {
+#pragma unroll
+    for (int j = 0; j < CNT; ++j) {
+        const int c = (R + j) & 3;
+        const int e = (R + j) >> 2;
+        const uint32_t send = (e ? p1 : p0) ? comp6(Hs[LO + 1], c) : comp6(Hs[LO], c);
+        W[j] = __shfl_sync(kFull6, send, e ? src1 : src0);
+    }
+}
+
+// One 128-word step at piece word n; dst = this lane's 16-byte slot of the step's output.
+template <uint32_t NW, int RC, int AC, bool CK, bool TAIL>
+__device__ __forceinline__ void step6(const M6Ctx& p, const uint4 (&Hs)[S6<NW>::H], uint4& nw, uint4* dst,
+                                      uint32_t n, uint32_t len, uint32_t* win_out, unsigned long long& sum,
+                                      uint32_t& xr) {
+    using S = S6<NW>;
+    uint32_t WA[5], WC[4];
+    fetch6<S::RA, S::AA, 5, S::H>(WA, Hs, p.srcA0, p.srcA1, p.pA0, p.pA1);
+    fetch6<RC, AC, 4, S::H>(WC, Hs, p.srcC0, p.srcC1, p.pC0, p.pC1);
+    uint32_t r[4], o[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        // refill (generator.cpp:68-88): y = upper(x_k) | lower(x_{k+1});
+        // x_{k+n} = x_{k+m} ^ (y >> 1) ^ (y odd ? a : 0)
+        const uint32_t y = (WA[c] & p.upper) | (WA[c + 1] & ~p.upper);  // one LOP3
+        uint32_t mag;  // (y & 1) * a as an IMAD (inline PTX: not turned back into ISETP + SEL)
+        asm("mul.lo.u32 %0, %1, %2;" : "=r"(mag) : "r"(y & 1u), "r"(p.a));
+        r[c] = WC[c] ^ (y >> 1) ^ mag;
+        // temper (generator.cpp:7-13)
+        uint32_t v = r[c];
+        v ^= shr6<MTGP6_SHR_IMAD >= 2>(v, p.u, p.hi_u);
+        v ^= (v * p.mul_s) & p.b;
+        v ^= (v * p.mul_t) & p.c;
+        v ^= shr6<MTGP6_SHR_IMAD >= 1>(v, p.l, p.hi_l);
+        o[c] = v;
+    }
+    const uint32_t w0 = n + 4 * p.lane;  // piece word of o[0]
+    if (!TAIL || w0 < len) {
+        __stcs(dst, make_uint4(o[0], o[1], o[2], o[3]));
+        if (CK) {
+#if MTGP6_CK_WIDE
+            // 64-bit sum on the FMA pipe: IMAD.WIDE.U32 sum = o * 1 + sum (the 1 is opaque)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(sum) : "r"(o[c]), "r"(p.one));
+#else
+#pragma unroll
+            for (int c = 0; c < 4; ++c) sum += o[c];
+#endif
+            xr ^= o[0] ^ o[1] ^ o[2] ^ o[3];
+        }
+    }
+    if (TAIL && win_out) {
+        // sequence index of r[c] is n_state + w0 + c; the end window is [len, len + n_state)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const uint32_t k = S::N + w0 + c - len;
+            if (k < S::N) win_out[k] = r[c];
+        }
+    }
+    nw = make_uint4(r[0], r[1], r[2], r[3]);
+}
+
+template <int NH>
+__device__ __forceinline__ void shift1(uint4 (&Hs)[NH], const uint4& nw) {
+#pragma unroll
+    for (int i = 0; i + 1 < NH; ++i) Hs[i] = Hs[i + 1];
+    Hs[NH - 1] = nw;
+}
+
+template <uint32_t NW, int RC, int AC, bool CK>
+__device__ __forceinline__ void run6(const M6Ctx& p, uint4 (&Hs)[S6<NW>::H], uint32_t* optr, uint32_t len,
+                                     uint32_t* win_out, unsigned long long& sum, uint32_t& xr) {
+    using S = S6<NW>;
+    const uint32_t steps = (len + kHalfWords - 1) / kHalfWords;
+    // A step at n makes sequence words [N + n, N + n + 128): no store predicate and no end
+    // window while n + 128 + N <= len. The main loop runs H such steps per trip (the history
+    // returns to its registers); the rest run the predicated tail variant.
+    uint32_t m = 0;
+    uint4* dst = reinterpret_cast<uint4*>(optr) + p.lane;  // step m's slot: dst + 32 m
+    for (; (m + S::H) * kHalfWords + S::N <= len; m += S::H, dst += 32 * S::H) {
+#pragma unroll
+        for (uint32_t k = 0; k < S::H; ++k) {
+            uint4 nw;
+            step6<NW, RC, AC, CK, false>(p, Hs, nw, dst + 32 * k, (m + k) * kHalfWords, len, nullptr, sum, xr);
+            shift1(Hs, nw);
+        }
+    }
+    for (; m < steps; ++m, dst += 32) {
+        uint4 nw;
+        step6<NW, RC, AC, CK, true>(p, Hs, nw, dst, m * kHalfWords, len, win_out, sum, xr);
+        shift1(Hs, nw);
+    }
+}
+
+template <uint32_t NW, int AC, bool CK>
+__device__ __forceinline__ void run6_rc(int rc, const M6Ctx& p, uint4 (&Hs)[S6<NW>::H], uint32_t* optr,
+                                        uint32_t len, uint32_t* win_out, unsigned long long& sum, uint32_t& xr) {
+    switch (rc) {
+        case 0: run6<NW, 0, AC, CK>(p, Hs, optr, len, win_out, sum, xr); break;
+        case 1: run6<NW, 1, AC, CK>(p, Hs, optr, len, win_out, sum, xr); break;
+        case 2: run6<NW, 2, AC, CK>(p, Hs, optr, len, win_out, sum, xr); break;
+        default: run6<NW, 3, AC, CK>(p, Hs, optr, len, win_out, sum, xr); break;
+    }
+}
+
+template <uint32_t NW, int AC, bool CK>
+__device__ __forceinline__ void run6_ac(int ac, int rc, const M6Ctx& p, uint4 (&Hs)[S6<NW>::H], uint32_t* optr,
+                                        uint32_t len, uint32_t* win_out, unsigned long long& sum, uint32_t& xr) {
+    if constexpr (AC <= (int)S6<NW>::AC_MAX) {
+        if (ac == AC)
+            run6_rc<NW, AC, CK>(rc, p, Hs, optr, len, win_out, sum, xr);
+        else
+            run6_ac<NW, AC + 1, CK>(ac, rc, p, Hs, optr, len, win_out, sum, xr);
+    }
+}
+
+}  // namespace
+
+template <uint32_t NW, bool CK>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, MTGP6_MIN_CTAS) mt_gen3_kernel(MtGenArgs a) {
+    using S = S6<NW>;
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t team = blockIdx.x * kWarpsPerCta + warp;
+    if (team >= a.n_teams) return;
+    M6Ctx p;
+    p.lane = lane;
+    p.srcA0 = (lane + S::BA) & 31;
+    p.srcA1 = (lane + S::BA + 1) & 31;
+    p.pA0 = lane < S::BA;
+    p.pA1 = lane < S::BA + 1;
+    const TeamWork tw = a.teams[team];
+    for (uint32_t pi = tw.first; pi < tw.first + tw.count; ++pi) {
+        const Piece pc = a.pieces[pi];
+        const DevMtParams prm = a.params[pc.set];
+        p.upper = prm.r ? (0xFFFFFFFFu << prm.r) : 0xFFFFFFFFu;
+        p.a = prm.a;
+        p.b = prm.b;
+        p.c = prm.c;
+        p.u = prm.u;
+        p.l = prm.l;
+        p.mul_s = prm.mul_s;  // 2^s, 2^t from the host: opaque, so the shifts stay IMADs
+        p.mul_t = prm.mul_t;
+        p.hi_u = 1u << (32 - prm.u);  // u, l in [1, 31]
+        p.hi_l = 1u << (32 - prm.l);
+        p.one = prm.n / S::N;  // 1, opaque to the compiler
+        const uint32_t qc = (S::BASE + prm.m) >> 2;  // C stream: BASE + m = 4 qc + rc
+        const int rc = (int)((S::BASE + prm.m) & 3);
+        const int ac = (int)(qc >> 5);
+        const uint32_t thr0 = qc & 31, thr1 = thr0 + 1;  // in [0, 32]
+        p.srcC0 = (lane + thr0) & 31;
+        p.srcC1 = (lane + thr1) & 31;
+        p.pC0 = lane < thr0;
+        p.pC1 = lane < thr1;
+        uint32_t* optr = reinterpret_cast<uint32_t*>(a.out) + (size_t)pc.set * a.L + pc.offset;
+        const uint32_t len = (uint32_t)pc.len;
+        const uint32_t* w0 = a.piece_win[pi];
+        // history before step 0: half-step h, lane t, component c holds x_{128h + 4t + c - BASE}
+        uint4 Hs[S::H];
+#pragma unroll
+        for (int h = 0; h < (int)S::H; ++h) {
+            uint32_t v[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int k = (int)kHalfWords * h + 4 * (int)lane + c - (int)S::BASE;
+                v[c] = k >= 0 ? w0[k] : 0u;
+            }
+            Hs[h] = make_uint4(v[0], v[1], v[2], v[3]);
+        }
+        uint32_t* win_out = nullptr;
+        if (pc.offset + pc.len == a.L) {
+            win_out = a.win_out + (size_t)pc.set * S::N;
+            for (uint32_t j = lane; j + len < S::N; j += 32) win_out[j] = w0[len + j];  // pieces shorter than n
+        }
+        unsigned long long sum = 0;
+        uint32_t xr = 0;
+        run6_ac<NW, 0, CK>(ac, rc, p, Hs, optr, len, win_out, sum, xr);
+        if (CK) {
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) {
+                sum += __shfl_xor_sync(kFull6, sum, s);
+                xr ^= __shfl_xor_sync(kFull6, xr, s);
+            }
+            if (lane == 0) {
+                atomicAdd(&a.ck[pc.set].sum64, sum);
+                atomicXor(&a.ck[pc.set].xor32, xr);
+                atomicAdd(&a.ck[pc.set].words, (unsigned long long)len);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+bool mt_gen3_supports(uint32_t n, uint32_t min_gap, int kind) {
+    return kind == MTGP_U32 && n == 624 && min_gap >= 129;
+}
+
+cudaError_t launch_mt_gen3(uint32_t n, bool cksum, const MtGenArgs& a, cudaStream_t st) {
+    if (a.n_teams == 0) return cudaSuccess;
+    if (n != 624) return cudaErrorInvalidValue;
+    const uint32_t grid = (a.n_teams + kWarpsPerCta - 1) / kWarpsPerCta;
+    if (cksum)
+        mt_gen3_kernel<624, true><<<grid, kWarpsPerCta * 32, 0, st>>>(a);
+    else
+        mt_gen3_kernel<624, false><<<grid, kWarpsPerCta * 32, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+int mt_gen3_ctas_per_sm(uint32_t n, bool cksum) {
+    if (n != 624) return 0;
+    int c = 0;
+    const cudaError_t e =
+        cksum ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, mt_gen3_kernel<624, true>, kWarpsPerCta * 32, 0)
+              : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, mt_gen3_kernel<624, false>, kWarpsPerCta * 32, 0);
+    return e == cudaSuccess ? c : 0;
+}
+
+}  // namespace mtgpb

@@ -75,6 +75,7 @@ struct PlannerImpl {
     int num_sms = 148;
     uint32_t M = 0, N = 0, S = 0;
     bool v2 = false;
+    uint32_t mt_min_gap = 0;  // Engine::mt: min over statuses of n - m
 
     // algebra (per set). Polynomials annihilate the state sequence from the reference point
     // x_{t0} on (t0 = N + 8, rounded to 4): degenerate (uncertified) recursions have a
@@ -150,8 +151,11 @@ Planner::Planner(const std::vector<mtgp_mt_params>& sets, int num_sms) : impl_(n
     impl_->N = sets[0].n;
     impl_->t0 = (impl_->N + 8 + 3) & ~3u;
     impl_->v2 = true;
-    for (const auto& p : sets)
+    impl_->mt_min_gap = impl_->N;
+    for (const auto& p : sets) {
         if (p.mexp != impl_->M || p.n != impl_->N || p.n - p.m < 32) impl_->v2 = false;
+        impl_->mt_min_gap = std::min(impl_->mt_min_gap, p.n - p.m);
+    }
 }
 Planner::~Planner() = default;
 
@@ -389,6 +393,19 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         err = "the Engine::mt warp-team kernel has no f64 output";
         return cudaSuccess;
     }
+    // Engine::mt: mt_gen3 (register-resident, version 6) when the shape allows, else mt_gen2
+    const bool mt3_ok = I.mt && mt_gen3_supports(I.N, I.mt_min_gap, r.kind) && r.L % 4 == 0 &&
+                        (reinterpret_cast<uintptr_t>(r.out) & 15) == 0;
+    if (!I.mt && r.want_kernel >= 5) {
+        err = "kernels 5 and 6 are Engine::mt kernels";
+        return cudaSuccess;
+    }
+    if (r.want_kernel == 6 && !mt3_ok) {
+        err = "kernel 6 needs n = 624, n - m >= 129 for every status, u32 output, words_per_stream % 4 == 0 "
+              "and 16-byte aligned output";
+        return cudaSuccess;
+    }
+    const bool use_mt3 = mt3_ok && r.want_kernel != 5;
     if (r.want_kernel == 3 && !v3_ok) {
         err = "kernel v3 needs mexp 11213, words_per_stream % 4 == 0 and 16-byte aligned output";
         return cudaSuccess;
@@ -402,7 +419,8 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     // v2 for request shapes the register kernels do not take (float kinds, L % 4 != 0, ...)
     const bool use_v3 = v3_ok && (r.want_kernel == 3 || (r.want_kernel == 0 && I.M == 11213));
     const bool use_v4 = !use_v3 && v4_ok && (r.want_kernel == 4 || (r.want_kernel == 0 && I.M != 11213));
-    const int cps = I.mt     ? mt_gen2_ctas_per_sm(I.N, r.kind, r.cksum)
+    const int cps = use_mt3  ? mt_gen3_ctas_per_sm(I.N, r.cksum)
+                    : I.mt   ? mt_gen2_ctas_per_sm(I.N, r.kind, r.cksum)
                     : use_v3 ? gen3_ctas_per_sm(r.kind, r.cksum)
                     : use_v4 ? gen4_ctas_per_sm(I.M, r.kind, r.cksum)
                              : gen_ctas_per_sm(I.M, r.kind, r.cksum);
@@ -472,8 +490,9 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         ma.n = I.N;
         ma.pairs = r.L % 2 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 7) == 0;
         if (r.timing) r.timing->record(r.stream, &g0);
-        if ((e = launch_mt_gen2(r.kind, r.cksum, ma, r.stream)) != cudaSuccess) return e;
-        r.version = 5;
+        e = use_mt3 ? launch_mt_gen3(I.N, r.cksum, ma, r.stream) : launch_mt_gen2(r.kind, r.cksum, ma, r.stream);
+        if (e != cudaSuccess) return e;
+        r.version = use_mt3 ? 6 : 5;
     } else {
         GenArgs ga;
         ga.params = static_cast<const DevParams*>(r.params);

@@ -53,7 +53,8 @@ struct S4 {
     static constexpr uint32_t AC_MIN = (BASE + 1) >> 7;  // pos >= 2
     static constexpr uint32_t AC_MAX = H - 3;            // pos <= N - 256
     static constexpr int MIN_CTAS = MTGP4_MIN_CTAS ? MTGP4_MIN_CTAS : (K == 2 ? 6 : K == 3 ? 5 : 4);
-    static constexpr uint32_t U = MTGP4_UNROLL > 0 ? MTGP4_UNROLL : MTGP4_UNROLL == 0 || K <= 3 ? K : 2;  // steps/trip
+    static constexpr int kUnroll = MTGP4_UNROLL;
+    static constexpr uint32_t U = kUnroll > 0 ? (uint32_t)kUnroll : (kUnroll == 0 || K <= 3) ? K : 2u;  // steps/trip
     // One CTA per SM holding all of the SM's warps (MIN_CTAS x 4): teams are ordered by stream,
     // so a CTA's warps share one or two streams -- one or two C-stream variants per SM instead of
     // one per 4-warp CTA (the variants otherwise thrash the instruction cache).

@@ -170,8 +170,9 @@ def _st12(st):
 @pytest.mark.gpu
 @pytest.mark.parametrize("which", ["mt19937", "m23209", "dc3217"])
 def test_mt_warp_teams_with_jumps_vs_reference(mt_golden, which):
-    """Engine::mt through the jump-ahead planner (warp teams, kernel version 5), many pieces per
-    stream, bit-exact against the reference compiled from its sources; the next call continues."""
+    """Engine::mt through the jump-ahead planner (warp teams: kernel version 6 for the n = 624
+    shape, 5 otherwise), many pieces per stream, bit-exact against the reference compiled from
+    its sources; the next call continues."""
     if which == "mt19937":
         sts = [mtgp.mt19937_status()] * 3
     elif which == "m23209":
@@ -186,7 +187,7 @@ def test_mt_warp_teams_with_jumps_vs_reference(mt_golden, which):
         pieces, _, kv = ctx.last_plan()
         b = ctx.fill_u32(5000)
         ck = ctx.checksums()
-    assert kv == 5 and pieces > 3
+    assert kv == (6 if which == "mt19937" else 5) and pieces > 3
     for s in range(3):
         ref = oracle_py.ref_fill(L + 5000, seeds[s], _st12(sts[s]))
         assert np.array_equal(a[s], ref[:L]) and np.array_equal(b[s], ref[L:])
@@ -248,3 +249,59 @@ def test_mt_seed0_state_and_first_words():
         w = ctx.fill_u32(2000)
     assert win[0, 0] == 0 and win[0, 1] == 1 and win[0].any()
     assert np.array_equal(w[0], oracle_py.ref_fill(2000, 0))
+
+
+# (16 + m) / 128 and (16 + m) mod 4 pick mt_gen3's C-stream template variant (csrc/mtgp_mt3.cu,
+# BASE = 16 for n = 624): these m cover all 16 variants, m = 1 and the n - m = 129 boundary.
+MT3_MS = [1, 2, 3, 4, 111, 112, 113, 114, 239, 240, 241, 242, 367, 397, 398, 399, 400, 495]
+
+
+@pytest.mark.gpu
+def test_mt_gen3_every_variant_vs_reference():
+    """mt_gen3 (kernel version 6): n = 624 statuses with every C-stream variant, jumped pieces,
+    a ragged length, a next call shorter than n (pieces shorter than the window) and a long
+    one; bit-exact against the reference, checksums included; kernel 5 agrees."""
+    sts = [_rand_status(19937, m, 100 + i) for i, m in enumerate(MT3_MS)]
+    seeds = [7 * i + 1 for i in range(len(sts))]
+    lens = [200_004, 308, 65_536]
+    outs = {}
+    for kern in (6, 5):
+        with mtgp.MtContext(sts, seeds) as ctx:
+            ctx.set_option(mtgp.OPT_KERNEL, kern)
+            ctx.set_option(mtgp.OPT_MIN_PIECE_WORDS, 1 << 12)
+            ws = []
+            for L in lens:
+                ws.append(ctx.fill_u32(L))
+                assert ctx.last_plan()[2] == kern
+            outs[kern] = (ws, ctx.checksums())
+    total = sum(lens)
+    for s in range(len(sts)):
+        ref = oracle_py.ref_fill(total, seeds[s], _st12(sts[s]))
+        got = np.concatenate([w[s] for w in outs[6][0]])
+        assert np.array_equal(got, ref), MT3_MS[s]
+        c = oracle_py.cksum(ref)
+        assert outs[6][1][s] == (c["sum64"], c["xor32"], total)
+    for a, b in zip(outs[6][0], outs[5][0]):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.gpu
+def test_mt_gen3_shape_limits():
+    """Kernel 6 is refused for L % 4 != 0 and for n - m = 128; auto then uses kernel 5."""
+    st = mtgp.mt19937_status()
+    with mtgp.MtContext([st, st], [1, 2]) as ctx:
+        ctx.set_option(mtgp.OPT_KERNEL, 6)
+        with pytest.raises(mtgp.MtgpInvalidArgument):
+            ctx.fill_u32(1001)
+    with mtgp.MtContext([st, st], [1, 2]) as ctx:
+        w = ctx.fill_u32(1001)
+        assert ctx.last_plan()[2] == 5
+    assert np.array_equal(w[1], oracle_py.ref_fill(1001, 2))
+    edge = _rand_status(19937, 496, 5)
+    with mtgp.MtContext([st, edge], [1, 2]) as ctx:
+        w = ctx.fill_u32(4096)
+        assert ctx.last_plan()[2] == 5
+        ctx.set_option(mtgp.OPT_KERNEL, 6)
+        with pytest.raises(mtgp.MtgpInvalidArgument):
+            ctx.fill_u32(4096)
+    assert np.array_equal(w[1], oracle_py.ref_fill(4096, 2, _st12(edge)))

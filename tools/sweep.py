@@ -7,6 +7,7 @@ the result is reported both as GB/s and as SM cycles per launch (clock-independe
     python tools/sweep.py [words_per_stream] [kind] [mexp] [rounds] [cksum] [sustain_seconds] [kernels]
 
 kernels: comma-separated MTGP_OPT_KERNEL values to compare within each library (default 0 = auto).
+mexp 19937 means Engine::mt MT19937 streams (the reference's preset, seeds 5489 + i).
 
 sustain_seconds > 0: instead of best-of short bursts, each variant generates back to back for
 that long per round (the power-capped regime the bench runs in) and the AVERAGE rate is kept.
@@ -51,7 +52,7 @@ class Clock:
             time.sleep(0.002)
 
 
-sets = tables.sets_for(mexp, 200)
+sets = None if mexp == 19937 else tables.sets_for(mexp, 200)
 out = torch.empty((200, words), dtype=torch.int32, device="cuda")
 libs = sorted((ROOT / "paper_1501_07701_b200" / "variants").glob("*.so"))
 libs.insert(0, mtgp.LIB_PATH)
@@ -59,7 +60,10 @@ ctxs = []
 for path in libs:
     lib = mtgp.load_library(str(path))
     for kern in kernels:
-        ctx = mtgp.MtgpContext(sets, [1] * 200, lib=lib)
+        if sets is None:
+            ctx = mtgp.MtContext([mtgp.mt19937_status()] * 200, [5489 + i for i in range(200)], lib=lib)
+        else:
+            ctx = mtgp.MtgpContext(sets, [1] * 200, lib=lib)
         ctx.set_option(mtgp.OPT_CHECKSUM, cksum)
         ctx.set_option(mtgp.OPT_KERNEL, kern)
         ctx.generate_device(kind, out.data_ptr(), words)  # plan + warm
