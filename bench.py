@@ -327,6 +327,19 @@ def main():
     ctx.set_option(mtgp.OPT_TIMING, 0)
     pieces, _, kver = ctx.last_plan()
 
+    # write-only store peak on this GPU in this run: a fill of the same output
+    # buffer (4*S*Lc bytes, >> L2), best of 3, CUDA events; reported beside the copy-peak roofline
+    wp0 = torch.cuda.Event(enable_timing=True)
+    wp1 = torch.cuda.Event(enable_timing=True)
+    wp_ms = float("inf")
+    for _ in range(3):
+        wp0.record()
+        out.fill_(0)
+        wp1.record()
+        wp1.synchronize()
+        wp_ms = min(wp_ms, wp0.elapsed_time(wp1))
+    write_peak = out.numel() * 4 / (wp_ms / 1e3) / 1e9
+
     if world > 1:
         t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -430,7 +443,10 @@ def main():
                          "avg_launch_ms": round(gen_avg_ms, 4),
                          "algorithmic_bytes_per_launch": bytes_per_launch,
                          "step_write_GBps": round(step_gbs, 1),
-                         "jump_ms_per_call": round(jump_ms / max(1, jump_n), 4)},
+                         "jump_ms_per_call": round(jump_ms / max(1, jump_n), 4),
+                         "write_peak_in_run": {"GBps": round(write_peak, 1), "frac": round(achieved / write_peak, 4),
+                                               "how": f"torch fill_ of the {out.numel() * 4 / 1e9:.1f} GB output "
+                                                      "buffer, best of 3 (write-only store peak)"}},
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,
