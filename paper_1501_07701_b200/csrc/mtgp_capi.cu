@@ -312,8 +312,10 @@ namespace {
 // One device-side generation of L words per stream into device memory `out`.
 int generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
     if (L == 0) return MTGP_OK;
-    const bool mt_teams = ctx->engine == 1 && ctx->kernel != 1 && kind != MTGP_F64_01 && ctx->planner &&
-                          ctx->planner->v2_supported();
+    // Engine::mt f64 (next_f64_01) rides the teams only on the register-resident kernel's shape
+    const bool mt_teams = ctx->engine == 1 && ctx->kernel != 1 && ctx->planner && ctx->planner->v2_supported() &&
+                          (kind != MTGP_F64_01 || ctx->kernel == 6 ||
+                           (ctx->kernel != 5 && ctx->planner->mt3_supported(kind, L, out)));
     if (ctx->engine == 1 && !mt_teams) {
         size_t e0 = 0, e1 = 0;
         if (ctx->timing) ctx->pool.record(ctx->stream, &e0);

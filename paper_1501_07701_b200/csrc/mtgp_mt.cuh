@@ -34,9 +34,9 @@ cudaError_t launch_mt_prefix(const DevMtParams* params, const uint32_t* win, con
 cudaError_t launch_mt_gen2(int kind, bool cksum, const MtGenArgs& a, cudaStream_t st);
 int mt_gen2_ctas_per_sm(uint32_t n, int kind, bool cksum);
 // Register-resident warp teams (csrc/mtgp_mt3.cu, kernel version 6): n = 624, every status
-// n - m >= 129 (min_gap), u32 output, L % 4 == 0, 16-byte aligned output.
+// n - m >= 129 (min_gap), u32 or f64 output, L % 4 == 0, 16-byte aligned output.
 bool mt_gen3_supports(uint32_t n, uint32_t min_gap, int kind);
-cudaError_t launch_mt_gen3(uint32_t n, bool cksum, const MtGenArgs& a, cudaStream_t st);
-int mt_gen3_ctas_per_sm(uint32_t n, bool cksum);
+cudaError_t launch_mt_gen3(uint32_t n, int kind, bool cksum, const MtGenArgs& a, cudaStream_t st);
+int mt_gen3_ctas_per_sm(uint32_t n, int kind, bool cksum);
 
 }  // namespace mtgpb

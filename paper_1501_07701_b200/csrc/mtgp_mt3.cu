@@ -82,8 +82,15 @@ __device__ __forceinline__ void fetch6(uint32_t* W, const uint4 (&Hs)[NH], uint3
     }
 }
 
-// One 128-word step at piece word n; dst = this lane's 16-byte slot of the step's output.
-template <uint32_t NW, int RC, int AC, bool CK, bool TAIL>
+// u32 -> double in [0,1): u * 2^-32 exactly (Generator::next_f64_01, generator.hpp:39-41), as
+// (1 + u * 2^-32) - 1: the bit pattern 0x3FF00000:00000000 | u << 20 minus 1.0 (both exact)
+__device__ __forceinline__ double u32_to_f64_01(uint32_t u) {
+    return __hiloint2double((int)(0x3FF00000u | (u >> 12)), (int)(u << 20)) - 1.0;
+}
+
+// One 128-word step at piece word n; dst = this lane's slot of the step's output (16 bytes for
+// u32, 32 bytes for f64: KIND = MTGP_U32 / MTGP_F64_01).
+template <uint32_t NW, int RC, int AC, int KIND, bool CK, bool TAIL>
 __device__ __forceinline__ void step6(const M6Ctx& p, const uint4 (&Hs)[S6<NW>::H], uint4& nw, uint4* dst,
                                       uint32_t n, uint32_t len, uint32_t* win_out, unsigned long long& sum,
                                       uint32_t& xr) {
@@ -110,7 +117,15 @@ __device__ __forceinline__ void step6(const M6Ctx& p, const uint4 (&Hs)[S6<NW>::
     }
     const uint32_t w0 = n + 4 * p.lane;  // piece word of o[0]
     if (!TAIL || w0 < len) {
-        __stcs(dst, make_uint4(o[0], o[1], o[2], o[3]));
+        if (KIND == MTGP_F64_01) {
+            // one 256-bit streaming store per lane (STG.E.EF.ENL2.256, sm_100): the warp's 1 KiB
+            // step in one contiguous instruction instead of two 16-byte-strided STG.128
+            asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "d"(u32_to_f64_01(o[0])),
+                         "d"(u32_to_f64_01(o[1])), "d"(u32_to_f64_01(o[2])), "d"(u32_to_f64_01(o[3]))
+                         : "memory");
+        } else {
+            __stcs(dst, make_uint4(o[0], o[1], o[2], o[3]));
+        }
         if (CK) {
 #if MTGP6_CK_WIDE
             // 64-bit sum on the FMA pipe: IMAD.WIDE.U32 sum = o * 1 + sum (the 1 is opaque)
@@ -141,7 +156,7 @@ __device__ __forceinline__ void shift1(uint4 (&Hs)[NH], const uint4& nw) {
     Hs[NH - 1] = nw;
 }
 
-template <uint32_t NW, int RC, int AC, bool CK>
+template <uint32_t NW, int RC, int AC, int KIND, bool CK>
 __device__ __forceinline__ void run6(const M6Ctx& p, uint4 (&Hs)[S6<NW>::H], uint32_t* optr, uint32_t len,
                                      uint32_t* win_out, unsigned long long& sum, uint32_t& xr) {
     using S = S6<NW>;
@@ -150,47 +165,49 @@ __device__ __forceinline__ void run6(const M6Ctx& p, uint4 (&Hs)[S6<NW>::H], uin
     // window while n + 128 + N <= len. The main loop runs H such steps per trip (the history
     // returns to its registers); the rest run the predicated tail variant.
     uint32_t m = 0;
-    uint4* dst = reinterpret_cast<uint4*>(optr) + p.lane;  // step m's slot: dst + 32 m
-    for (; (m + S::H) * kHalfWords + S::N <= len; m += S::H, dst += 32 * S::H) {
+    constexpr uint32_t V = KIND == MTGP_F64_01 ? 2 : 1;  // 16-byte vectors per lane per step
+    uint4* dst = reinterpret_cast<uint4*>(optr) + V * p.lane;  // step m's slot: dst + 32 V m
+    for (; (m + S::H) * kHalfWords + S::N <= len; m += S::H, dst += 32 * V * S::H) {
 #pragma unroll
         for (uint32_t k = 0; k < S::H; ++k) {
             uint4 nw;
-            step6<NW, RC, AC, CK, false>(p, Hs, nw, dst + 32 * k, (m + k) * kHalfWords, len, nullptr, sum, xr);
+            step6<NW, RC, AC, KIND, CK, false>(p, Hs, nw, dst + 32 * V * k, (m + k) * kHalfWords, len, nullptr, sum,
+                                               xr);
             shift1(Hs, nw);
         }
     }
-    for (; m < steps; ++m, dst += 32) {
+    for (; m < steps; ++m, dst += 32 * V) {
         uint4 nw;
-        step6<NW, RC, AC, CK, true>(p, Hs, nw, dst, m * kHalfWords, len, win_out, sum, xr);
+        step6<NW, RC, AC, KIND, CK, true>(p, Hs, nw, dst, m * kHalfWords, len, win_out, sum, xr);
         shift1(Hs, nw);
     }
 }
 
-template <uint32_t NW, int AC, bool CK>
+template <uint32_t NW, int AC, int KIND, bool CK>
 __device__ __forceinline__ void run6_rc(int rc, const M6Ctx& p, uint4 (&Hs)[S6<NW>::H], uint32_t* optr,
                                         uint32_t len, uint32_t* win_out, unsigned long long& sum, uint32_t& xr) {
     switch (rc) {
-        case 0: run6<NW, 0, AC, CK>(p, Hs, optr, len, win_out, sum, xr); break;
-        case 1: run6<NW, 1, AC, CK>(p, Hs, optr, len, win_out, sum, xr); break;
-        case 2: run6<NW, 2, AC, CK>(p, Hs, optr, len, win_out, sum, xr); break;
-        default: run6<NW, 3, AC, CK>(p, Hs, optr, len, win_out, sum, xr); break;
+        case 0: run6<NW, 0, AC, KIND, CK>(p, Hs, optr, len, win_out, sum, xr); break;
+        case 1: run6<NW, 1, AC, KIND, CK>(p, Hs, optr, len, win_out, sum, xr); break;
+        case 2: run6<NW, 2, AC, KIND, CK>(p, Hs, optr, len, win_out, sum, xr); break;
+        default: run6<NW, 3, AC, KIND, CK>(p, Hs, optr, len, win_out, sum, xr); break;
     }
 }
 
-template <uint32_t NW, int AC, bool CK>
+template <uint32_t NW, int AC, int KIND, bool CK>
 __device__ __forceinline__ void run6_ac(int ac, int rc, const M6Ctx& p, uint4 (&Hs)[S6<NW>::H], uint32_t* optr,
                                         uint32_t len, uint32_t* win_out, unsigned long long& sum, uint32_t& xr) {
     if constexpr (AC <= (int)S6<NW>::AC_MAX) {
         if (ac == AC)
-            run6_rc<NW, AC, CK>(rc, p, Hs, optr, len, win_out, sum, xr);
+            run6_rc<NW, AC, KIND, CK>(rc, p, Hs, optr, len, win_out, sum, xr);
         else
-            run6_ac<NW, AC + 1, CK>(ac, rc, p, Hs, optr, len, win_out, sum, xr);
+            run6_ac<NW, AC + 1, KIND, CK>(ac, rc, p, Hs, optr, len, win_out, sum, xr);
     }
 }
 
 }  // namespace
 
-template <uint32_t NW, bool CK>
+template <uint32_t NW, int KIND, bool CK>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, MTGP6_MIN_CTAS) mt_gen3_kernel(MtGenArgs a) {
     using S = S6<NW>;
     const uint32_t warp = threadIdx.x >> 5;
@@ -226,7 +243,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MTGP6_MIN_CTAS) mt_gen3_ker
         p.srcC1 = (lane + thr1) & 31;
         p.pC0 = lane < thr0;
         p.pC1 = lane < thr1;
-        uint32_t* optr = reinterpret_cast<uint32_t*>(a.out) + (size_t)pc.set * a.L + pc.offset;
+        // u32 words or doubles (2 words each): stream stride L samples, piece offset in samples
+        constexpr uint32_t kW = KIND == MTGP_F64_01 ? 2 : 1;
+        uint32_t* optr = reinterpret_cast<uint32_t*>(a.out) + kW * ((size_t)pc.set * a.L + pc.offset);
         const uint32_t len = (uint32_t)pc.len;
         const uint32_t* w0 = a.piece_win[pi];
         // history before step 0: half-step h, lane t, component c holds x_{128h + 4t + c - BASE}
@@ -248,7 +267,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MTGP6_MIN_CTAS) mt_gen3_ker
         }
         unsigned long long sum = 0;
         uint32_t xr = 0;
-        run6_ac<NW, 0, CK>(ac, rc, p, Hs, optr, len, win_out, sum, xr);
+        run6_ac<NW, 0, KIND, CK>(ac, rc, p, Hs, optr, len, win_out, sum, xr);
         if (CK) {
 #pragma unroll
             for (int s = 16; s > 0; s >>= 1) {
@@ -266,27 +285,38 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MTGP6_MIN_CTAS) mt_gen3_ker
 }
 
 bool mt_gen3_supports(uint32_t n, uint32_t min_gap, int kind) {
-    return kind == MTGP_U32 && n == 624 && min_gap >= 129;
+    return (kind == MTGP_U32 || kind == MTGP_F64_01) && n == 624 && min_gap >= 129;
 }
 
-cudaError_t launch_mt_gen3(uint32_t n, bool cksum, const MtGenArgs& a, cudaStream_t st) {
+template <int KIND, bool CK>
+static int mt3_occ() {
+    int c = 0;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, mt_gen3_kernel<624, KIND, CK>, kWarpsPerCta * 32, 0) ==
+                   cudaSuccess
+               ? c
+               : 0;
+}
+
+cudaError_t launch_mt_gen3(uint32_t n, int kind, bool cksum, const MtGenArgs& a, cudaStream_t st) {
     if (a.n_teams == 0) return cudaSuccess;
     if (n != 624) return cudaErrorInvalidValue;
     const uint32_t grid = (a.n_teams + kWarpsPerCta - 1) / kWarpsPerCta;
-    if (cksum)
-        mt_gen3_kernel<624, true><<<grid, kWarpsPerCta * 32, 0, st>>>(a);
-    else
-        mt_gen3_kernel<624, false><<<grid, kWarpsPerCta * 32, 0, st>>>(a);
+    const dim3 block(kWarpsPerCta * 32);
+    switch ((kind == MTGP_F64_01 ? 2 : kind == MTGP_U32 ? 0 : 4) + (cksum ? 1 : 0)) {
+        case 0: mt_gen3_kernel<624, MTGP_U32, false><<<grid, block, 0, st>>>(a); break;
+        case 1: mt_gen3_kernel<624, MTGP_U32, true><<<grid, block, 0, st>>>(a); break;
+        case 2: mt_gen3_kernel<624, MTGP_F64_01, false><<<grid, block, 0, st>>>(a); break;
+        case 3: mt_gen3_kernel<624, MTGP_F64_01, true><<<grid, block, 0, st>>>(a); break;
+        default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 
-int mt_gen3_ctas_per_sm(uint32_t n, bool cksum) {
+int mt_gen3_ctas_per_sm(uint32_t n, int kind, bool cksum) {
     if (n != 624) return 0;
-    int c = 0;
-    const cudaError_t e =
-        cksum ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, mt_gen3_kernel<624, true>, kWarpsPerCta * 32, 0)
-              : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, mt_gen3_kernel<624, false>, kWarpsPerCta * 32, 0);
-    return e == cudaSuccess ? c : 0;
+    if (kind == MTGP_U32) return cksum ? mt3_occ<MTGP_U32, true>() : mt3_occ<MTGP_U32, false>();
+    if (kind == MTGP_F64_01) return cksum ? mt3_occ<MTGP_F64_01, true>() : mt3_occ<MTGP_F64_01, false>();
+    return 0;
 }
 
 }  // namespace mtgpb

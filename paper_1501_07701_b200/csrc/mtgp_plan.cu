@@ -160,6 +160,10 @@ Planner::Planner(const std::vector<mtgp_mt_params>& sets, int num_sms) : impl_(n
 Planner::~Planner() = default;
 
 bool Planner::v2_supported() const { return impl_->v2; }
+bool Planner::mt3_supported(int kind, uint64_t L, const void* out) const {
+    return impl_->mt && impl_->v2 && mt_gen3_supports(impl_->N, impl_->mt_min_gap, kind) && L % 4 == 0 &&
+           (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+}
 void Planner::invalidate() {
     impl_->analyzed = false;
     impl_->jumps_ok = false;
@@ -389,13 +393,12 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     const bool reg_ok = !I.mt && r.L % 4 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 15) == 0;
     const bool v3_ok = I.M == 11213 && reg_ok;
     const bool v4_ok = v4_supports(I.M, r.kind) && reg_ok;
-    if (I.mt && r.kind == MTGP_F64_01) {
-        err = "the Engine::mt warp-team kernel has no f64 output";
+    // Engine::mt: mt_gen3 (register-resident, version 6) when the shape allows, else mt_gen2
+    const bool mt3_ok = mt3_supported(r.kind, r.L, r.out);
+    if (I.mt && r.kind == MTGP_F64_01 && !mt3_ok) {
+        err = "Engine::mt f64 output on the warp teams needs kernel 6's shape";
         return cudaSuccess;
     }
-    // Engine::mt: mt_gen3 (register-resident, version 6) when the shape allows, else mt_gen2
-    const bool mt3_ok = I.mt && mt_gen3_supports(I.N, I.mt_min_gap, r.kind) && r.L % 4 == 0 &&
-                        (reinterpret_cast<uintptr_t>(r.out) & 15) == 0;
     if (!I.mt && r.want_kernel >= 5) {
         err = "kernels 5 and 6 are Engine::mt kernels";
         return cudaSuccess;
@@ -419,7 +422,7 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     // v2 for request shapes the register kernels do not take (float kinds, L % 4 != 0, ...)
     const bool use_v3 = v3_ok && (r.want_kernel == 3 || (r.want_kernel == 0 && I.M == 11213));
     const bool use_v4 = !use_v3 && v4_ok && (r.want_kernel == 4 || (r.want_kernel == 0 && I.M != 11213));
-    const int cps = use_mt3  ? mt_gen3_ctas_per_sm(I.N, r.cksum)
+    const int cps = use_mt3  ? mt_gen3_ctas_per_sm(I.N, r.kind, r.cksum)
                     : I.mt   ? mt_gen2_ctas_per_sm(I.N, r.kind, r.cksum)
                     : use_v3 ? gen3_ctas_per_sm(r.kind, r.cksum)
                     : use_v4 ? gen4_ctas_per_sm(I.M, r.kind, r.cksum)
@@ -490,7 +493,8 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         ma.n = I.N;
         ma.pairs = r.L % 2 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 7) == 0;
         if (r.timing) r.timing->record(r.stream, &g0);
-        e = use_mt3 ? launch_mt_gen3(I.N, r.cksum, ma, r.stream) : launch_mt_gen2(r.kind, r.cksum, ma, r.stream);
+        e = use_mt3 ? launch_mt_gen3(I.N, r.kind, r.cksum, ma, r.stream)
+                    : launch_mt_gen2(r.kind, r.cksum, ma, r.stream);
         if (e != cudaSuccess) return e;
         r.version = use_mt3 ? 6 : 5;
     } else {

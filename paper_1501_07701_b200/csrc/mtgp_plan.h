@@ -43,6 +43,8 @@ public:
     Planner(const std::vector<mtgp_mt_params>& sets, int num_sms);
     ~Planner();
     bool v2_supported() const;
+    // Engine::mt: the register-resident team kernel (version 6) takes this request shape
+    bool mt3_supported(int kind, uint64_t L, const void* out) const;
     // forget per-stream algebra and cached plans (after a state restore)
     void invalidate();
     // run the per-stream annihilator analysis now, at the current window (no-op if done). An

@@ -305,3 +305,33 @@ def test_mt_gen3_shape_limits():
         with pytest.raises(mtgp.MtgpInvalidArgument):
             ctx.fill_u32(4096)
     assert np.array_equal(w[1], oracle_py.ref_fill(4096, 2, _st12(edge)))
+
+
+@pytest.mark.gpu
+def test_mt_gen3_f64_with_jumps_vs_reference():
+    """Generator::next_f64_01 (generator.hpp:39-41) on the register-resident teams: jumped pieces
+    and a continuation, bit-exact doubles; checksums cover the u32 draws; the CTA-per-stream
+    kernel (MTGP_OPT_KERNEL=1) agrees."""
+    sts = [mtgp.mt19937_status(), _rand_status(19937, 300, 4)]
+    seeds = [5489, 77]
+    lens = [100_000, 404]
+    res = {}
+    for kern in (0, 1):
+        with mtgp.MtContext(sts, seeds) as ctx:
+            ctx.set_option(mtgp.OPT_KERNEL, kern)
+            ctx.set_option(mtgp.OPT_MIN_PIECE_WORDS, 1 << 12)
+            ds, kv = [], []
+            for L in lens:
+                ds.append(ctx.generate_host(mtgp.F64_01, L))
+                kv.append(ctx.last_plan()[2])
+            res[kern] = (ds, ctx.checksums(), kv)
+    assert res[0][2] == [6, 6] and res[1][2] == [1, 1]
+    total = sum(lens)
+    for s in range(2):
+        u = oracle_py.ref_fill(total, seeds[s], _st12(sts[s]))
+        got = np.concatenate([d[s] for d in res[0][0]])
+        assert np.array_equal(got, u.astype(np.float64) * (1.0 / 4294967296.0))
+        c = oracle_py.cksum(u)
+        assert res[0][1][s] == (c["sum64"], c["xor32"], total)
+    for a, b in zip(res[0][0], res[1][0]):
+        assert np.array_equal(a, b)
