@@ -202,8 +202,8 @@ int mtgp_mt_validate_params(const mtgp_mt_params* p);
  * n - m >= 32, generation and long skips use the jump-ahead planner with warp teams (kernel
  * version 5 in mtgp_last_plan; version 6, the register-resident team kernel, for n = 624 with
  * every n - m >= 129, u32 or f64 output, words_per_stream % 4 == 0 and 16-byte aligned output);
- * otherwise (and for MTGP_F64_01 outside version 6's shape) one CTA per stream. MTGP_OPT_KERNEL 5 / 6 force the team
- * kernel, 1 the CTA-per-stream one.
+ * otherwise (and for MTGP_F64_01 outside version 6's shape) one CTA per stream.
+ * MTGP_OPT_KERNEL 5 / 6 force the team kernel, 1 the CTA-per-stream one.
  */
 int mtgp_mt_ctx_create(mtgp_ctx** out, int device, const mtgp_mt_params* sets, uint32_t n_sets,
                        const uint32_t* seeds, void* stream);
