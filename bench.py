@@ -87,16 +87,19 @@ class ClockSampler:
 
     def _nvml_loop(self):
         import pynvml
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(self.nv, pynvml.NVML_CLOCK_SM)
+        pw, i = None, 0
         while not self.stop_flag:
-            try:
+            try:  # SM clock + reasons every 5 ms; power (a slower query) every 4th sample
                 mhz = pynvml.nvmlDeviceGetClockInfo(self.nv, pynvml.NVML_CLOCK_SM)
-                mx = pynvml.nvmlDeviceGetMaxClockInfo(self.nv, pynvml.NVML_CLOCK_SM)
                 rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.nv)
-                pw = pynvml.nvmlDeviceGetPowerUsage(self.nv) / 1000.0
+                if i % 4 == 0:
+                    pw = pynvml.nvmlDeviceGetPowerUsage(self.nv) / 1000.0
                 self.nvml_rows.append((mhz, mx, rs, pw))
             except Exception:  # noqa: BLE001
                 pass
-            time.sleep(0.01)
+            i += 1
+            time.sleep(0.005)
 
     def start(self):
         try:
@@ -143,8 +146,8 @@ class ClockSampler:
             loaded = [v for v in sm if smax and v > 0.5 * smax] or sm
             return {"sm_mhz": float(np.median(loaded)) if loaded else None, "sm_max_mhz": smax,
                     "sm_mhz_min": float(min(loaded)) if loaded else None, "reasons": sorted(reasons),
-                    "power_w_max": max((r[3] for r in self.nvml_rows), default=None),
-                    "samples": len(sm), "source": "nvml, 10 ms"}
+                    "power_w_max": max((r[3] for r in self.nvml_rows if r[3] is not None), default=None),
+                    "samples": len(sm), "source": "nvml, 5 ms"}
         if self.proc:
             self.proc.terminate()
             try:
