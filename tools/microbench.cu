@@ -1,7 +1,8 @@
 // microbench.cu -- B200 facts the MTGP32 kernel design depends on (run under gpurun).
 //   1. HBM write-only peak: coalesced STG.128 grid-stride stores, and cudaMemsetAsync
 //   2. MIO pipe: SHFL.IDX and LDS.128 / LDS.32 throughput per SM per clock
-//   3. STG.128 with a 32-byte lane stride (a lane owning 8 consecutive words) vs contiguous
+//   3. STG.128 with a 32-byte lane stride (a lane owning 8 consecutive words) vs contiguous,
+//      and the same 8 words as one 256-bit store (sm_100)
 //   4. TMA bulk stores (cp.async.bulk.global.shared::cta, 16 KB per op) from a double-buffered
 //      shared-memory stage -- the store path north_star names, against direct STG.128
 //
@@ -36,6 +37,19 @@ __global__ void store_stride32(uint4* __restrict__ p, size_t n4, uint32_t v) {
         uint4* q = p + c * 64 + lane * 2;
         __stcs(q, make_uint4(v, lane, v, v));
         __stcs(q + 1, make_uint4(v, lane, v + 1, v));
+    }
+}
+
+__global__ void store_256(uint4* __restrict__ p, size_t n4, uint32_t v) {
+    // lane owns 8 words (32 B) as ONE 256-bit store (STG.E.EF.ENL2.256, sm_100): 1 KB per warp instr
+    const size_t warp = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
+    for (size_t c = warp; c * 64 < n4; c += nwarps) {
+        uint4* q = p + c * 64 + lane * 2;
+        asm volatile("st.global.cs.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(q), "r"(v), "r"(lane),
+                     "r"(v), "r"(v), "r"(v), "r"(lane), "r"(v + 1), "r"(v)
+                     : "memory");
     }
 }
 
@@ -128,20 +142,23 @@ int main() {
     const int sms = prop.multiProcessorCount;
 
     // 1. write peak
-    for (int pass = 0; pass < 2; ++pass) {
+    for (int pass = 0; pass < 3; ++pass) {
         float best = 1e30f;
         for (int r = 0; r < 5; ++r) {
             CK(cudaEventRecord(a));
             if (pass == 0)
                 store_peak<<<sms * 8, 512>>>(buf, bytes / 16, r);
-            else
+            else if (pass == 1)
                 store_stride32<<<sms * 8, 512>>>(buf, bytes / 16, r);
+            else
+                store_256<<<sms * 8, 512>>>(buf, bytes / 16, r);
             CK(cudaEventRecord(b));
             CK(cudaEventSynchronize(b));
             CK(cudaEventElapsedTime(&ms, a, b));
             if (ms < best) best = ms;
         }
-        printf(", \"%s_GBps\": %.1f", pass == 0 ? "stg128_coalesced" : "stg128_stride32", bytes / (best * 1e6));
+        printf(", \"%s_GBps\": %.1f", pass == 0 ? "stg128_coalesced" : pass == 1 ? "stg128_stride32" : "stg256_coalesced",
+               bytes / (best * 1e6));
     }
     {
         float best = 1e30f;
