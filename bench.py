@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-words-per-thread", type=int, default=1 << 28)
+    ap.add_argument("--as-rank", type=int, default=None,
+                    help="single process: generate rank R's shard of a multi-GPU run (its parameter sets / seeds), "
+                         "to time every rank's workload alone on one GPU")
     return ap.parse_args()
 
 
@@ -257,12 +260,17 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     mexp, kind, L_step, label = CONFIGS[args.config]
     S = args.sets
+    shard_rank = rank
+    if args.as_rank is not None:
+        if world > 1:
+            raise SystemExit("--as-rank is for single-process runs")
+        shard_rank = args.as_rank
     is_mt = args.config in MT_CONFIGS
     if is_mt:  # MT19937 statuses, distinct seeds per stream (and per rank)
         sets = [mtgp.mt19937_status()] * S
-        seeds = [5489 + rank * S + i for i in range(S)]
+        seeds = [5489 + shard_rank * S + i for i in range(S)]
     else:
-        sets = shard.sets_for_rank(mexp, S, rank)
+        sets = shard.sets_for_rank(mexp, S, shard_rank)
         seeds = [1] * S
 
     def make_ctx(ss, sd):
@@ -428,10 +436,13 @@ def main():
             "config": {"workload": label, "sets_per_gpu": S, "seed": 1, "words_per_set_per_step": L_step,
                        "calls_per_step": calls, "kernel": f"v{kver}", "pieces_per_call": pieces,
                        "checksums_fused": not args.no_checksum,
+                       **({"as_rank": shard_rank, "global_set_ids": [shard_rank * S, (shard_rank + 1) * S]}
+                          if args.as_rank is not None else {}),
                        "checksums_gathered_streams": gathered_streams,
                        "l2": "output 4*S*L/calls bytes per call >> 126 MB L2; no flush needed",
                        "parameter_sets": ("MT19937 (mt19937_params, proj/src/params.cpp:63-77)" if is_mt
                                           else "synthetic (uncertified period)" if mexp != 11213 or S > 200
+                                          or shard_rank > 0
                                           else "cuRAND MTGP32-11213 (certified)" if world == 1
                                           else "rank 0: cuRAND MTGP32-11213 (certified); ranks 1..N-1: synthetic "
                                                "MTGP32-11213 (uncertified period)")},

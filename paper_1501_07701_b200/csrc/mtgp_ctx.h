@@ -37,6 +37,7 @@ struct mtgp_ctx {
     // options
     bool cksum = true;
     int kernel = 0;
+    int jump_mode = 0;  // MTGP_OPT_JUMP
     uint32_t max_pieces = 0;
     uint64_t min_piece_words = 1ull << 21;
     bool timing = false;

@@ -1,0 +1,241 @@
+// mtgp_jump.cu -- jump-ahead windows by a transposed-Karatsuba middle product (large N).
+//
+// A jump computes the window at offset o of a stream: y_j = XOR_{i : q_i = 1} x_{i+j}, j < N,
+// where q = x^(o - t0) mod P (mtgp_plan.cu) and x is the stream's state-word prefix from the
+// reference point t0. jump_flat_kernel (mtgp_v2.cu) does this directly: N * M word operations
+// per piece, which at MTGP32-44497 (N = 1391, M = 44497) is 16% of a bench step.
+//
+// Here the output range is padded to n_out = 384 * 2^d >= N (d = 1 for N <= 768, 2 for
+// N <= 1536) and q is cut into B blocks of n_out bits, so y = XOR_b MP(Q_b, x[b n_out ..]),
+// MP(a, z)_j = XOR_i a_i z_{i+j} being a middle product of size n_out. Each MP is split d
+// times by the transposed Karatsuba identity (for halves a0, a1 of a and z windows Z0, Z1, Z2
+// at offsets 0, m/2, m):
+//     y_lo = P ^ L,  y_hi = P ^ H,  P = MP(a0 ^ a1, Z1),  L = MP(a0, Z0 ^ Z1),  H = MP(a1, Z1 ^ Z2)
+// so one size-n_out product becomes 3^d size-384 "leaf" products instead of 4^d: 0.75x the
+// word operations at d = 1, 0.56x at d = 2. Everything is GF(2)-linear, so the leaves are
+// summed over the blocks first and recombined once per piece.
+//
+//   jump_ztrans_kernel  per prefix row (stream): the leaf z vectors of every block, each an
+//                       XOR of up to 2^d shifted prefix windows (shared by all pieces of the
+//                       stream).
+//   jump_leaf_kernel    one warp per (piece, leaf): the flat kernel's inner loop (lane keeps
+//                       12 outputs, q walked two bits at a time, warp-uniform branches) over
+//                       the leaf's q words, which are XORs of up to 2^d raw q words.
+//   jump_combine_kernel per piece: window word j = XOR of the 2^d leaf outputs of its quarter.
+#include <algorithm>
+#include <vector>
+
+#include "mtgp_jump.cuh"
+
+namespace mtgpb {
+
+#define FULL 0xffffffffu
+
+namespace {
+
+constexpr int kJ = 12;                 // outputs per lane
+constexpr uint32_t kH = 32 * kJ;       // leaf size (outputs per warp) = 384
+constexpr uint32_t kZ = 2 * kH;        // leaf z vector words (2h - 1, padded)
+constexpr uint32_t kHq = kH / 32;      // q words per leaf block = 12
+constexpr int kLeafWarps = 4;
+
+__global__ void jump_ztrans_kernel(const JumpArgs a, const KaraPlan k, uint32_t n_rows, uint4* __restrict__ zbuf) {
+    // one thread per 4 output words: index over (row, block, leaf, t4)
+    const uint64_t per_row = (uint64_t)k.blocks * k.n_leaf * (kZ / 4);
+    const uint64_t total = per_row * n_rows;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t row = (uint32_t)(i / per_row);
+        const uint32_t r = (uint32_t)(i % per_row);
+        const uint32_t t4 = r % (kZ / 4);
+        const uint32_t bl = r / (kZ / 4);
+        const uint32_t s = bl % k.n_leaf, b = bl / k.n_leaf;
+        const uint4* x4 = reinterpret_cast<const uint4*>(a.pre + (size_t)row * a.pre_stride + a.pre_off);
+        const uint32_t base = b * k.n_out + 4 * t4;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        for (uint32_t u = 0; u < k.nz[s]; ++u) {
+            const uint4 g = __ldg(x4 + ((base + k.oz[s][u]) >> 2));
+            v.x ^= g.x;
+            v.y ^= g.y;
+            v.z ^= g.z;
+            v.w ^= g.w;
+        }
+        zbuf[i] = v;
+    }
+}
+
+__global__ void __launch_bounds__(kLeafWarps * 32) jump_leaf_kernel(const JumpArgs a, const KaraPlan k,
+                                                                    const uint4* __restrict__ zbuf,
+                                                                    uint4* __restrict__ leaf_out) {
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t unit = blockIdx.x * kLeafWarps + warp;
+    const uint32_t job = unit / k.n_leaf, s = unit % k.n_leaf;
+    if (job >= a.n_jobs) return;
+    const JumpJob jb = a.jobs[job];
+    const uint32_t* q = a.q + (size_t)jb.q * a.q_words;
+    const uint32_t jl = kJ * lane;
+    const uint4* zrow = zbuf + (size_t)jb.row * k.blocks * k.n_leaf * (kZ / 4);
+    const uint32_t nq = k.nq[s];
+    uint32_t acc[kJ];
+#pragma unroll
+    for (int i = 0; i < kJ; ++i) acc[i] = 0;
+    // lanes 0..11 hold the leaf's q words of the current block (XOR of nq raw q words)
+    auto load_q = [&](uint32_t b) -> uint32_t {
+        uint32_t v = 0;
+        if (lane < kHq)
+            for (uint32_t u = 0; u < nq; ++u) {
+                const uint32_t idx = b * k.blk_qwords + k.oq[s][u] + lane;
+                if (idx < a.q_words) v ^= __ldg(q + idx);
+            }
+        return v;
+    };
+    uint32_t qnext = load_q(0);
+    for (uint32_t b = 0; b < k.blocks; ++b) {
+        const uint32_t qmine = qnext;
+        if (b + 1 < k.blocks) qnext = load_q(b + 1);
+        const uint4* z4 = zrow + (size_t)(b * k.n_leaf + s) * (kZ / 4);
+        for (uint32_t iw = 0; iw < kHq; ++iw) {
+            const uint32_t qw = __shfl_sync(FULL, qmine, iw);
+            if (qw == 0) continue;
+            const uint32_t base4 = (iw * 32 + jl) >> 2;
+            uint32_t w[kJ + 32];
+#pragma unroll
+            for (int v = 0; v < (kJ + 32) / 4; ++v) {
+                const uint4 g = __ldg(z4 + base4 + v);
+                w[4 * v] = g.x;
+                w[4 * v + 1] = g.y;
+                w[4 * v + 2] = g.z;
+                w[4 * v + 3] = g.w;
+            }
+#pragma unroll
+            for (int bb = 0; bb < 32; bb += 2) {
+                const uint32_t pat = (qw >> bb) & 3u;
+                if (pat == 1) {
+#pragma unroll
+                    for (int i = 0; i < kJ; ++i) acc[i] ^= w[bb + i];
+                } else if (pat == 2) {
+#pragma unroll
+                    for (int i = 0; i < kJ; ++i) acc[i] ^= w[bb + 1 + i];
+                } else if (pat == 3) {
+#pragma unroll
+                    for (int i = 0; i < kJ; ++i) acc[i] ^= w[bb + i] ^ w[bb + 1 + i];
+                }
+            }
+        }
+    }
+    uint4* dst = leaf_out + ((size_t)job * k.n_leaf + s) * (kH / 4) + jl / 4;
+#pragma unroll
+    for (int v = 0; v < kJ / 4; ++v) dst[v] = make_uint4(acc[4 * v], acc[4 * v + 1], acc[4 * v + 2], acc[4 * v + 3]);
+}
+
+__global__ void jump_combine_kernel(const JumpArgs a, const KaraPlan k, uint32_t N, const uint32_t* __restrict__ leaf_out) {
+    const uint32_t job = blockIdx.y;
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    const JumpJob jb = a.jobs[job];
+    const uint32_t c = t / kH, tt = t % kH;
+    const uint32_t* lo = leaf_out + (size_t)job * k.n_leaf * kH + tt;
+    uint32_t v = 0;
+    for (uint32_t u = 0; u < k.n_comb; ++u) v ^= lo[(size_t)k.comb[c][u] * kH];
+    a.piece_win[(size_t)jb.piece * N + t] = v;
+}
+
+}  // namespace
+
+bool kara_plan(uint32_t N, uint32_t q_words, int depth_override, KaraPlan& k) {
+    int d = depth_override >= 0 ? depth_override : (N <= kH ? 0 : N <= 2 * kH ? 1 : 2);
+    if (d <= 0 || d > 2 || (kH << d) < N) return false;
+    k = KaraPlan{};
+    k.depth = (uint32_t)d;
+    k.n_out = kH << d;
+    k.blk_qwords = k.n_out / 32;
+    k.blocks = (32 * q_words + k.n_out - 1) / k.n_out;
+    // leaves: base-3 digits s_1..s_d (level 1 most significant), P = 0, L = 1, H = 2.
+    // Offsets (in words) of the z windows XORed into a leaf's z vector and of the raw q words
+    // XORed into its q words; each level halves the size m.
+    k.n_leaf = 1;
+    for (int i = 0; i < d; ++i) k.n_leaf *= 3;
+    for (uint32_t s = 0; s < k.n_leaf; ++s) {
+        std::vector<uint32_t> oz{0}, oq{0};
+        uint32_t m = k.n_out, rest = s, div = k.n_leaf / 3;
+        auto sym = [](std::vector<uint32_t> v) {  // multiset mod 2
+            std::sort(v.begin(), v.end());
+            std::vector<uint32_t> o;
+            for (size_t i = 0; i < v.size();) {
+                size_t j = i;
+                while (j < v.size() && v[j] == v[i]) ++j;
+                if ((j - i) & 1) o.push_back(v[i]);
+                i = j;
+            }
+            return o;
+        };
+        for (int lev = 0; lev < d; ++lev) {
+            const uint32_t dig = rest / div;
+            rest %= div;
+            div = div ? div / 3 : 0;
+            const uint32_t half = m / 2;
+            std::vector<uint32_t> nz, nqv;
+            if (dig == 0) {  // P = MP(a0 ^ a1, Z1)
+                for (uint32_t o : oz) nz.push_back(o + half);
+                for (uint32_t o : oq) nqv.push_back(o), nqv.push_back(o + half);
+            } else if (dig == 1) {  // L = MP(a0, Z0 ^ Z1)
+                for (uint32_t o : oz) nz.push_back(o), nz.push_back(o + half);
+                nqv = oq;
+            } else {  // H = MP(a1, Z1 ^ Z2)
+                for (uint32_t o : oz) nz.push_back(o + half), nz.push_back(o + m);
+                for (uint32_t o : oq) nqv.push_back(o + half);
+            }
+            oz = sym(nz);
+            oq = sym(nqv);
+            m = half;
+        }
+        if (oz.size() > 4 || oq.size() > 4) return false;
+        k.nz[s] = (uint32_t)oz.size();
+        k.nq[s] = (uint32_t)oq.size();
+        for (size_t i = 0; i < oz.size(); ++i) k.oz[s][i] = oz[i];
+        for (size_t i = 0; i < oq.size(); ++i) k.oq[s][i] = oq[i] / 32;
+    }
+    // output quarter c (d bits, level 1 most significant): XOR of the leaves whose digit at
+    // every level is P or (bit ? H : L)
+    k.n_comb = 1u << d;
+    for (uint32_t c = 0; c < (1u << d); ++c)
+        for (uint32_t pick = 0; pick < (1u << d); ++pick) {
+            uint32_t s = 0;
+            for (int lev = 0; lev < d; ++lev) {
+                const uint32_t bit = (c >> (d - 1 - lev)) & 1u;
+                const uint32_t dig = ((pick >> (d - 1 - lev)) & 1u) ? (bit ? 2u : 1u) : 0u;
+                s = s * 3 + dig;
+            }
+            k.comb[c][pick] = s;
+        }
+    return true;
+}
+
+uint32_t kara_prefix_words(const KaraPlan& k) {
+    // the last block's windows reach x[(B + 1) n_out - 1]
+    return (k.blocks + 1) * k.n_out;
+}
+
+size_t kara_zbuf_words(const KaraPlan& k, uint32_t n_rows) { return (size_t)n_rows * k.blocks * k.n_leaf * kZ; }
+size_t kara_leaf_words(const KaraPlan& k, uint32_t n_jobs) { return (size_t)n_jobs * k.n_leaf * kH; }
+
+cudaError_t launch_jump_kara(const JumpArgs& a, const KaraPlan& k, uint32_t N, uint32_t n_rows, uint32_t* zbuf,
+                             uint32_t* leaf_out, cudaStream_t st) {
+    if (a.n_jobs == 0 || n_rows == 0) return cudaSuccess;
+    {
+        const uint64_t total = (uint64_t)n_rows * k.blocks * k.n_leaf * (kZ / 4);
+        const uint32_t grid = (uint32_t)std::min<uint64_t>((total + 255) / 256, 148u * 16u);
+        jump_ztrans_kernel<<<grid, 256, 0, st>>>(a, k, n_rows, reinterpret_cast<uint4*>(zbuf));
+    }
+    {
+        const uint32_t units = a.n_jobs * k.n_leaf;
+        jump_leaf_kernel<<<(units + kLeafWarps - 1) / kLeafWarps, kLeafWarps * 32, 0, st>>>(
+            a, k, reinterpret_cast<const uint4*>(zbuf), reinterpret_cast<uint4*>(leaf_out));
+    }
+    {
+        const dim3 grid((N + 255) / 256, a.n_jobs);
+        jump_combine_kernel<<<grid, 256, 0, st>>>(a, k, N, leaf_out);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace mtgpb

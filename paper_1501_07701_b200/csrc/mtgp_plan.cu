@@ -18,6 +18,7 @@
 
 #include "gf2.h"
 #include "mtgp_plan.h"
+#include "mtgp_jump.cuh"
 #include "mtgp_v2.cuh"
 #include "sha1.h"
 
@@ -100,19 +101,28 @@ struct PlannerImpl {
     uint32_t q_words = 0;
     uint32_t pre_len = 0;
 
-    DevBuf d_pieces, d_teams, d_pwin_ptrs, d_pwin, d_q, d_pre, d_rows, d_joboff, d_jobs, d_win_next, d_all_rows;
+    // jump algorithm: the Karatsuba middle product (mtgp_jump.cu) for N > 384 unless forced flat
+    int jump_mode = 0;
+    bool kara_ok = false;
+    KaraPlan kara;
+
+    DevBuf d_pieces, d_teams, d_pwin_ptrs, d_pwin, d_q, d_pre, d_rows, d_joboff, d_jobs, d_win_next, d_all_rows,
+        d_zbuf, d_leaf;
 
     ~PlannerImpl() {
         for (DevBuf* b : {&d_pieces, &d_teams, &d_pwin_ptrs, &d_pwin, &d_q, &d_pre, &d_rows, &d_joboff, &d_jobs,
-                          &d_win_next, &d_all_rows})
+                          &d_win_next, &d_all_rows, &d_zbuf, &d_leaf})
             b->release();
     }
+    void init_jump() { kara_ok = kara_plan(N, (M + 31) / 32, -1, kara); }
+    bool use_kara() const { return kara_ok && jump_mode == 0; }
 
-    // words the jump kernel stages per row (from x_{t0})
+    // words the jump kernels read per row (from x_{t0})
     uint32_t prefix_len() const {
         const uint32_t qw = (M + 31) / 32;
         const uint32_t jblk = 32 * 12;
-        const uint32_t need = 32 * qw + jblk * ((N + jblk - 1) / jblk) + 36;
+        uint32_t need = 32 * qw + jblk * ((N + jblk - 1) / jblk) + 36;
+        if (kara_ok) need = std::max(need, kara_prefix_words(kara) + 36);
         return (need + 31) & ~31u;
     }
     // words the prefix kernel generates per row (x_0 .. ), rows 128-byte aligned
@@ -126,7 +136,13 @@ struct PlannerImpl {
         return mt ? launch_mt_prefix(static_cast<const DevMtParams*>(params), win, rows, n_rows, N, pre, len, st)
                   : launch_prefix(static_cast<const DevParams*>(params), win, rows, n_rows, N, pre, len, st);
     }
-    cudaError_t jump(const JumpArgs& a, uint32_t n_rows, cudaStream_t st) const {
+    cudaError_t jump(const JumpArgs& a, uint32_t n_rows, cudaStream_t st) {
+        if (use_kara()) {
+            cudaError_t e;
+            if ((e = d_zbuf.ensure(4 * kara_zbuf_words(kara, n_rows))) != cudaSuccess) return e;
+            if ((e = d_leaf.ensure(4 * kara_leaf_words(kara, a.n_jobs))) != cudaSuccess) return e;
+            return launch_jump_kara(a, kara, N, n_rows, d_zbuf.as<uint32_t>(), d_leaf.as<uint32_t>(), st);
+        }
         return mt ? launch_jump_rt(a, N, st) : launch_jump(M, a, n_rows, st);
     }
     cudaError_t build_plan(uint64_t L, uint32_t T, uint64_t min_piece, std::string& err);
@@ -142,6 +158,7 @@ Planner::Planner(const std::vector<mtgp_params>& sets, int num_sms) : impl_(new 
     impl_->v2 = v2_supports(impl_->M);
     for (const auto& p : sets)
         if (p.pos + kStepWords > impl_->N) impl_->v2 = false;  // needs N - pos >= 256
+    impl_->init_jump();
 }
 Planner::Planner(const std::vector<mtgp_mt_params>& sets, int num_sms) : impl_(new PlannerImpl) {
     impl_->mt = true;
@@ -156,7 +173,9 @@ Planner::Planner(const std::vector<mtgp_mt_params>& sets, int num_sms) : impl_(n
         if (p.mexp != impl_->M || p.n != impl_->N || p.n - p.m < 32) impl_->v2 = false;
         impl_->mt_min_gap = std::min(impl_->mt_min_gap, p.n - p.m);
     }
+    impl_->init_jump();
 }
+void Planner::set_jump_mode(int mode) { impl_->jump_mode = mode; }
 Planner::~Planner() = default;
 
 bool Planner::v2_supported() const { return impl_->v2; }
