@@ -87,7 +87,8 @@ typedef struct mtgp_ctx mtgp_ctx;
                                    /* (shared-memory ring), 3 = v3 (register ring, mexp 11213),   */
                                    /* 4 = v4 (register ring for any supported exponent);          */
                                    /* Engine::mt contexts: 5 = warp teams, shared-memory rings,   */
-                                   /* 6 = warp teams, register-resident (n = 624)                 */
+                                   /* 6 = warp teams, register-resident (n = 624);                */
+                                   /* 7 = v5 (v3 with 8 words per lane and 256-bit stores)        */
 #define MTGP_OPT_MAX_PIECES 3      /* cap on jump-ahead pieces per call (0 = auto)                  */
 #define MTGP_OPT_MIN_PIECE_WORDS 4 /* minimum words per jump-ahead piece (default 1<<21)            */
 #define MTGP_OPT_TIMING 5          /* 0/1: record CUDA events around every generation kernel        */

@@ -285,7 +285,7 @@ int mtgp_set_option(mtgp_ctx* ctx, int option, int64_t value) {
     switch (option) {
         case MTGP_OPT_CHECKSUM: ctx->cksum = value != 0; return MTGP_OK;
         case MTGP_OPT_KERNEL:
-            if (value < 0 || value > 6) return fail(MTGP_EINVAL, "kernel must be 0 (auto) or 1 .. 6");
+            if (value < 0 || value > 7) return fail(MTGP_EINVAL, "kernel must be 0 (auto) or 1 .. 7");
             ctx->kernel = (int)value;
             return MTGP_OK;
         case MTGP_OPT_MAX_PIECES:

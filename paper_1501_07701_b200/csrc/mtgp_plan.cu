@@ -300,13 +300,13 @@ cudaError_t PlannerImpl::build_plan(uint64_t L, uint32_t T, uint64_t min_piece, 
         }
     } else {
         // Split the concatenation of all streams into `want` equal ranges cut at stream
-        // boundaries; cuts are multiples of 4 words (16-byte aligned pieces), never inside a
+        // boundaries; cuts are multiples of 8 words (32-byte aligned pieces), never inside a
         // stream that cannot be jumped, and never in (0, t0) of a stream (jumps start at x_{t0}).
         std::vector<uint64_t> cut(want + 1);
         cut[0] = 0;
         cut[want] = W;
         for (uint64_t g = 1; g < want; ++g) {
-            uint64_t c = (W * g / want) & ~3ull;
+            uint64_t c = (W * g / want) & ~7ull;
             const uint64_t s = c / L, off = c % L;
             if (off && !set_ok[s]) c = (off < L / 2) ? s * L : (s + 1) * L;
             else if (off && off < t0) c = s * L + t0;
@@ -411,6 +411,8 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     // 16-byte aligned output, L % 4 == 0 (piece offsets are multiples of 4 by construction)
     const bool reg_ok = !I.mt && r.L % 4 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 15) == 0;
     const bool v3_ok = I.M == 11213 && reg_ok;
+    // v5 (gen3 with 8 consecutive words per lane, one 256-bit store per step): 32-byte pieces
+    const bool v5_ok = v3_ok && r.L % 8 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 31) == 0 && I.t0 % 8 == 0;
     const bool v4_ok = v4_supports(I.M, r.kind) && reg_ok;
     // Engine::mt: mt_gen3 (register-resident, version 6) when the shape allows, else mt_gen2
     const bool mt3_ok = mt3_supported(r.kind, r.L, r.out);
@@ -418,8 +420,16 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         err = "Engine::mt f64 output on the warp teams needs kernel 6's shape";
         return cudaSuccess;
     }
-    if (!I.mt && r.want_kernel >= 5) {
+    if (!I.mt && (r.want_kernel == 5 || r.want_kernel == 6)) {
         err = "kernels 5 and 6 are Engine::mt kernels";
+        return cudaSuccess;
+    }
+    if (I.mt && r.want_kernel == 7) {
+        err = "kernel 7 is an MTGP32-11213 kernel";
+        return cudaSuccess;
+    }
+    if (r.want_kernel == 7 && !v5_ok) {
+        err = "kernel v5 needs mexp 11213, words_per_stream % 8 == 0 and 32-byte aligned output";
         return cudaSuccess;
     }
     if (r.want_kernel == 6 && !mt3_ok) {
@@ -439,10 +449,12 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     // auto: v3 for 11213; v4 (the same register-resident design, templated on N) for 23209 and
     // 44497, where it beats the shared-memory ring by 18% / 27% (profiles/r1_v4_sweep.jsonl);
     // v2 for request shapes the register kernels do not take (float kinds, L % 4 != 0, ...)
-    const bool use_v3 = v3_ok && (r.want_kernel == 3 || (r.want_kernel == 0 && I.M == 11213));
-    const bool use_v4 = !use_v3 && v4_ok && (r.want_kernel == 4 || (r.want_kernel == 0 && I.M != 11213));
+    const bool use_v5 = v5_ok && r.want_kernel == 7;
+    const bool use_v3 = !use_v5 && v3_ok && (r.want_kernel == 3 || (r.want_kernel == 0 && I.M == 11213));
+    const bool use_v4 = !use_v5 && !use_v3 && v4_ok && (r.want_kernel == 4 || (r.want_kernel == 0 && I.M != 11213));
     const int cps = use_mt3  ? mt_gen3_ctas_per_sm(I.N, r.kind, r.cksum)
                     : I.mt   ? mt_gen2_ctas_per_sm(I.N, r.kind, r.cksum)
+                    : use_v5 ? gen5_ctas_per_sm(r.kind, r.cksum)
                     : use_v3 ? gen3_ctas_per_sm(r.kind, r.cksum)
                     : use_v4 ? gen4_ctas_per_sm(I.M, r.kind, r.cksum)
                              : gen_ctas_per_sm(I.M, r.kind, r.cksum);
@@ -528,11 +540,12 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         ga.L = r.L;
         ga.ck = r.ck;
         if (r.timing) r.timing->record(r.stream, &g0);
-        e = use_v3   ? launch_gen3(r.kind, r.cksum, ga, r.stream)
+        e = use_v5   ? launch_gen5(r.kind, r.cksum, ga, r.stream)
+            : use_v3 ? launch_gen3(r.kind, r.cksum, ga, r.stream)
             : use_v4 ? launch_gen4(I.M, r.kind, r.cksum, ga, r.stream)
                      : launch_gen(I.M, r.kind, r.cksum, ga, r.stream);
         if (e != cudaSuccess) return e;
-        r.version = use_v3 ? 3 : use_v4 ? 4 : 2;
+        r.version = use_v5 ? 7 : use_v3 ? 3 : use_v4 ? 4 : 2;
     }
     if (r.timing) {
         r.timing->record(r.stream, &g1);
