@@ -18,9 +18,10 @@
 //   jump_ztrans_kernel  per prefix row (stream): the leaf z vectors of every block, each an
 //                       XOR of up to 2^d shifted prefix windows (shared by all pieces of the
 //                       stream).
+//   jump_qleaf_kernel   per piece: every leaf's q words (XORs of up to 2^d raw q words).
 //   jump_leaf_kernel    one warp per (piece, leaf): the flat kernel's inner loop (lane keeps
 //                       12 outputs, q walked two bits at a time, warp-uniform branches) over
-//                       the leaf's q words, which are XORs of up to 2^d raw q words.
+//                       the leaf's B * 12 q words.
 //   jump_combine_kernel per piece: window word j = XOR of the 2^d leaf outputs of its quarter.
 #include <algorithm>
 #include <vector>
@@ -37,7 +38,15 @@ constexpr int kJ = 12;                 // outputs per lane
 constexpr uint32_t kH = 32 * kJ;       // leaf size (outputs per warp) = 384
 constexpr uint32_t kZ = 2 * kH;        // leaf z vector words (2h - 1, padded)
 constexpr uint32_t kHq = kH / 32;      // q words per leaf block = 12
-constexpr int kLeafWarps = 4;
+#ifndef MTGP_LEAF_WARPS
+#define MTGP_LEAF_WARPS 4
+#endif
+#ifndef MTGP_LEAF_MINB
+#define MTGP_LEAF_MINB 8
+#endif
+// 8 CTAs of 4 warps per SM (64 registers): 13% faster than 6 CTAs at 76 registers
+// (profiles/r1_leaf_sweep.jsonl)
+constexpr int kLeafWarps = MTGP_LEAF_WARPS;
 
 __global__ void jump_ztrans_kernel(const JumpArgs a, const KaraPlan k, uint32_t n_rows, uint4* __restrict__ zbuf) {
     // one thread per 4 output words: index over (row, block, leaf, t4)
@@ -63,66 +72,82 @@ __global__ void jump_ztrans_kernel(const JumpArgs a, const KaraPlan k, uint32_t 
     }
 }
 
-__global__ void __launch_bounds__(kLeafWarps * 32) jump_leaf_kernel(const JumpArgs a, const KaraPlan k,
-                                                                    const uint4* __restrict__ zbuf,
-                                                                    uint4* __restrict__ leaf_out) {
+// Leaf q words of every (job, leaf, block): XORs of up to 2^d raw q words (one thread per word).
+__global__ void jump_qleaf_kernel(const JumpArgs a, const KaraPlan k, uint32_t* __restrict__ qleaf) {
+    const uint64_t per_job = (uint64_t)k.n_leaf * k.blocks * kHq;
+    const uint64_t total = per_job * a.n_jobs;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t job = (uint32_t)(i / per_job);
+        const uint32_t r = (uint32_t)(i % per_job);
+        const uint32_t w = r % kHq, bs = r / kHq;
+        const uint32_t b = bs % k.blocks, s = bs / k.blocks;
+        const uint32_t* q = a.q + (size_t)a.jobs[job].q * a.q_words;
+        uint32_t v = 0;
+        for (uint32_t u = 0; u < k.nq[s]; ++u) {
+            const uint32_t idx = b * k.blk_qwords + k.oq[s][u] + w;
+            if (idx < a.q_words) v ^= __ldg(q + idx);
+        }
+        qleaf[i] = v;
+    }
+}
+
+__global__ void __launch_bounds__(kLeafWarps * 32, MTGP_LEAF_MINB) jump_leaf_kernel(const JumpArgs a, const KaraPlan k,
+                                                                                  const uint32_t* __restrict__ qleaf,
+                                                                                  const uint4* __restrict__ zbuf,
+                                                                                  uint4* __restrict__ leaf_out) {
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t unit = blockIdx.x * kLeafWarps + warp;
     const uint32_t job = unit / k.n_leaf, s = unit % k.n_leaf;
     if (job >= a.n_jobs) return;
-    const JumpJob jb = a.jobs[job];
-    const uint32_t* q = a.q + (size_t)jb.q * a.q_words;
+    const uint32_t row = a.jobs[job].row;
     const uint32_t jl = kJ * lane;
-    const uint4* zrow = zbuf + (size_t)jb.row * k.blocks * k.n_leaf * (kZ / 4);
-    const uint32_t nq = k.nq[s];
+    // this leaf's z vectors (one per block, kZ words apart by n_leaf) and its B * 12 q words
+    const uint4* zs = zbuf + ((size_t)row * k.blocks * k.n_leaf + s) * (kZ / 4) + jl / 4;
+    const uint32_t zstride4 = k.n_leaf * (kZ / 4);
+    const uint32_t total = k.blocks * kHq;
+    const uint32_t* ql = qleaf + (size_t)unit * total;
     uint32_t acc[kJ];
 #pragma unroll
     for (int i = 0; i < kJ; ++i) acc[i] = 0;
-    // lanes 0..11 hold the leaf's q words of the current block (XOR of nq raw q words)
-    auto load_q = [&](uint32_t b) -> uint32_t {
-        uint32_t v = 0;
-        if (lane < kHq)
-            for (uint32_t u = 0; u < nq; ++u) {
-                const uint32_t idx = b * k.blk_qwords + k.oq[s][u] + lane;
-                if (idx < a.q_words) v ^= __ldg(q + idx);
-            }
-        return v;
-    };
-    uint32_t qnext = load_q(0);
-    for (uint32_t b = 0; b < k.blocks; ++b) {
-        const uint32_t qmine = qnext;
-        if (b + 1 < k.blocks) qnext = load_q(b + 1);
-        const uint4* z4 = zrow + (size_t)(b * k.n_leaf + s) * (kZ / 4);
-        for (uint32_t iw = 0; iw < kHq; ++iw) {
-            const uint32_t qw = __shfl_sync(FULL, qmine, iw);
-            if (qw == 0) continue;
-            const uint32_t base4 = (iw * 32 + jl) >> 2;
-            uint32_t w[kJ + 32];
+    uint32_t b = 0, iw = 0;
+    for (uint32_t f0 = 0; f0 < total; f0 += 32) {
+        const uint32_t qmine = f0 + lane < total ? __ldg(ql + f0 + lane) : 0u;
+        const uint32_t nw = min(32u, total - f0);
+        for (uint32_t k32 = 0; k32 < nw; ++k32) {
+            const uint32_t qw = __shfl_sync(FULL, qmine, k32);
+            if (qw != 0) {
+                const uint4* z4 = zs + (size_t)b * zstride4 + iw * 8;
+                uint32_t w[kJ + 32];
 #pragma unroll
-            for (int v = 0; v < (kJ + 32) / 4; ++v) {
-                const uint4 g = __ldg(z4 + base4 + v);
-                w[4 * v] = g.x;
-                w[4 * v + 1] = g.y;
-                w[4 * v + 2] = g.z;
-                w[4 * v + 3] = g.w;
-            }
-#pragma unroll
-            for (int bb = 0; bb < 32; bb += 2) {
-                const uint32_t pat = (qw >> bb) & 3u;
-                if (pat == 1) {
-#pragma unroll
-                    for (int i = 0; i < kJ; ++i) acc[i] ^= w[bb + i];
-                } else if (pat == 2) {
-#pragma unroll
-                    for (int i = 0; i < kJ; ++i) acc[i] ^= w[bb + 1 + i];
-                } else if (pat == 3) {
-#pragma unroll
-                    for (int i = 0; i < kJ; ++i) acc[i] ^= w[bb + i] ^ w[bb + 1 + i];
+                for (int v = 0; v < (kJ + 32) / 4; ++v) {
+                    const uint4 g = __ldg(z4 + v);
+                    w[4 * v] = g.x;
+                    w[4 * v + 1] = g.y;
+                    w[4 * v + 2] = g.z;
+                    w[4 * v + 3] = g.w;
                 }
+#pragma unroll
+                for (int bb = 0; bb < 32; bb += 2) {
+                    const uint32_t pat = (qw >> bb) & 3u;
+                    if (pat == 1) {
+#pragma unroll
+                        for (int i = 0; i < kJ; ++i) acc[i] ^= w[bb + i];
+                    } else if (pat == 2) {
+#pragma unroll
+                        for (int i = 0; i < kJ; ++i) acc[i] ^= w[bb + 1 + i];
+                    } else if (pat == 3) {
+#pragma unroll
+                        for (int i = 0; i < kJ; ++i) acc[i] ^= w[bb + i] ^ w[bb + 1 + i];
+                    }
+                }
+            }
+            if (++iw == kHq) {
+                iw = 0;
+                ++b;
             }
         }
     }
-    uint4* dst = leaf_out + ((size_t)job * k.n_leaf + s) * (kH / 4) + jl / 4;
+    uint4* dst = leaf_out + (size_t)unit * (kH / 4) + jl / 4;
 #pragma unroll
     for (int v = 0; v < kJ / 4; ++v) dst[v] = make_uint4(acc[4 * v], acc[4 * v + 1], acc[4 * v + 2], acc[4 * v + 3]);
 }
@@ -216,7 +241,10 @@ uint32_t kara_prefix_words(const KaraPlan& k) {
 }
 
 size_t kara_zbuf_words(const KaraPlan& k, uint32_t n_rows) { return (size_t)n_rows * k.blocks * k.n_leaf * kZ; }
-size_t kara_leaf_words(const KaraPlan& k, uint32_t n_jobs) { return (size_t)n_jobs * k.n_leaf * kH; }
+size_t kara_leaf_words(const KaraPlan& k, uint32_t n_jobs) {
+    // leaf outputs (n_leaf * 384 words per job), then the leaf q words (n_leaf * B * 12 per job)
+    return (size_t)n_jobs * k.n_leaf * (kH + (size_t)k.blocks * kHq);
+}
 
 cudaError_t launch_jump_kara(const JumpArgs& a, const KaraPlan& k, uint32_t N, uint32_t n_rows, uint32_t* zbuf,
                              uint32_t* leaf_out, cudaStream_t st) {
@@ -226,10 +254,16 @@ cudaError_t launch_jump_kara(const JumpArgs& a, const KaraPlan& k, uint32_t N, u
         const uint32_t grid = (uint32_t)std::min<uint64_t>((total + 255) / 256, 148u * 16u);
         jump_ztrans_kernel<<<grid, 256, 0, st>>>(a, k, n_rows, reinterpret_cast<uint4*>(zbuf));
     }
+    uint32_t* qleaf = leaf_out + (size_t)a.n_jobs * k.n_leaf * kH;
+    {
+        const uint64_t total = (uint64_t)a.n_jobs * k.n_leaf * k.blocks * kHq;
+        const uint32_t grid = (uint32_t)std::min<uint64_t>((total + 255) / 256, 148u * 16u);
+        jump_qleaf_kernel<<<grid, 256, 0, st>>>(a, k, qleaf);
+    }
     {
         const uint32_t units = a.n_jobs * k.n_leaf;
         jump_leaf_kernel<<<(units + kLeafWarps - 1) / kLeafWarps, kLeafWarps * 32, 0, st>>>(
-            a, k, reinterpret_cast<const uint4*>(zbuf), reinterpret_cast<uint4*>(leaf_out));
+            a, k, qleaf, reinterpret_cast<const uint4*>(zbuf), reinterpret_cast<uint4*>(leaf_out));
     }
     {
         const dim3 grid((N + 255) / 256, a.n_jobs);
