@@ -37,11 +37,16 @@ CONFIGS = {
     "c3-f01": (11213, 2, 1 << 28, "MTGP32-11213 x200 sets, 2^28 f32 (0,1]/set/step (BASELINE config 3)"),
     "c4-23209": (23209, 0, 1 << 28, "MTGP32-23209 x200 synthetic sets, 2^28 u32/set/step (BASELINE config 4)"),
     "c4-44497": (44497, 0, 1 << 28, "MTGP32-44497 x200 synthetic sets, 2^28 u32/set/step (BASELINE config 4)"),
+    # BASELINE config 5: 1024 sets in total (200 certified + 824 synthetic) split into contiguous
+    # balanced ranges over the ranks, 2^34 outputs per step in total (2^24 per set): strong scaling
+    "c5": (11213, 0, 1 << 24, "MTGP32-11213 x1024 sets split across the ranks, 2^24 u32/set/step = 2^34 "
+                              "u32/step in total (BASELINE config 5)"),
     # the reference's own recurrence (Engine::mt) on the GPU: like for like with --impl reference
     "mt19937": (19937, 0, 1 << 28, "Engine::mt MT19937 x200 streams (seeds 5489+i), 2^28 u32/stream/step "
                                    "(the reference arm's generator, on the GPU)"),
 }
 MT_CONFIGS = {"mt19937"}
+C5_SETS = 1024
 
 
 def parse():
@@ -52,14 +57,17 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--sets", type=int, default=200)
-    ap.add_argument("--calls", type=int, default=2, help="device calls per step (output buffer = step/calls)")
+    ap.add_argument("--calls", type=int, default=None,
+                    help="device calls per step (output buffer = step/calls); default 2, 1 for c5")
     ap.add_argument("--no-checksum", action="store_true")
+    ap.add_argument("--min-piece-words", type=int, default=None, help="MTGP_OPT_MIN_PIECE_WORDS (default: library's)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-words-per-thread", type=int, default=1 << 28)
     ap.add_argument("--as-rank", type=int, default=None,
                     help="single process: generate rank R's shard of a multi-GPU run (its parameter sets / seeds), "
                          "to time every rank's workload alone on one GPU")
+    ap.add_argument("--as-world", type=int, default=None, help="with --as-rank: the world size to shard for (c5)")
     return ap.parse_args()
 
 
@@ -87,6 +95,7 @@ class ClockSampler:
         self.nv = None
         self.stop_flag = False
         self.nvml_rows = []
+        self.first = 0
 
     def _nvml_loop(self):
         import pynvml
@@ -111,6 +120,12 @@ class ClockSampler:
             self.nv = pynvml.nvmlDeviceGetHandleByIndex(self.index)
             self.t = threading.Thread(target=self._nvml_loop, daemon=True)
             self.t.start()
+            # NVML's first clock queries can take tens of ms: return once the loop is sampling,
+            # then keep only the samples taken from now on (the timed region)
+            t_end = time.perf_counter() + 1.0
+            while not self.nvml_rows and time.perf_counter() < t_end:
+                time.sleep(0.001)
+            self.first = len(self.nvml_rows)
             return
         except Exception:  # noqa: BLE001
             self.nv = None
@@ -139,6 +154,8 @@ class ClockSampler:
             import pynvml
             self.stop_flag = True
             self.t.join(timeout=2)
+            rows = self.nvml_rows[self.first:] or self.nvml_rows[-1:]
+            self.nvml_rows = rows
             sm = [r[0] for r in self.nvml_rows]
             smax = float(self.nvml_rows[-1][1]) if self.nvml_rows else None
             reasons = set()
@@ -260,25 +277,36 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     mexp, kind, L_step, label = CONFIGS[args.config]
     S = args.sets
-    shard_rank = rank
+    shard_rank, shard_world = rank, world
     if args.as_rank is not None:
         if world > 1:
             raise SystemExit("--as-rank is for single-process runs")
         shard_rank = args.as_rank
+        shard_world = args.as_world or max(1, shard_rank + 1)
+    is_c5 = args.config == "c5"
+    set_range = None
+    if is_c5:  # strong scaling: this rank's contiguous share of the 1024 global set IDs
+        set_range = shard.status_range(C5_SETS, shard_rank, shard_world)
+        S = len(set_range)
     is_mt = args.config in MT_CONFIGS
     if is_mt:  # MT19937 statuses, distinct seeds per stream (and per rank)
         sets = [mtgp.mt19937_status()] * S
         seeds = [5489 + shard_rank * S + i for i in range(S)]
+    elif is_c5:
+        sets = tables.sets_for(mexp, S, first=set_range.start)
+        seeds = [1] * S
     else:
         sets = shard.sets_for_rank(mexp, S, shard_rank)
         seeds = [1] * S
 
     def make_ctx(ss, sd):
         return mtgp.MtContext(ss, sd, device=local) if is_mt else mtgp.MtgpContext(ss, sd, device=local)
-    calls = max(1, args.calls)
+    calls = max(1, args.calls if args.calls is not None else (1 if is_c5 else 2))
     Lc = L_step // calls
     ctx = make_ctx(sets, seeds)
     ctx.set_option(mtgp.OPT_CHECKSUM, 0 if args.no_checksum else 1)
+    if args.min_piece_words:
+        ctx.set_option(mtgp.OPT_MIN_PIECE_WORDS, args.min_piece_words)
     ext = torch.cuda.ExternalStream(ctx.stream_handle(), device=torch.device("cuda", local))
     out = torch.empty((S, Lc), dtype=torch.int32, device=f"cuda:{local}")
 
@@ -371,7 +399,8 @@ def main():
     gathered_streams = len(allck)
 
     samples_rank = S * L_step * args.steps
-    total = samples_rank * world
+    # whole job: every rank's samples (c5: the 1024 sets, however they are split)
+    total = (C5_SETS if is_c5 and args.as_rank is None else S * world) * L_step * args.steps
     value = total / (ms / 1e3) / 1e9
     hbm, hbm_src = peaks()
     bytes_per_launch = 4.0 * S * Lc
@@ -430,17 +459,21 @@ def main():
             "metric": "Gsamples/s (uint32 & float) per GPU and at 1/2/4/8 B200; % of HBM write peak",
             "value": round(value, 3), "unit": "Gsamples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": "strong" if is_c5 else "weak", "vs_baseline": None,
             "dtype": ["u32", "f32", "f32"][kind],
             "data": "synthetic (seeded generator streams; no input data)",
             "config": {"workload": label, "sets_per_gpu": S, "seed": 1, "words_per_set_per_step": L_step,
                        "calls_per_step": calls, "kernel": f"v{kver}", "pieces_per_call": pieces,
                        "checksums_fused": not args.no_checksum,
-                       **({"as_rank": shard_rank, "global_set_ids": [shard_rank * S, (shard_rank + 1) * S]}
-                          if args.as_rank is not None else {}),
+                       **({"as_rank": shard_rank, "as_world": shard_world} if args.as_rank is not None else {}),
+                       "global_set_ids": ([set_range.start, set_range.stop] if is_c5
+                                          else [shard_rank * S, (shard_rank + 1) * S]),
                        "checksums_gathered_streams": gathered_streams,
                        "l2": "output 4*S*L/calls bytes per call >> 126 MB L2; no flush needed",
                        "parameter_sets": ("MT19937 (mt19937_params, proj/src/params.cpp:63-77)" if is_mt
+                                          else f"global set IDs {set_range.start}..{set_range.stop - 1}: IDs < 200 "
+                                               "cuRAND MTGP32-11213 (certified), the rest synthetic (uncertified period)"
+                                          if is_c5
                                           else "synthetic (uncertified period)" if mexp != 11213 or S > 200
                                           or shard_rank > 0
                                           else "cuRAND MTGP32-11213 (certified)" if world == 1

@@ -90,7 +90,8 @@ typedef struct mtgp_ctx mtgp_ctx;
                                    /* 6 = warp teams, register-resident (n = 624);                */
                                    /* 7 = v5 (v3 with 8 words per lane and 256-bit stores)        */
 #define MTGP_OPT_MAX_PIECES 3      /* cap on jump-ahead pieces per call (0 = auto)                  */
-#define MTGP_OPT_MIN_PIECE_WORDS 4 /* minimum words per jump-ahead piece (default 1<<21)            */
+#define MTGP_OPT_MIN_PIECE_WORDS 4 /* minimum words per jump-ahead piece; 0 (default) = auto: 1<<21, */
+                                   /* down to 1<<19 to keep >= 3 CTAs per SM busy                  */
 #define MTGP_OPT_TIMING 5          /* 0/1: record CUDA events around every generation kernel        */
 #define MTGP_OPT_HOST_CHUNK 6      /* words per stream per device chunk when out is host memory     */
 #define MTGP_OPT_JUMP 7            /* jump-ahead algorithm: 0 = auto (Karatsuba middle product for  */

@@ -293,7 +293,7 @@ int mtgp_set_option(mtgp_ctx* ctx, int option, int64_t value) {
             ctx->max_pieces = (uint32_t)value;
             return MTGP_OK;
         case MTGP_OPT_MIN_PIECE_WORDS:
-            if (value < 1) return fail(MTGP_EINVAL, "min_piece_words must be >= 1");
+            if (value < 0) return fail(MTGP_EINVAL, "min_piece_words must be >= 0 (0 = auto)");
             ctx->min_piece_words = (uint64_t)value;
             return MTGP_OK;
         case MTGP_OPT_TIMING: ctx->timing = value != 0; return MTGP_OK;

@@ -39,7 +39,7 @@ struct mtgp_ctx {
     int kernel = 0;
     int jump_mode = 0;  // MTGP_OPT_JUMP
     uint32_t max_pieces = 0;
-    uint64_t min_piece_words = 1ull << 21;
+    uint64_t min_piece_words = 0;  // 0 = auto (pieces_wanted, mtgp_plan.cu)
     bool timing = false;
     uint64_t host_chunk = 1ull << 20;
 

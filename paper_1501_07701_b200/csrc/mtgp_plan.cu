@@ -68,6 +68,21 @@ void parallel_for(size_t n, F&& f) {
 
 constexpr uint64_t kMaxPieceWords = 1ull << 30;
 
+// Pieces wanted for W words over T resident teams. An explicit minimum piece length is honoured.
+// Auto (min_piece == 0): 2^21-word (8 MB) pieces, but never fewer than three 4-warp CTAs per SM
+// while pieces stay >= 2^19 words -- one CTA per SM left 85% of the warps idle on a
+// 128 sets x 2^24 request (902 vs 1038 Gsamples/s; profiles/r1_c5_min_piece.jsonl).
+uint64_t pieces_wanted(uint64_t W, uint64_t T, uint64_t quantum, uint64_t min_piece) {
+    uint64_t w;
+    if (min_piece) {
+        w = W / min_piece;
+    } else {
+        w = W >> 21;
+        w = std::max<uint64_t>(w, std::min<uint64_t>(3 * quantum, W >> 19));
+    }
+    return std::min<uint64_t>(T, std::max<uint64_t>(1, w));
+}
+
 }  // namespace
 
 struct PlannerImpl {
@@ -277,11 +292,10 @@ cudaError_t PlannerImpl::analyze(const void* params, const uint32_t* win, cudaSt
 cudaError_t PlannerImpl::build_plan(uint64_t L, uint32_t T, uint64_t min_piece, std::string& err) {
     if (plan_valid && plan_L == L && plan_T == T) return cudaSuccess;
     const uint64_t W = (uint64_t)S * L;
-    uint64_t want = std::max<uint64_t>(1, W / std::max<uint64_t>(1, min_piece));
-    want = std::min<uint64_t>(want, T);
     // Equal work per SM: team counts are whole multiples of (SMs x warps per CTA), so every SM
     // holds the same number of CTAs (a 5-vs-6 CTA split costs ~10% of the makespan).
     const uint64_t quantum = (uint64_t)num_sms * kWarpsPerCta;
+    uint64_t want = pieces_wanted(W, T, quantum, min_piece);
     if (want >= quantum) want -= want % quantum;
     want = std::max<uint64_t>(want, (W + kMaxPieceWords - 1) / kMaxPieceWords);
     pieces.clear();
@@ -465,7 +479,7 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     uint32_t T = (uint32_t)(cps * kWarpsPerCta * I.num_sms);
     if (r.max_pieces) T = std::min(T, r.max_pieces);
     const uint64_t W = (uint64_t)I.S * r.L;
-    const bool need_jumps = std::min<uint64_t>(T, W / std::max<uint64_t>(1, r.min_piece_words)) > I.S ||
+    const bool need_jumps = pieces_wanted(W, T, (uint64_t)I.num_sms * kWarpsPerCta, r.min_piece_words) > I.S ||
                             r.L > kMaxPieceWords;
     cudaError_t e;
     if (need_jumps && !I.analyzed) {

@@ -32,12 +32,22 @@ def gather_checksums(local: Sequence[Cksum], device=None) -> List[Cksum]:
     import torch.distributed as dist
 
     rows = [[c[0] & 0xFFFFFFFF, (c[0] >> 32) & 0xFFFFFFFF, c[1] & 0xFFFFFFFF, c[2]] for c in local]
-    t = torch.tensor(rows, dtype=torch.int64, device=device)
+    t = torch.tensor(rows, dtype=torch.int64, device=device).reshape(-1, 4)
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
         parts = [t]
     else:
-        parts = [torch.empty_like(t) for _ in range(dist.get_world_size())]
-        dist.all_gather(parts, t)
+        # ranks may own different stream counts (a balanced split of n sets over any world size):
+        # gather the counts, pad to the largest, gather, trim
+        world = dist.get_world_size()
+        n = torch.tensor([t.shape[0]], dtype=torch.int64, device=device)
+        counts = [torch.empty_like(n) for _ in range(world)]
+        dist.all_gather(counts, n)
+        counts = [int(c.item()) for c in counts]
+        pad = torch.zeros((max(counts), 4), dtype=torch.int64, device=device)
+        pad[:t.shape[0]] = t
+        parts = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(parts, pad)
+        parts = [p[:c] for p, c in zip(parts, counts)]
     out: List[Cksum] = []
     for p in parts:
         for lo, hi, x, w in p.cpu().tolist():

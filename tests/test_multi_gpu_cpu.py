@@ -130,3 +130,54 @@ def test_run_grid_distributed_order_and_coverage(n_status):
     want = [(si, wi, t, float(statuses[si]), str(si)) for si in range(n_status) for wi in range(2)
             for t in ("gap", "hamming_indep")]
     assert got[0][1] == want
+
+
+def _worker_strong(rank, world, port, n_total, L, q):
+    """bench.py --config c5: rank r owns the balanced contiguous range status_range(n_total, r, world)
+    of the global set IDs (uneven when n_total % world != 0); the gather pads and trims."""
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    sys.path.insert(0, str(root))
+    sys.path.insert(0, str(root / "oracle"))
+    import numpy as np
+    import torch.distributed as dist
+
+    import oracle_py
+    from paper_1501_07701_b200 import shard, tables
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = shard.status_range(n_total, rank, world)
+    sets = tables.sets_for(11213, len(rng), first=rng.start)
+    words, _ = oracle_py.mtgp_bulk(sets, [1] * len(sets), L, threads=2) if len(sets) else ([], None)
+    local = [(int(w.astype("uint64").sum()), int(np.bitwise_xor.reduce(w)), L) for w in words]
+    allck = shard.gather_checksums(local)
+    if rank == 0:
+        q.put(allck)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_strong_split_uneven_gather():
+    from paper_1501_07701_b200 import tables
+    import numpy as np
+    import oracle_py
+
+    world, n_total, L = 3, 7, 3000  # 3 / 2 / 2 sets; IDs cross nothing (all certified) but shapes differ
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_strong, args=(r, world, port, n_total, L, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    allck = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    every = tables.sets_for(11213, n_total)
+    assert len(allck) == n_total
+    for gid, (p, ck) in enumerate(zip(every, allck)):
+        w = oracle_py.MtgpOracle(p, 1).fill(L)
+        assert ck == (int(w.astype("uint64").sum()), int(np.bitwise_xor.reduce(w)), L), gid
