@@ -95,7 +95,8 @@ typedef struct mtgp_ctx mtgp_ctx;
 #define MTGP_OPT_TIMING 5          /* 0/1: record CUDA events around every generation kernel        */
 #define MTGP_OPT_HOST_CHUNK 6      /* words per stream per device chunk when out is host memory     */
 #define MTGP_OPT_JUMP 7            /* jump-ahead algorithm: 0 = auto (Karatsuba middle product for  */
-                                   /* windows N > 384 words, direct otherwise), 1 = direct always  */
+                                   /* windows N > 384 words, direct otherwise), 1 = direct always, */
+                                   /* 2 = split (Karatsuba, or q blocks over several warps at d=0) */
 
 /* Library / device info. */
 int mtgp_abi_version(void);

@@ -302,7 +302,7 @@ int mtgp_set_option(mtgp_ctx* ctx, int option, int64_t value) {
             ctx->host_chunk = (uint64_t)value;
             return MTGP_OK;
         case MTGP_OPT_JUMP:
-            if (value < 0 || value > 1) return fail(MTGP_EINVAL, "jump must be 0 (auto) or 1 (direct)");
+            if (value < 0 || value > 2) return fail(MTGP_EINVAL, "jump must be 0 (auto), 1 (direct) or 2 (split)");
             ctx->jump_mode = (int)value;
             if (ctx->planner) ctx->planner->set_jump_mode((int)value);
             return MTGP_OK;

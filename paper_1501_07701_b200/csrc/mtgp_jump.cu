@@ -42,10 +42,10 @@ constexpr uint32_t kHq = kH / 32;      // q words per leaf block = 12
 #define MTGP_LEAF_WARPS 4
 #endif
 #ifndef MTGP_LEAF_MINB
-#define MTGP_LEAF_MINB 8
+#define MTGP_LEAF_MINB 7
 #endif
-// 8 CTAs of 4 warps per SM (64 registers): 13% faster than 6 CTAs at 76 registers
-// (profiles/r1_leaf_sweep.jsonl)
+// 7 CTAs of 4 warps per SM (72 registers, no spills): 6 CTAs at 76 registers were 13% slower,
+// 8 CTAs (64 registers, spilling) the same (profiles/r1_leaf_sweep.jsonl, r1_jump_sweep.jsonl)
 constexpr int kLeafWarps = MTGP_LEAF_WARPS;
 
 __global__ void jump_ztrans_kernel(const JumpArgs a, const KaraPlan k, uint32_t n_rows, uint4* __restrict__ zbuf) {
@@ -91,32 +91,48 @@ __global__ void jump_qleaf_kernel(const JumpArgs a, const KaraPlan k, uint32_t* 
     }
 }
 
+template <bool DIRECT>
 __global__ void __launch_bounds__(kLeafWarps * 32, MTGP_LEAF_MINB) jump_leaf_kernel(const JumpArgs a, const KaraPlan k,
                                                                                   const uint32_t* __restrict__ qleaf,
                                                                                   const uint4* __restrict__ zbuf,
                                                                                   uint4* __restrict__ leaf_out) {
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t unit = blockIdx.x * kLeafWarps + warp;
-    const uint32_t job = unit / k.n_leaf, s = unit % k.n_leaf;
+    const uint32_t unit = blockIdx.x * kLeafWarps + warp;  // (job, leaf, group)
+    const uint32_t g = unit % k.groups, js = unit / k.groups;
+    const uint32_t job = js / k.n_leaf, s = js % k.n_leaf;
     if (job >= a.n_jobs) return;
     const uint32_t row = a.jobs[job].row;
     const uint32_t jl = kJ * lane;
-    // this leaf's z vectors (one per block, kZ words apart by n_leaf) and its B * 12 q words
-    const uint4* zs = zbuf + ((size_t)row * k.blocks * k.n_leaf + s) * (kZ / 4) + jl / 4;
-    const uint32_t zstride4 = k.n_leaf * (kZ / 4);
-    const uint32_t total = k.blocks * kHq;
-    const uint32_t* ql = qleaf + (size_t)unit * total;
+    // this group's blocks [b0, b1) of the leaf
+    const uint32_t per = (k.blocks + k.groups - 1) / k.groups;
+    const uint32_t b0 = min(k.blocks, g * per), b1 = min(k.blocks, b0 + per);
+    // z vector of block b: d = 0 reads the prefix itself (x[b * 384, b * 384 + 768)); d >= 1 the
+    // transformed vectors (one per block, n_leaf * kZ words apart)
+    const uint4* zs;
+    uint32_t zstride4;
+    if (DIRECT) {
+        zs = reinterpret_cast<const uint4*>(a.pre + (size_t)row * a.pre_stride + a.pre_off) + jl / 4;
+        zstride4 = k.n_out / 4;
+    } else {
+        zs = zbuf + ((size_t)row * k.blocks * k.n_leaf + s) * (kZ / 4) + jl / 4;
+        zstride4 = k.n_leaf * (kZ / 4);
+    }
+    zs += (size_t)b0 * zstride4;
+    const uint32_t total = (b1 - b0) * kHq;
+    const uint32_t* ql = qleaf + (size_t)js * k.blocks * kHq + b0 * kHq;
     uint32_t acc[kJ];
 #pragma unroll
     for (int i = 0; i < kJ; ++i) acc[i] = 0;
-    uint32_t b = 0, iw = 0;
+    // zb: the current block's z vector; iw: q word within the block
+    const uint4* zb = zs;
+    uint32_t iw = 0;
     for (uint32_t f0 = 0; f0 < total; f0 += 32) {
         const uint32_t qmine = f0 + lane < total ? __ldg(ql + f0 + lane) : 0u;
         const uint32_t nw = min(32u, total - f0);
         for (uint32_t k32 = 0; k32 < nw; ++k32) {
             const uint32_t qw = __shfl_sync(FULL, qmine, k32);
             if (qw != 0) {
-                const uint4* z4 = zs + (size_t)b * zstride4 + iw * 8;
+                const uint4* z4 = zb + iw * 8;
                 uint32_t w[kJ + 32];
 #pragma unroll
                 for (int v = 0; v < (kJ + 32) / 4; ++v) {
@@ -143,7 +159,7 @@ __global__ void __launch_bounds__(kLeafWarps * 32, MTGP_LEAF_MINB) jump_leaf_ker
             }
             if (++iw == kHq) {
                 iw = 0;
-                ++b;
+                zb += zstride4;
             }
         }
     }
@@ -158,9 +174,10 @@ __global__ void jump_combine_kernel(const JumpArgs a, const KaraPlan k, uint32_t
     if (t >= N) return;
     const JumpJob jb = a.jobs[job];
     const uint32_t c = t / kH, tt = t % kH;
-    const uint32_t* lo = leaf_out + (size_t)job * k.n_leaf * kH + tt;
+    const uint32_t* lo = leaf_out + (size_t)job * k.n_leaf * k.groups * kH + tt;
     uint32_t v = 0;
-    for (uint32_t u = 0; u < k.n_comb; ++u) v ^= lo[(size_t)k.comb[c][u] * kH];
+    for (uint32_t u = 0; u < k.n_comb; ++u)
+        for (uint32_t g = 0; g < k.groups; ++g) v ^= lo[((size_t)k.comb[c][u] * k.groups + g) * kH];
     a.piece_win[(size_t)jb.piece * N + t] = v;
 }
 
@@ -168,7 +185,7 @@ __global__ void jump_combine_kernel(const JumpArgs a, const KaraPlan k, uint32_t
 
 bool kara_plan(uint32_t N, uint32_t q_words, int depth_override, KaraPlan& k) {
     int d = depth_override >= 0 ? depth_override : (N <= kH ? 0 : N <= 2 * kH ? 1 : 2);
-    if (d <= 0 || d > 2 || (kH << d) < N) return false;
+    if (d < 0 || d > 2 || (kH << d) < N) return false;
     k = KaraPlan{};
     k.depth = (uint32_t)d;
     k.n_out = kH << d;
@@ -242,27 +259,36 @@ uint32_t kara_prefix_words(const KaraPlan& k) {
 
 size_t kara_zbuf_words(const KaraPlan& k, uint32_t n_rows) { return (size_t)n_rows * k.blocks * k.n_leaf * kZ; }
 size_t kara_leaf_words(const KaraPlan& k, uint32_t n_jobs) {
-    // leaf outputs (n_leaf * 384 words per job), then the leaf q words (n_leaf * B * 12 per job)
-    return (size_t)n_jobs * k.n_leaf * (kH + (size_t)k.blocks * kHq);
+    // partial leaf outputs (n_leaf * G * 384 words per job), then the leaf q words (n_leaf * B * 12)
+    return (size_t)n_jobs * k.n_leaf * ((size_t)k.groups * kH + (size_t)k.blocks * kHq);
+}
+
+uint32_t kara_groups(const KaraPlan& k, uint32_t n_jobs, int num_sms) {
+    // MTGP_LEAF_MINB CTAs x 4 warps per SM resident; at least 4 blocks per group
+    const uint64_t want = (uint64_t)num_sms * MTGP_LEAF_MINB * kLeafWarps;
+    const uint64_t have = std::max<uint64_t>(1, (uint64_t)n_jobs * k.n_leaf);
+    const uint32_t g = (uint32_t)std::min<uint64_t>((want + have - 1) / have, std::max<uint32_t>(1, k.blocks / 4));
+    return std::max<uint32_t>(1, g);
 }
 
 cudaError_t launch_jump_kara(const JumpArgs& a, const KaraPlan& k, uint32_t N, uint32_t n_rows, uint32_t* zbuf,
                              uint32_t* leaf_out, cudaStream_t st) {
     if (a.n_jobs == 0 || n_rows == 0) return cudaSuccess;
-    {
+    if (k.depth > 0) {  // d = 0 reads its z windows straight from the prefix
         const uint64_t total = (uint64_t)n_rows * k.blocks * k.n_leaf * (kZ / 4);
         const uint32_t grid = (uint32_t)std::min<uint64_t>((total + 255) / 256, 148u * 16u);
         jump_ztrans_kernel<<<grid, 256, 0, st>>>(a, k, n_rows, reinterpret_cast<uint4*>(zbuf));
     }
-    uint32_t* qleaf = leaf_out + (size_t)a.n_jobs * k.n_leaf * kH;
+    uint32_t* qleaf = leaf_out + (size_t)a.n_jobs * k.n_leaf * k.groups * kH;
     {
         const uint64_t total = (uint64_t)a.n_jobs * k.n_leaf * k.blocks * kHq;
         const uint32_t grid = (uint32_t)std::min<uint64_t>((total + 255) / 256, 148u * 16u);
         jump_qleaf_kernel<<<grid, 256, 0, st>>>(a, k, qleaf);
     }
     {
-        const uint32_t units = a.n_jobs * k.n_leaf;
-        jump_leaf_kernel<<<(units + kLeafWarps - 1) / kLeafWarps, kLeafWarps * 32, 0, st>>>(
+        const uint32_t units = a.n_jobs * k.n_leaf * k.groups;
+        auto kern = k.depth == 0 ? jump_leaf_kernel<true> : jump_leaf_kernel<false>;
+        kern<<<(units + kLeafWarps - 1) / kLeafWarps, kLeafWarps * 32, 0, st>>>(
             a, k, qleaf, reinterpret_cast<const uint4*>(zbuf), reinterpret_cast<uint4*>(leaf_out));
     }
     {

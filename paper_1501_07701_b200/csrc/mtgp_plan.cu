@@ -129,8 +129,11 @@ struct PlannerImpl {
                           &d_win_next, &d_all_rows, &d_zbuf, &d_leaf})
             b->release();
     }
+    // d = 0 (N <= 384, i.e. 11213) keeps the flat jump: the grouped d = 0 leaf path measured
+    // 0.66 vs 0.51 ms per C2 call and only 0.35 vs 0.37 on config-5 shards
+    // (profiles/r1_jump_sweep.jsonl)
     void init_jump() { kara_ok = kara_plan(N, (M + 31) / 32, -1, kara); }
-    bool use_kara() const { return kara_ok && jump_mode == 0; }
+    bool use_kara() const { return kara_ok && ((jump_mode == 0 && kara.depth > 0) || jump_mode == 2); }
 
     // words the jump kernels read per row (from x_{t0})
     uint32_t prefix_len() const {
@@ -153,10 +156,12 @@ struct PlannerImpl {
     }
     cudaError_t jump(const JumpArgs& a, uint32_t n_rows, cudaStream_t st) {
         if (use_kara()) {
+            KaraPlan k = kara;
+            k.groups = kara_groups(k, a.n_jobs, num_sms);
             cudaError_t e;
-            if ((e = d_zbuf.ensure(4 * kara_zbuf_words(kara, n_rows))) != cudaSuccess) return e;
-            if ((e = d_leaf.ensure(4 * kara_leaf_words(kara, a.n_jobs))) != cudaSuccess) return e;
-            return launch_jump_kara(a, kara, N, n_rows, d_zbuf.as<uint32_t>(), d_leaf.as<uint32_t>(), st);
+            if (k.depth > 0 && (e = d_zbuf.ensure(4 * kara_zbuf_words(k, n_rows))) != cudaSuccess) return e;
+            if ((e = d_leaf.ensure(4 * kara_leaf_words(k, a.n_jobs))) != cudaSuccess) return e;
+            return launch_jump_kara(a, k, N, n_rows, d_zbuf.as<uint32_t>(), d_leaf.as<uint32_t>(), st);
         }
         return mt ? launch_jump_rt(a, N, st) : launch_jump(M, a, n_rows, st);
     }

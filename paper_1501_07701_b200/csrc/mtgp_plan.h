@@ -45,7 +45,7 @@ public:
     bool v2_supported() const;
     // Engine::mt: the register-resident team kernel (version 6) takes this request shape
     bool mt3_supported(int kind, uint64_t L, const void* out) const;
-    // MTGP_OPT_JUMP: 0 = auto (Karatsuba jump for N > 384), 1 = direct (flat) jump
+    // MTGP_OPT_JUMP: 0 = auto (Karatsuba jump for N > 384), 1 = direct (flat) jump, 2 = split always
     void set_jump_mode(int mode);
     // forget per-stream algebra and cached plans (after a state restore)
     void invalidate();

@@ -39,16 +39,19 @@ def test_kara_jump_matches_direct_and_oracle(mexp, kernel):
     assert np.array_equal(a2, ref[:, L1:])
 
 
-def test_kara_jump_is_a_noop_choice_at_11213(curand_sets):
-    """N = 351 <= 384: both modes run the direct jump; results identical and exact."""
+@pytest.mark.parametrize("jump", [0, 2])
+def test_split_jump_at_11213(curand_sets, jump):
+    """N = 351 <= 384: auto runs the direct jump; mode 2 splits each jump's q blocks over
+    several warps (d = 0, partial windows XOR-combined). Both exact."""
     sets = curand_sets[10:14]
     seeds = [1, 2, 3, 4]
-    a1, a2, _, _ = _run_mtgp(sets, seeds, 0, 3, 200_000, 1000, 4096)
+    a1, a2, pieces, _ = _run_mtgp(sets, seeds, jump, 3, 200_000, 1000, 4096)
+    assert pieces > 4 * 20
     ref, _ = oracle_py.mtgp_bulk(sets, seeds, 201_000, threads=4)
     assert np.array_equal(a1, ref[:, :200_000]) and np.array_equal(a2, ref[:, 200_000:])
 
 
-@pytest.mark.parametrize("jump", [0, 1])
+@pytest.mark.parametrize("jump", [0, 1, 2])
 def test_kara_skip_44497(jump):
     sets = tables.synthetic_sets(44497, 3)
     with mtgp.MtgpContext(sets, [1, 2, 3]) as ctx:
