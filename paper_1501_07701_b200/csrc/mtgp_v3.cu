@@ -39,6 +39,13 @@ namespace mtgpb {
 #ifndef MTGP3_CK_WIDE
 #define MTGP3_CK_WIDE 0
 #endif
+// Checksum sum on the FMA pipe without 64-bit adds: within a run of <= 2^16 words per lane, `sum`
+// holds two 32-bit accumulators, A = sum(o) mod 2^32 (IMAD) and B = sum(o >> 16) mod 2^32
+// (IMAD.HI); then sum(o) = 2^16 B + ((A - (B << 16)) mod 2^32) exactly (the low halves add up to
+// less than 2^32). run3 folds them into the 64-bit total every 8192 steps.
+#ifndef MTGP3_CK_HILO
+#define MTGP3_CK_HILO 0
+#endif
 // Operand select on the FMA pipe: send = hi * m + lo * (1 - m) with a per-lane 0/1 multiplier
 // (two IMADs instead of one SEL on the ALU pipe). 0: SEL everywhere, 1: IMAD for the A and C
 // streams, 2: A only, 3: C only.
@@ -161,7 +168,15 @@ __device__ __forceinline__ void step3(const V3Ctx& p, const uint4& h1, const uin
         if (!TAIL || w0 < len) {
             __stcs(reinterpret_cast<uint4*>(optr + w0), make_uint4(o[0], o[1], o[2], o[3]));
             if (CK) {
-#if MTGP3_CK_WIDE
+#if MTGP3_CK_HILO
+                uint32_t ca = (uint32_t)sum, cb = (uint32_t)(sum >> 32);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(ca) : "r"(o[c]), "r"(p.one));
+                    asm("mad.hi.u32 %0, %1, %2, %0;" : "+r"(cb) : "r"(o[c]), "r"(p.m16));
+                }
+                sum = ((unsigned long long)cb << 32) | ca;
+#elif MTGP3_CK_WIDE
                 // 64-bit sum on the FMA pipe: IMAD.WIDE.U32 sum = o * one + sum (one is opaque)
 #pragma unroll
                 for (int c = 0; c < 4; ++c) asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(sum) : "r"(o[c]), "r"(p.one));
@@ -187,6 +202,12 @@ __device__ __forceinline__ void step3(const V3Ctx& p, const uint4& h1, const uin
     }
 }
 
+// packed (A, B) accumulators -> the exact sum of the words they saw (MTGP3_CK_HILO)
+__device__ __forceinline__ unsigned long long hilo_sum(unsigned long long packed) {
+    const uint32_t a = (uint32_t)packed, b = (uint32_t)(packed >> 32);
+    return ((unsigned long long)b << 16) + (uint32_t)(a - (b << 16));
+}
+
 template <int RC, int KIND, bool CK>
 __device__ __forceinline__ void run3(const V3Ctx& p, uint4 X0, uint4 X1, uint4 Y1, uint32_t* optr, uint32_t len,
                                      uint32_t* win_out, unsigned long long& sum, uint32_t& xr) {
@@ -197,16 +218,35 @@ __device__ __forceinline__ void run3(const V3Ctx& p, uint4 X0, uint4 X1, uint4 Y
     // cannot reach the end window [len, len + N) while n + 256 + N <= len: the main loop runs
     // pairs of such steps; the (at most three) remaining steps run the predicated tail variant.
     uint32_t m = 0;
+#if MTGP3_CK_HILO
+    unsigned long long tot = sum;
+    sum = 0;
+#endif
     for (; (m + 2) * kStepWords + kN <= len; m += 2) {
         step3<RC, KIND, CK, false>(p, Y1, X0, X1, Y0, Y1, optr, m * kStepWords, len, nullptr, len, sum, xr);
         step3<RC, KIND, CK, false>(p, X1, Y0, Y1, X0, X1, optr, (m + 1) * kStepWords, len, nullptr, len, sum, xr);
+#if MTGP3_CK_HILO
+        if (CK && (m & 8190u) == 8190u) {  // 8192 steps = 2^16 words per lane
+            tot += hilo_sum(sum);
+            sum = 0;
+        }
+#endif
     }
+#if MTGP3_CK_HILO
+    if (CK) {
+        tot += hilo_sum(sum);
+        sum = 0;
+    }
+#endif
     while (m < steps) {
         step3<RC, KIND, CK, true>(p, Y1, X0, X1, Y0, Y1, optr, m * kStepWords, len, win_out, len, sum, xr);
         if (++m >= steps) break;
         step3<RC, KIND, CK, true>(p, X1, Y0, Y1, X0, X1, optr, m * kStepWords, len, win_out, len, sum, xr);
         ++m;
     }
+#if MTGP3_CK_HILO
+    if (CK) sum = tot + hilo_sum(sum);
+#endif
 }
 
 }  // namespace
