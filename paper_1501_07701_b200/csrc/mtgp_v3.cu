@@ -46,6 +46,10 @@ namespace mtgpb {
 #ifndef MTGP3_CK_HILO
 #define MTGP3_CK_HILO 0
 #endif
+// x << sh1 as a shift on the ALU pipe instead of an IMAD by 2^sh1 on the FMA pipe
+#ifndef MTGP3_SH1_SHF
+#define MTGP3_SH1_SHF 0
+#endif
 // Operand select on the FMA pipe: send = hi * m + lo * (1 - m) with a per-lane 0/1 multiplier
 // (two IMADs instead of one SEL on the ALU pipe). 0: SEL everywhere, 1: IMAD for the A and C
 // streams, 2: A only, 3: C only.
@@ -77,7 +81,11 @@ __device__ __forceinline__ uint32_t rec3(const V3Ctx& p, uint32_t a, uint32_t b,
 #else
     const uint32_t cs = c >> p.sh2;
 #endif
+#if MTGP3_SH1_SHF
+    const uint32_t y = x ^ (x << p.sh1) ^ cs;
+#else
     const uint32_t y = x ^ (x * p.mul1) ^ cs;
+#endif
     return y ^ __shfl_sync(FULL, p.tblr, y, 16);
 }
 
