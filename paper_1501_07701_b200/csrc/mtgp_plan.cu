@@ -69,16 +69,17 @@ void parallel_for(size_t n, F&& f) {
 constexpr uint64_t kMaxPieceWords = 1ull << 30;
 
 // Pieces wanted for W words over T resident teams. An explicit minimum piece length is honoured.
-// Auto (min_piece == 0): 2^21-word (8 MB) pieces, but never fewer than three 4-warp CTAs per SM
-// while pieces stay >= 2^19 words -- one CTA per SM left 85% of the warps idle on a
-// 128 sets x 2^24 request (902 vs 1038 Gsamples/s; profiles/r1_c5_min_piece.jsonl).
+// Auto (min_piece == 0): 2^21-word (8 MB) pieces, but at least three 4-warp CTAs per SM when
+// that still leaves pieces of >= 2^19 words -- one CTA per SM left 85% of the warps idle on a
+// 128 sets x 2^24 request (902 vs 1038 Gsamples/s; profiles/r1_c5_min_piece.jsonl). Small
+// requests (a single GpuWordSource refill) keep one piece per stream and never jump.
 uint64_t pieces_wanted(uint64_t W, uint64_t T, uint64_t quantum, uint64_t min_piece) {
     uint64_t w;
     if (min_piece) {
         w = W / min_piece;
     } else {
         w = W >> 21;
-        w = std::max<uint64_t>(w, std::min<uint64_t>(3 * quantum, W >> 19));
+        if ((W >> 19) >= 3 * quantum) w = std::max<uint64_t>(w, 3 * quantum);
     }
     return std::min<uint64_t>(T, std::max<uint64_t>(1, w));
 }
