@@ -403,7 +403,12 @@ int mtgp_generate(mtgp_ctx* ctx, int kind, void* out, uint64_t L, int out_is_dev
     const size_t es = kind == MTGP_F64_01 ? 8 : 4;  // bytes per sample
     // chunk lengths are multiples of 4 (the register-resident kernels need L % 4 == 0 per call),
     // so the device path a request takes does not depend on the staging size
-    const uint64_t Lc = std::min<uint64_t>(L, std::max<uint64_t>(4, ctx->host_chunk & ~3ull));
+    uint64_t Lc = std::min<uint64_t>(L, std::max<uint64_t>(4, ctx->host_chunk & ~3ull));
+    // Few streams (a GpuWordSource refill): one device call for the whole request when it is at
+    // most 2^24 words, so the call can split each stream into jump-ahead pieces over many warps and
+    // its plan (cached per request length) is reused refill after refill; no ramp.
+    const bool single = (uint64_t)ctx->n_sets * L <= (1ull << 24) && L % 4 == 0;
+    if (single) Lc = L;
     const size_t chunk_bytes = (size_t)Lc * ctx->n_sets * es;
     if (ctx->stage_bytes < 2 * chunk_bytes) {
         CK(cudaStreamSynchronize(ctx->copy_stream), "sync");
@@ -417,7 +422,7 @@ int mtgp_generate(mtgp_ctx* ctx, int kind, void* out, uint64_t L, int out_is_dev
     // Chunk sizes ramp up 16x per chunk from a small first chunk: the copy engine starts after
     // ~1/64 of a chunk's generation instead of a whole one (generation outruns PCIe ~20x, so
     // the ramp never starves the copy). Lengths stay multiples of 4 words (v3 eligibility).
-    uint64_t next_len = std::max<uint64_t>(std::min<uint64_t>(Lc, 4096), (Lc >> 6) & ~3ull);
+    uint64_t next_len = single ? Lc : std::max<uint64_t>(std::min<uint64_t>(Lc, 4096), (Lc >> 6) & ~3ull);
     int c = 0;
     for (uint64_t done = 0, len = 0; done < L; done += len, ++c) {
         len = std::min<uint64_t>(next_len, L - done);

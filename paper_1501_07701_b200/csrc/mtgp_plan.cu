@@ -11,6 +11,7 @@
 // For the certified cuRAND sets P is the irreducible characteristic polynomial of degree 11213.
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -72,14 +73,21 @@ constexpr uint64_t kMaxPieceWords = 1ull << 30;
 // Auto (min_piece == 0): 2^21-word (8 MB) pieces, but at least three 4-warp CTAs per SM when
 // that still leaves pieces of >= 2^19 words -- one CTA per SM left 85% of the warps idle on a
 // 128 sets x 2^24 request (902 vs 1038 Gsamples/s; profiles/r1_c5_min_piece.jsonl). Small
-// requests (a single GpuWordSource refill) keep one piece per stream and never jump.
-uint64_t pieces_wanted(uint64_t W, uint64_t T, uint64_t quantum, uint64_t min_piece) {
+// requests that would not fill one CTA per SM (a few streams: a GpuWordSource refill) are split
+// into about sqrt(W * jump_k) pieces. That minimises W / (P * r) + P * J / G: one warp generates
+// r words/s, the whole GPU G, and one jump costs the GPU as much as J generated words.
+// jump_k = G / (r J); ~3.8e-3 at 11213, lower where jumps cost more (PlannerImpl::init_jump).
+// Only streams of >= 2^19 words per call are split this way: below that one warp finishes in
+// less time than the prefix + jump launches take (~0.1 ms).
+uint64_t pieces_wanted(uint64_t W, uint64_t L, uint64_t T, uint64_t quantum, uint64_t min_piece, double jump_k) {
     uint64_t w;
     if (min_piece) {
         w = W / min_piece;
     } else {
         w = W >> 21;
         if ((W >> 19) >= 3 * quantum) w = std::max<uint64_t>(w, 3 * quantum);
+        if (w < quantum && jump_k > 0 && L >= (1ull << 19))
+            w = std::max<uint64_t>(w, std::min<uint64_t>(quantum, (uint64_t)std::sqrt((double)W * jump_k)));
     }
     return std::min<uint64_t>(T, std::max<uint64_t>(1, w));
 }
@@ -130,10 +138,16 @@ struct PlannerImpl {
                           &d_win_next, &d_all_rows, &d_zbuf, &d_leaf})
             b->release();
     }
-    // d = 0 (N <= 384, i.e. 11213) keeps the flat jump: the grouped d = 0 leaf path measured
-    // 0.66 vs 0.51 ms per C2 call and only 0.35 vs 0.37 on config-5 shards
-    // (profiles/r1_jump_sweep.jsonl)
-    void init_jump() { kara_ok = kara_plan(N, (M + 31) / 32, -1, kara); }
+    // d = 0 (N <= 384, i.e. 11213) keeps the flat jump when the jumps fill the GPU: the grouped
+    // d = 0 leaf path measured 0.66 vs 0.51 ms per C2 call (profiles/r1_jump_sweep.jsonl)
+    double jump_k = 0;  // pieces_wanted's G / (r J) for this shape
+    void init_jump() {
+        kara_ok = kara_plan(N, (M + 31) / 32, -1, kara);
+        // calibrated at 11213 (N M = 3.9e6, direct jump): r ~ 2.4e9 words/s per warp
+        // (profiles/r1_single_stream.jsonl), G ~ 1.15e12, J ~ 1.25e5 words
+        const double f = !kara_ok || kara.depth == 0 ? 1.0 : kara.depth == 1 ? 0.75 : 0.5625;
+        jump_k = 3.8e-3 * (351.0 * 11213.0) / ((double)N * (double)M * f);
+    }
     bool use_kara() const { return kara_ok && ((jump_mode == 0 && kara.depth > 0) || jump_mode == 2); }
 
     // words the jump kernels read per row (from x_{t0})
@@ -156,7 +170,12 @@ struct PlannerImpl {
                   : launch_prefix(static_cast<const DevParams*>(params), win, rows, n_rows, N, pre, len, st);
     }
     cudaError_t jump(const JumpArgs& a, uint32_t n_rows, cudaStream_t st) {
-        if (use_kara()) {
+        // d = 0 (11213): the flat kernel runs one warp per jump, which is slow in latency when there
+        // are few jumps (a single stream: ~0.3 ms for 351 q words). Split the q blocks over >= 3
+        // warps per jump then (profiles/r1_single_stream.jsonl); keep the flat kernel when the
+        // jumps already fill the GPU (C2: 0.51 vs 0.66 ms, profiles/r1_jump_sweep.jsonl).
+        const bool split0 = jump_mode == 0 && kara_ok && kara.depth == 0 && kara_groups(kara, a.n_jobs, num_sms) >= 3;
+        if (use_kara() || split0) {
             KaraPlan k = kara;
             k.groups = kara_groups(k, a.n_jobs, num_sms);
             cudaError_t e;
@@ -301,7 +320,7 @@ cudaError_t PlannerImpl::build_plan(uint64_t L, uint32_t T, uint64_t min_piece, 
     // Equal work per SM: team counts are whole multiples of (SMs x warps per CTA), so every SM
     // holds the same number of CTAs (a 5-vs-6 CTA split costs ~10% of the makespan).
     const uint64_t quantum = (uint64_t)num_sms * kWarpsPerCta;
-    uint64_t want = pieces_wanted(W, T, quantum, min_piece);
+    uint64_t want = pieces_wanted(W, L, T, quantum, min_piece, jump_k);
     if (want >= quantum) want -= want % quantum;
     want = std::max<uint64_t>(want, (W + kMaxPieceWords - 1) / kMaxPieceWords);
     pieces.clear();
@@ -485,7 +504,8 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     uint32_t T = (uint32_t)(cps * kWarpsPerCta * I.num_sms);
     if (r.max_pieces) T = std::min(T, r.max_pieces);
     const uint64_t W = (uint64_t)I.S * r.L;
-    const bool need_jumps = pieces_wanted(W, T, (uint64_t)I.num_sms * kWarpsPerCta, r.min_piece_words) > I.S ||
+    const bool need_jumps =
+        pieces_wanted(W, r.L, T, (uint64_t)I.num_sms * kWarpsPerCta, r.min_piece_words, I.jump_k) > I.S ||
                             r.L > kMaxPieceWords;
     cudaError_t e;
     if (need_jumps && !I.analyzed) {
