@@ -366,6 +366,7 @@ int generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
         run.stream = ctx->stream;
         run.max_pieces = ctx->max_pieces;
         run.min_piece_words = ctx->min_piece_words;
+        run.words_done = ctx->position.empty() ? 0 : *std::min_element(ctx->position.begin(), ctx->position.end());
         run.timing = ctx->timing ? &ctx->pool : nullptr;
         // Engine::mt contexts: 5 / 6 pick the warp-team kernel, the MTGP kernel numbers mean auto
         run.want_kernel = ctx->engine == 1 ? (ctx->kernel >= 5 ? ctx->kernel : 0) : ctx->kernel;

@@ -78,15 +78,20 @@ constexpr uint64_t kMaxPieceWords = 1ull << 30;
 // r words/s, the whole GPU G, and one jump costs the GPU as much as J generated words.
 // jump_k = G / (r J); ~3.8e-3 at 11213, lower where jumps cost more (PlannerImpl::init_jump).
 // Only streams of >= 2^19 words per call are split this way: below that one warp finishes in
-// less time than the prefix + jump launches take (~0.1 ms).
-uint64_t pieces_wanted(uint64_t W, uint64_t L, uint64_t T, uint64_t quantum, uint64_t min_piece, double jump_k) {
+// less time than the prefix + jump launches take (~0.1 ms). And only once every stream has
+// produced 2^25 words: the first split pays the one-off annihilator analysis and jump
+// polynomials (13-45 ms, profiles/r1_first_call.jsonl), which a short-lived source (a sieve cell's
+// make_word_source, 10^7 words) would not win back.
+constexpr uint64_t kLongLivedWords = 1ull << 25;
+uint64_t pieces_wanted(uint64_t W, uint64_t L, uint64_t T, uint64_t quantum, uint64_t min_piece, double jump_k,
+                       uint64_t words_done) {
     uint64_t w;
     if (min_piece) {
         w = W / min_piece;
     } else {
         w = W >> 21;
         if ((W >> 19) >= 3 * quantum) w = std::max<uint64_t>(w, 3 * quantum);
-        if (w < quantum && jump_k > 0 && L >= (1ull << 19))
+        if (w < quantum && jump_k > 0 && L >= (1ull << 19) && words_done >= kLongLivedWords)
             w = std::max<uint64_t>(w, std::min<uint64_t>(quantum, (uint64_t)std::sqrt((double)W * jump_k)));
     }
     return std::min<uint64_t>(T, std::max<uint64_t>(1, w));
@@ -185,7 +190,7 @@ struct PlannerImpl {
         }
         return mt ? launch_jump_rt(a, N, st) : launch_jump(M, a, n_rows, st);
     }
-    cudaError_t build_plan(uint64_t L, uint32_t T, uint64_t min_piece, std::string& err);
+    cudaError_t build_plan(uint64_t L, uint32_t T, uint64_t min_piece, uint64_t words_done, std::string& err);
 };
 
 Planner::Planner(const std::vector<mtgp_params>& sets, int num_sms) : impl_(new PlannerImpl) {
@@ -314,13 +319,14 @@ cudaError_t PlannerImpl::analyze(const void* params, const uint32_t* win, cudaSt
     return cudaSuccess;
 }
 
-cudaError_t PlannerImpl::build_plan(uint64_t L, uint32_t T, uint64_t min_piece, std::string& err) {
+cudaError_t PlannerImpl::build_plan(uint64_t L, uint32_t T, uint64_t min_piece, uint64_t words_done,
+                                    std::string& err) {
     if (plan_valid && plan_L == L && plan_T == T) return cudaSuccess;
     const uint64_t W = (uint64_t)S * L;
     // Equal work per SM: team counts are whole multiples of (SMs x warps per CTA), so every SM
     // holds the same number of CTAs (a 5-vs-6 CTA split costs ~10% of the makespan).
     const uint64_t quantum = (uint64_t)num_sms * kWarpsPerCta;
-    uint64_t want = pieces_wanted(W, L, T, quantum, min_piece, jump_k);
+    uint64_t want = pieces_wanted(W, L, T, quantum, min_piece, jump_k, words_done);
     if (want >= quantum) want -= want % quantum;
     want = std::max<uint64_t>(want, (W + kMaxPieceWords - 1) / kMaxPieceWords);
     pieces.clear();
@@ -505,14 +511,14 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     if (r.max_pieces) T = std::min(T, r.max_pieces);
     const uint64_t W = (uint64_t)I.S * r.L;
     const bool need_jumps =
-        pieces_wanted(W, r.L, T, (uint64_t)I.num_sms * kWarpsPerCta, r.min_piece_words, I.jump_k) > I.S ||
+        pieces_wanted(W, r.L, T, (uint64_t)I.num_sms * kWarpsPerCta, r.min_piece_words, I.jump_k, r.words_done) > I.S ||
                             r.L > kMaxPieceWords;
     cudaError_t e;
     if (need_jumps && !I.analyzed) {
         if ((e = I.analyze(r.params, r.win, r.stream, err)) != cudaSuccess) return e;
         if (!err.empty()) return cudaSuccess;
     }
-    if ((e = I.build_plan(r.L, need_jumps ? T : I.S, r.min_piece_words, err)) != cudaSuccess) return e;
+    if ((e = I.build_plan(r.L, need_jumps ? T : I.S, r.min_piece_words, r.words_done, err)) != cudaSuccess) return e;
     if (!err.empty()) return cudaSuccess;
 
     // per-piece start-window pointers: jumped pieces -> d_pwin rows; offset-0 pieces -> current window
