@@ -144,6 +144,8 @@ public:
     void generate_host(OutputKind kind, void* out, std::uint64_t words_per_stream);
     /// same into device memory (asynchronous on the context stream).
     void generate_device(OutputKind kind, void* device_out, std::uint64_t words_per_stream);
+    /// generate_host without waiting (mtgp_generate_async): out is valid after synchronize().
+    void generate_host_async(OutputKind kind, void* out, std::uint64_t words_per_stream);
     void skip(std::uint64_t words);
     std::uint64_t position(std::uint32_t s) const;
     std::vector<mtgp_cksum> checksums() const;
@@ -172,6 +174,9 @@ public:
     /// Engine::mt stream: the GPU counterpart of MtWordSource itself (word_source.hpp:27-37).
     GpuWordSource(const MtStatus& params, std::uint32_t seed, OutputKind kind = OutputKind::u32,
                   int device = 0, std::size_t chunk_words = std::size_t{1} << 20);
+    ~GpuWordSource() override;
+    GpuWordSource(const GpuWordSource&) = delete;
+    GpuWordSource& operator=(const GpuWordSource&) = delete;
     void fill(std::span<std::uint32_t> out) override;
     std::uint32_t next_u32();
     /// next_u32() / 2^32 in [0, 1), draw for draw (generator.hpp:39-41).
@@ -182,7 +187,15 @@ private:
     void refill();
     StreamBatch batch_;
     OutputKind kind_;
-    std::vector<std::uint32_t> buf_;
+    // two refill buffers in page-locked memory (mtgp_host_alloc): the consumer reads buf_[cur_]
+    // while the next chunk is generated and copied into buf_[cur_ ^ 1] (mtgp_generate_async)
+    struct PinnedFree {
+        void operator()(std::uint32_t* p) const;
+    };
+    std::unique_ptr<std::uint32_t[], PinnedFree> buf_[2];
+    int cur_ = 0;
+    bool pending_ = false;  // a chunk is in flight into buf_[cur_ ^ 1]
+    std::size_t cap_ = 0;
     std::size_t pos_ = 0, len_ = 0;
     std::uint64_t consumed_ = 0;
 };

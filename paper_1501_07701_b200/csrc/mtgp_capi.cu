@@ -389,9 +389,24 @@ int mtgpb::ctx_generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
     return generate_device(ctx, kind, out, L);
 }
 
+namespace {
+int generate_impl(mtgp_ctx* ctx, int kind, void* out, uint64_t L, int out_is_device, bool wait);
+}
+
 extern "C" {
 
 int mtgp_generate(mtgp_ctx* ctx, int kind, void* out, uint64_t L, int out_is_device) {
+    return generate_impl(ctx, kind, out, L, out_is_device, true);
+}
+
+int mtgp_generate_async(mtgp_ctx* ctx, int kind, void* out, uint64_t L, int out_is_device) {
+    return generate_impl(ctx, kind, out, L, out_is_device, false);
+}
+
+}  // extern "C"
+
+namespace {
+int generate_impl(mtgp_ctx* ctx, int kind, void* out, uint64_t L, int out_is_device, bool wait) {
     if (!ctx) return fail(MTGP_EINVAL, "null context");
     if (kind < MTGP_U32 || kind > MTGP_F64_01) return fail(MTGP_EINVAL, "unknown output kind %d", kind);
     if (!out && L) return fail(MTGP_EINVAL, "null output");
@@ -424,12 +439,13 @@ int mtgp_generate(mtgp_ctx* ctx, int kind, void* out, uint64_t L, int out_is_dev
     // ~1/64 of a chunk's generation instead of a whole one (generation outruns PCIe ~20x, so
     // the ramp never starves the copy). Lengths stay multiples of 4 words (v3 eligibility).
     uint64_t next_len = single ? Lc : std::max<uint64_t>(std::min<uint64_t>(Lc, 4096), (Lc >> 6) & ~3ull);
-    int c = 0;
-    for (uint64_t done = 0, len = 0; done < L; done += len, ++c) {
+    for (uint64_t done = 0, len = 0; done < L; done += len) {
         len = std::min<uint64_t>(next_len, L - done);
         next_len = std::min<uint64_t>(Lc, next_len * 16);
-        const int b = c & 1;
-        char* stage = static_cast<char*>(ctx->d_stage) + b * chunk_bytes;
+        const int b = (int)(ctx->stage_next++ & 1);
+        // halves of the stage at fixed offsets: a chunk never overlaps the other half, whose copy
+        // may still be in flight from an earlier (asynchronous) call with another chunk size
+        char* stage = static_cast<char*>(ctx->d_stage) + b * (ctx->stage_bytes / 2);
         // buffer b is free once its previous copy finished
         CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_copy[b], 0), "wait");
         int rc = generate_device(ctx, kind, stage, len);
@@ -441,9 +457,12 @@ int mtgp_generate(mtgp_ctx* ctx, int kind, void* out, uint64_t L, int out_is_dev
            "D2H copy");
         CK(cudaEventRecord(ctx->ev_copy[b], ctx->copy_stream), "event");
     }
-    CK(cudaStreamSynchronize(ctx->copy_stream), "sync");
+    if (wait) CK(cudaStreamSynchronize(ctx->copy_stream), "sync");
     return MTGP_OK;
 }
+}  // namespace
+
+extern "C" {
 
 int mtgp_generate_u32(mtgp_ctx* ctx, uint32_t* out, uint64_t L, int out_is_device) {
     return mtgp_generate(ctx, MTGP_U32, out, L, out_is_device);
@@ -541,6 +560,19 @@ int mtgp_checksums_reset(mtgp_ctx* ctx) {
     if (!ctx) return fail(MTGP_EINVAL, "null context");
     CK(cudaSetDevice(ctx->device), "cudaSetDevice");
     CK(cudaMemsetAsync(ctx->d_ck, 0, sizeof(DevCksum) * ctx->n_sets, ctx->stream), "memset");
+    return MTGP_OK;
+}
+
+int mtgp_host_alloc(size_t bytes, void** out) {
+    if (!out) return fail(MTGP_EINVAL, "null output pointer");
+    *out = nullptr;
+    if (bytes == 0) return MTGP_OK;
+    CK(cudaHostAlloc(out, bytes, cudaHostAllocPortable), "cudaHostAlloc");
+    return MTGP_OK;
+}
+
+int mtgp_host_free(void* p) {
+    if (p) CK(cudaFreeHost(p), "cudaFreeHost");
     return MTGP_OK;
 }
 

@@ -38,6 +38,7 @@ struct mtgp_ctx {
     bool cksum = true;
     int kernel = 0;
     int jump_mode = 0;  // MTGP_OPT_JUMP
+    uint32_t stage_next = 0;  // host output: the staging buffer the next chunk uses (alternates across calls)
     uint32_t max_pieces = 0;
     uint64_t min_piece_words = 0;  // 0 = auto (pieces_wanted, mtgp_plan.cu)
     bool timing = false;

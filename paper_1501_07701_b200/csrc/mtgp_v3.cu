@@ -210,11 +210,13 @@ __device__ __forceinline__ void step3(const V3Ctx& p, const uint4& h1, const uin
     }
 }
 
-// packed (A, B) accumulators -> the exact sum of the words they saw (MTGP3_CK_HILO)
+#if MTGP3_CK_HILO
+// packed (A, B) accumulators -> the exact sum of the words they saw
 __device__ __forceinline__ unsigned long long hilo_sum(unsigned long long packed) {
     const uint32_t a = (uint32_t)packed, b = (uint32_t)(packed >> 32);
     return ((unsigned long long)b << 16) + (uint32_t)(a - (b << 16));
 }
+#endif
 
 template <int RC, int KIND, bool CK>
 __device__ __forceinline__ void run3(const V3Ctx& p, uint4 X0, uint4 X1, uint4 Y1, uint32_t* optr, uint32_t len,

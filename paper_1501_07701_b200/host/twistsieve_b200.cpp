@@ -478,6 +478,10 @@ void StreamBatch::generate_host(OutputKind kind, void* out, std::uint64_t words)
     check(mtgp_generate(ctx_, static_cast<int>(kind), out, words, 0), "mtgp_generate");
 }
 
+void StreamBatch::generate_host_async(OutputKind kind, void* out, std::uint64_t words) {
+    check(mtgp_generate_async(ctx_, static_cast<int>(kind), out, words, 0), "mtgp_generate_async");
+}
+
 void StreamBatch::generate_device(OutputKind kind, void* out, std::uint64_t words) {
     check(mtgp_generate(ctx_, static_cast<int>(kind), out, words, 1), "mtgp_generate");
 }
@@ -522,35 +526,59 @@ void StreamBatch::set_option(int option, std::int64_t value) {
 void StreamBatch::synchronize() { check(mtgp_sync(ctx_), "mtgp_sync"); }
 
 // ---------------------------------------------------------------------------------------------
+void GpuWordSource::PinnedFree::operator()(std::uint32_t* p) const { mtgp_host_free(p); }
+
+namespace {
+std::uint32_t* pinned_words(std::size_t n) {
+    void* p = nullptr;
+    check(mtgp_host_alloc(n * sizeof(std::uint32_t), &p), "mtgp_host_alloc");
+    return static_cast<std::uint32_t*>(p);
+}
+}  // namespace
+
+// chunk_words is rounded up to a multiple of 4: the register-resident kernels take L % 4 == 0
 GpuWordSource::GpuWordSource(const MtgpStatus& params, std::uint32_t seed, OutputKind kind, int device,
                              std::size_t chunk_words)
-    : batch_({params}, {seed}, device), kind_(kind), buf_(std::max<std::size_t>(chunk_words, 256)) {}
+    : batch_({params}, {seed}, device), kind_(kind), cap_((std::max<std::size_t>(chunk_words, 256) + 3) & ~std::size_t{3}) {
+    buf_[0].reset(pinned_words(cap_));
+    buf_[1].reset(pinned_words(cap_));
+}
 
 GpuWordSource::GpuWordSource(const MtStatus& params, std::uint32_t seed, OutputKind kind, int device,
                              std::size_t chunk_words)
-    : batch_(std::vector<MtStatus>{params}, {seed}, device), kind_(kind), buf_(std::max<std::size_t>(chunk_words, 256)) {}
+    : batch_(std::vector<MtStatus>{params}, {seed}, device), kind_(kind),
+      cap_((std::max<std::size_t>(chunk_words, 256) + 3) & ~std::size_t{3}) {
+    buf_[0].reset(pinned_words(cap_));
+    buf_[1].reset(pinned_words(cap_));
+}
 
+GpuWordSource::~GpuWordSource() {
+    // a chunk may still be in flight into a buffer that is about to be freed
+    if (pending_) mtgp_sync(batch_.handle());
+}
+
+// The stream's words arrive chunk by chunk: buf_[cur_] (being read), then the chunk in flight
+// into buf_[cur_ ^ 1]. A refill waits for that chunk, switches to it, and starts the next one.
 void GpuWordSource::refill() {
-    batch_.generate_host(kind_, buf_.data(), buf_.size());
+    if (!pending_) {  // first refill: nothing in flight yet
+        batch_.generate_host_async(kind_, buf_[cur_ ^ 1].get(), cap_);
+        pending_ = true;
+    }
+    batch_.synchronize();
+    cur_ ^= 1;
     pos_ = 0;
-    len_ = buf_.size();
+    len_ = cap_;
+    batch_.generate_host_async(kind_, buf_[cur_ ^ 1].get(), cap_);
 }
 
 void GpuWordSource::fill(std::span<std::uint32_t> out) {
+    // every word passes through the page-locked buffers: a direct device->host copy into the
+    // caller's (pageable) span is slower than the copy out of a pinned buffer
     std::size_t done = 0;
     while (done < out.size()) {
-        if (pos_ == len_) {
-            const std::size_t rest = out.size() - done;
-            if (rest >= buf_.size()) {
-                // large request: generate straight into the caller's span
-                batch_.generate_host(kind_, out.data() + done, rest);
-                done += rest;
-                break;
-            }
-            refill();
-        }
+        if (pos_ == len_) refill();
         const std::size_t n = std::min(len_ - pos_, out.size() - done);
-        std::memcpy(out.data() + done, buf_.data() + pos_, n * sizeof(std::uint32_t));
+        std::memcpy(out.data() + done, buf_[cur_].get() + pos_, n * sizeof(std::uint32_t));
         pos_ += n;
         done += n;
     }
@@ -560,7 +588,7 @@ void GpuWordSource::fill(std::span<std::uint32_t> out) {
 std::uint32_t GpuWordSource::next_u32() {
     if (pos_ == len_) refill();
     ++consumed_;
-    return buf_[pos_++];
+    return buf_[cur_][pos_++];
 }
 
 std::unique_ptr<WordSource> make_word_source(const MtgpStatus& params, std::uint32_t seed) {

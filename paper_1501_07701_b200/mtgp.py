@@ -37,6 +37,7 @@ EXPORTS = (
     "mtgp_ln_gamma", "mtgp_gamma_p", "mtgp_gamma_q", "mtgp_chi_square_pvalue", "mtgp_poisson_cdf",
     "mtgp_poisson_sf", "mtgp_poisson_pmf", "mtgp_binomial_log_pmf", "mtgp_binomial_upper_tail",
     "mtgp_classify_pvalue", "mtgp_certify", "mtgp_mt_charpoly_digest", "mtgp_gf2_is_irreducible",
+    "mtgp_host_alloc", "mtgp_host_free", "mtgp_generate_async",
 )
 
 
