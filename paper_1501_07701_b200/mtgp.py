@@ -106,6 +106,9 @@ def load_library(path: Optional[str] = None) -> C.CDLL:
     lib.mtgp_ctx_stream.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
     lib.mtgp_set_option.argtypes = [C.c_void_p, C.c_int, C.c_int64]
     lib.mtgp_generate.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_int]
+    lib.mtgp_generate_async.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_int]
+    lib.mtgp_host_alloc.argtypes = [C.c_size_t, C.POINTER(C.c_void_p)]
+    lib.mtgp_host_free.argtypes = [C.c_void_p]
     lib.mtgp_skip.argtypes = [C.c_void_p, C.c_uint64]
     lib.mtgp_state_save.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
     lib.mtgp_state_restore.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -240,6 +243,13 @@ class MtgpContext:
         _check(self.lib, self.lib.mtgp_generate(self.h, kind, out.ctypes.data_as(C.c_void_p),
                                                 words_per_stream, 0))
         return out
+
+    def generate_host_async(self, kind: int, out: np.ndarray) -> None:
+        """mtgp_generate_async into host memory `out` (n_sets, L): valid after sync(). Keep `out`
+        alive (and preferably page-locked) until then."""
+        assert out.flags.c_contiguous and out.size % self.n_sets == 0
+        _check(self.lib, self.lib.mtgp_generate_async(self.h, kind, out.ctypes.data_as(C.c_void_p),
+                                                      out.size // self.n_sets, 0))
 
     def fill_u32(self, L: int) -> np.ndarray:
         return self.generate_host(U32, L)

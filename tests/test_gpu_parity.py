@@ -365,3 +365,29 @@ def test_other_mtgp_exponents_cta_per_stream(mexp):
     assert np.array_equal(a, ref[:, :5001])
     assert np.array_equal(b, ref[:, 5001:6000]) and np.array_equal(b2, b)
     assert np.array_equal(c, ref[:, 6000 + 12345:])
+
+
+def test_async_host_generation_into_pinned_buffers(curand_sets):
+    """mtgp_generate_async + mtgp_host_alloc (GpuWordSource's double buffering): two chunks in
+    flight into two page-locked buffers, both valid after mtgp_sync, in stream order."""
+    import ctypes as C
+    sets = curand_sets[20:22]
+    L = 1 << 18
+    with mtgp.MtgpContext(sets, [3, 4]) as ctx:
+        lib = ctx.lib
+        ptrs = []
+        for _ in range(2):
+            p = C.c_void_p()
+            assert lib.mtgp_host_alloc(2 * L * 4, C.byref(p)) == 0
+            ptrs.append(p)
+        bufs = [np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_uint32)), shape=(2, L)) for p in ptrs]
+        try:
+            ctx.generate_host_async(mtgp.U32, bufs[0])
+            ctx.generate_host_async(mtgp.U32, bufs[1])
+            ctx.sync()
+            got = np.concatenate([bufs[0], bufs[1]], axis=1).copy()
+        finally:
+            for p in ptrs:
+                lib.mtgp_host_free(p)
+    ref, _ = oracle_py.mtgp_bulk(sets, [3, 4], 2 * L, threads=2)
+    assert np.array_equal(got, ref)
