@@ -46,6 +46,10 @@ namespace mtgpb {
 #ifndef MTGP3_CK_HILO
 #define MTGP3_CK_HILO 0
 #endif
+// float kinds: the [1,2) conversion as I2F.RZ + FFMA.RZ instead of LEA.HI on the ALU pipe
+#ifndef MTGP3_FLT_FMA
+#define MTGP3_FLT_FMA 0
+#endif
 // x << sh1 as a shift on the ALU pipe instead of an IMAD by 2^sh1 on the FMA pipe
 #ifndef MTGP3_SH1_SHF
 #define MTGP3_SH1_SHF 0
@@ -115,7 +119,14 @@ __device__ __forceinline__ void fold2(uint32_t t1, uint32_t t2, uint32_t& i1, ui
 template <int KIND>
 __device__ __forceinline__ uint32_t conv3(const V3Ctx& p, uint32_t o) {
     if (KIND == MTGP_U32) return o;
+#if MTGP3_FLT_FMA
+    // (o >> 9) | 0x3F800000 on the FMA pipe, bit-exact: I2F.RZ keeps o's top 24 significant
+    // bits (what it drops is below bit 9), and the FFMA.RZ with 1.0 truncates 1 + o * 2^-32 to
+    // 23 fraction bits, i.e. 1 + floor(o / 2^9) * 2^-23
+    uint32_t v = __float_as_uint(__fmaf_rz(__uint2float_rz(o), 2.3283064365386963e-10f, 1.0f));
+#else
     uint32_t v = (o >> 9) | 0x3F800000u;
+#endif
     if (KIND == MTGP_F32_01OC) v = __float_as_uint(2.0f - __uint_as_float(v));
     return v;
 }
