@@ -91,4 +91,8 @@ int set_error(int code, const char* fmt, ...);
 int cuda_error(cudaError_t e, const char* what);
 // One device-side generation of L words per stream into device memory `out` (advances positions).
 int ctx_generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L);
+// The same L words per stream, but only bit 0 of each word into `bitmap` (kKindBitmapBit0; per
+// stream ceil(L / 32) words, which the caller zeroes). MTGP32-11213 warp-team contexts only
+// (gen3); MTGP_EINVAL elsewhere.
+int ctx_generate_bitmap(mtgp_ctx* ctx, uint32_t* bitmap, uint64_t L);
 }  // namespace mtgpb

@@ -23,6 +23,12 @@ struct alignas(16) DevParams {
     uint32_t tmp[16];
 };
 
+// Internal output kind (not in the ABI) for the device-side random-walk test: instead of the
+// words, one bit per word (bit 0 of the word) into a per-stream bitmap (stride ceil(L / 32)
+// words; bit j of the call's words at word j / 32, bit j % 32). Only gen3 (MTGP32-11213)
+// produces it; the walk pass falls back to words elsewhere.
+constexpr int kKindBitmapBit0 = 16;
+
 struct DevCksum {
     unsigned long long sum64;
     unsigned long long words;

@@ -456,6 +456,11 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     // 16-byte aligned output, L % 4 == 0 (piece offsets are multiples of 4 by construction)
     const bool reg_ok = !I.mt && r.L % 4 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 15) == 0;
     const bool v3_ok = I.M == 11213 && reg_ok;
+    const bool bitmap = r.kind >= kKindBitmapBit0;
+    if (bitmap && (!v3_ok || (r.want_kernel != 0 && r.want_kernel != 3))) {
+        err = "bitmap output needs kernel v3 (mexp 11213, words_per_stream % 4 == 0)";
+        return cudaSuccess;
+    }
     // v5 (gen3 with 8 consecutive words per lane, one 256-bit store per step): 32-byte pieces
     const bool v5_ok = v3_ok && r.L % 8 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 31) == 0 && I.t0 % 8 == 0;
     const bool v4_ok = v4_supports(I.M, r.kind) && reg_ok;
@@ -494,7 +499,7 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     // auto: v3 for 11213; v4 (the same register-resident design, templated on N) for 23209 and
     // 44497, where it beats the shared-memory ring by 18% / 27% (profiles/r1_v4_sweep.jsonl);
     // v2 for request shapes the register kernels do not take (float kinds, L % 4 != 0, ...)
-    const bool use_v5 = v5_ok && r.want_kernel == 7;
+    const bool use_v5 = v5_ok && r.want_kernel == 7 && !bitmap;
     const bool use_v3 = !use_v5 && v3_ok && (r.want_kernel == 3 || (r.want_kernel == 0 && I.M == 11213));
     const bool use_v4 = !use_v5 && !use_v3 && v4_ok && (r.want_kernel == 4 || (r.want_kernel == 0 && I.M != 11213));
     const int cps = use_mt3  ? mt_gen3_ctas_per_sm(I.N, r.kind, r.cksum)

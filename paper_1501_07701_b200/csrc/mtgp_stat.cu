@@ -89,6 +89,39 @@ __global__ void __launch_bounds__(kThreads) walk_kernel(const uint32_t* __restri
     }
 }
 
+// The same walks from a bit-0 bitmap the generator wrote directly (ctx_generate_bitmap,
+// kKindBitmapBit0): the chunk's words never reach HBM. Bit j of a stream's bitmap is word j of
+// its chunk; one thread per walk popcounts its l bits.
+template <bool SMEM_HIST>
+__global__ void __launch_bounds__(kThreads) walk_bm_kernel(const uint32_t* __restrict__ bm, uint64_t bm_stride,
+                                                           uint32_t l, uint32_t wpt, uint64_t walk0, uint64_t n,
+                                                           unsigned long long* __restrict__ counts) {
+    extern __shared__ uint32_t sm[];
+    uint32_t* hist = sm;
+    const uint32_t st = blockIdx.y;
+    const uint64_t first_walk = walk0 + (uint64_t)blockIdx.x * wpt;
+    if (first_walk >= n) return;
+    const uint32_t* b = bm + (size_t)st * bm_stride;
+    if (SMEM_HIST) {
+        for (uint32_t i = threadIdx.x; i <= l; i += kThreads) hist[i] = 0;
+        __syncthreads();
+    }
+    unsigned long long* cs = counts + (size_t)st * (l + 1);
+    for (uint32_t t = threadIdx.x; t < wpt && first_walk + t < n; t += kThreads) {
+        const uint32_t a = (blockIdx.x * wpt + t) * l;
+        const uint32_t h = range_popc(b, a, a + l);
+        if (SMEM_HIST)
+            atomicAdd(hist + h, 1u);
+        else
+            atomicAdd(cs + h, 1ull);
+    }
+    if (SMEM_HIST) {
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i <= l; i += kThreads)
+            if (hist[i]) atomicAdd(cs + i, (unsigned long long)hist[i]);
+    }
+}
+
 // ---------------------------------------------------------------------------------------------
 // Hamming-weight independence (stat_tests.hpp:149-208): s-bit letters concatenated MSB first
 // into L-bit blocks; blocks (2i, 2i+1) form pair i. A CTA takes ppt whole pairs (tile_words
@@ -576,6 +609,12 @@ void generate_chunk(mtgp_ctx* ctx, uint32_t* buf, uint64_t C) {
     if (rc) throw Failure{rc};
 }
 
+// The generator can write the bit-0 bitmap instead of words (gen3: MTGP32-11213 warp teams)
+bool bitmap_fusable(const mtgp_ctx* ctx, uint64_t C) {
+    return ctx->engine == 0 && ctx->mexp == 11213 && (ctx->kernel == 0 || ctx->kernel == 3) && ctx->planner &&
+           ctx->planner->v2_supported() && C % 4 == 0;
+}
+
 void launched(mtgp_ctx* ctx, const char* what) {
     check(cudaGetLastError(), what);
     ctx->total_launches += 1;
@@ -602,6 +641,29 @@ void run_walk(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res) {
     DevBuf counts;
     Arena ar;
     ar.add(counts, (size_t)S * (l + 1) * 8);
+    if (bitmap_fusable(ctx, C)) {
+        // fused: the generator writes only the bit-0 bitmap (1/32 of the chunk's bytes)
+        const uint64_t bm_stride = (C + 31) / 32;
+        uint32_t* const bm = ar.commit(ctx, (size_t)S * bm_stride * 4);
+        check(cudaMemsetAsync(counts.p, 0, (size_t)S * (l + 1) * 8, ctx->stream), "memset");
+        auto kb = smem_hist ? walk_bm_kernel<true> : walk_bm_kernel<false>;
+        const size_t smem_b = smem_hist ? 4 * (size_t)(l + 1) : 0;
+        check(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b), "smem attribute");
+        for (uint64_t c = 0; c < chunks; ++c) {
+            check(cudaMemsetAsync(bm, 0, (size_t)S * bm_stride * 4, ctx->stream), "memset bitmap");
+            const int rc = ctx_generate_bitmap(ctx, bm, C);
+            if (rc) throw Failure{rc};
+            kb<<<dim3(tpc, S), kThreads, smem_b, ctx->stream>>>(bm, bm_stride, l, wpt, c * tpc * wpt, sp.n,
+                                                               counts.as<unsigned long long>());
+            launched(ctx, "walk bitmap kernel");
+        }
+        const auto h = fetch(ctx, counts, (size_t)S * (l + 1));
+        for (uint32_t s = 0; s < S; ++s) {
+            stat::finish(sp, h.data() + (size_t)s * (l + 1), res + s);
+            res[s].words_used = stat::words_needed(sp);
+        }
+        return;
+    }
     uint32_t* const wbuf = ar.commit(ctx, (size_t)S * C * 4);
     check(cudaMemsetAsync(counts.p, 0, (size_t)S * (l + 1) * 8, ctx->stream), "memset");
     auto k = smem_hist ? walk_kernel<true> : walk_kernel<false>;
@@ -727,6 +789,9 @@ void run_gap(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res) {
     ar.add(pre, (size_t)S * T * sizeof(GapPre));
     ar.add(state, (size_t)S * sizeof(GapState));
     ar.add(end, (size_t)S * 8);
+    // (the gap test stays on words: a generator-written hit bitmap measured 21.8 vs 20.5 ms for the
+    // desk test -- the bitmap step costs the generator more than the count pass it saves;
+    // DESIGN.md 4.5)
     uint32_t* const wbuf = ar.commit(ctx, (size_t)S * C * 4);
     check(cudaMemsetAsync(counts.p, 0, (size_t)S * (tcut + 1) * 8, ctx->stream), "memset");
     std::vector<GapState> hs(S, GapState{0, -1, 0, 0, 0});

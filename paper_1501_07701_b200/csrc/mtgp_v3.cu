@@ -72,6 +72,9 @@ struct V3Ctx {
     bool pA0, pA1, pC0, pC1;              // "take the newer half-step" predicates
     uint32_t mA0, mA1, mC0, mC1;          // the same as 0/1 multipliers (MTGP3_SEL_IMAD)
     uint32_t nA0, nA1, nC0, nC1;          // 1 - m
+    // bitmap kind: this stream's bitmap, the piece's first word within the call
+    uint32_t* bm;
+    unsigned long long poff;
 };
 
 __device__ __forceinline__ uint32_t comp4(const uint4& g, int c) {
@@ -118,7 +121,7 @@ __device__ __forceinline__ void fold2(uint32_t t1, uint32_t t2, uint32_t& i1, ui
 
 template <int KIND>
 __device__ __forceinline__ uint32_t conv3(const V3Ctx& p, uint32_t o) {
-    if (KIND == MTGP_U32) return o;
+    if (KIND == MTGP_U32 || KIND >= kKindBitmapBit0) return o;
 #if MTGP3_FLT_FMA
     // (o >> 9) | 0x3F800000 on the FMA pipe, bit-exact: I2F.RZ keeps o's top 24 significant
     // bits (what it drops is below bit 9), and the FFMA.RZ with 1.0 truncates 1 + o * 2^-32 to
@@ -155,6 +158,32 @@ __device__ __forceinline__ void fetch5(uint32_t W[5], const uint4& h1, const uin
     }
 }
 
+// Bitmap kind: the half-step's 128 words (lane t holds words 4t..4t+3 starting at piece word hs)
+// become their 128 bit-0s in word order. Each lane packs its 4 bits into nibble t % 8 of a word;
+// three OR butterflies over 8-lane groups leave bitmap word q (words 32q..32q+31) in lane 8q; the
+// word is shifted by the piece's bit offset (funnel with lane 8q - 8's word) and ORed into the
+// stream's bitmap (pieces share boundary words, hence atomicOr: one per 32 words). Lane 1 writes
+// the fifth, partial word of a shifted half-step.
+template <int KIND>
+__device__ __forceinline__ void bitmap_store(const V3Ctx& p, const uint32_t o[4], uint32_t hs, bool valid) {
+    uint32_t nib = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) nib |= (o[c] & 1u) << c;
+    uint32_t v = valid ? nib << (4 * (p.lane & 7u)) : 0u;
+    v |= __shfl_xor_sync(FULL, v, 1);
+    v |= __shfl_xor_sync(FULL, v, 2);
+    v |= __shfl_xor_sync(FULL, v, 4);
+    // lanes 8q: v = bitmap word q; prev = word q - 1 (0 for q = 0); lane 1 gets word 3 for the tail
+    const uint32_t sh = (uint32_t)(p.poff & 31u);
+    uint32_t prev = __shfl_sync(FULL, v, (p.lane - 8u) & 31u);
+    const uint32_t m3 = __shfl_sync(FULL, v, 24);
+    prev = p.lane < 8 ? 0u : prev;
+    const bool lead = (p.lane & 7u) == 0;
+    const uint32_t w = lead ? __funnelshift_l(prev, v, sh) : (p.lane == 1 ? __funnelshift_l(m3, 0u, sh) : 0u);
+    const uint32_t widx = lead ? (p.lane >> 3) : 4u;
+    if (w != 0) atomicOr(p.bm + ((p.poff + hs) >> 5) + widx, w);
+}
+
 // One 256-word step. Reads history (h1: older step's upper half; h2/h3: newer step's halves),
 // returns the new step's two halves in n0/n1. Stores outputs when the chunk is inside the piece.
 template <int RC, int KIND, bool CK, bool TAIL>
@@ -184,7 +213,9 @@ __device__ __forceinline__ void step3(const V3Ctx& p, const uint4& h1, const uin
         for (int c = 0; c < 4; ++c) o[c] = conv3<KIND>(p, temper3(p, r[c], WC[u][c]));
 #endif
         const uint32_t w0 = n + 128 * u + 4 * p.lane;  // piece word of o[0]
-        if (!TAIL || w0 < len) {
+        if constexpr (KIND >= kKindBitmapBit0) {
+            bitmap_store<KIND>(p, o, n + 128 * u, !TAIL || w0 < len);
+        } else if (!TAIL || w0 < len) {
             __stcs(reinterpret_cast<uint4*>(optr + w0), make_uint4(o[0], o[1], o[2], o[3]));
             if (CK) {
 #if MTGP3_CK_HILO
@@ -314,6 +345,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MTGP3_MIN_CTAS) gen3_kernel
         p.nC0 = 1u - p.mC0;
         p.nC1 = 1u - p.mC1;
         uint32_t* optr = reinterpret_cast<uint32_t*>(a.out) + (size_t)pc.set * a.L + pc.offset;
+        if (KIND >= kKindBitmapBit0) {
+            p.bm = reinterpret_cast<uint32_t*>(a.out) + (size_t)pc.set * ((a.L + 31) / 32);
+            p.poff = pc.offset;
+        }
         const uint32_t len = (uint32_t)pc.len;
         const uint32_t* w0 = a.piece_win[pi];
         // history before step 0: X = "step -1" = x_{95+p}, Y.upper = "step -2" upper = x_{-33+4t+c}
@@ -386,6 +421,8 @@ cudaError_t launch_gen3(int kind, bool cksum, const GenArgs& a, cudaStream_t st)
         case 4: return launch3_t<MTGP_F32_01OC, false>(a, st);
         case 5: return launch3_t<MTGP_F32_01OC, true>(a, st);
     }
+    // bitmap kinds carry no checksums (the words are never output)
+    if (kind == kKindBitmapBit0) return launch3_t<kKindBitmapBit0, false>(a, st);
     return cudaErrorInvalidValue;
 }
 
@@ -398,6 +435,7 @@ int gen3_ctas_per_sm(int kind, bool cksum) {
         case 4: return occ3_t<MTGP_F32_01OC, false>();
         case 5: return occ3_t<MTGP_F32_01OC, true>();
     }
+    if (kind == kKindBitmapBit0) return occ3_t<kKindBitmapBit0, false>();
     return 0;
 }
 
