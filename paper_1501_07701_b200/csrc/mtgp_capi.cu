@@ -317,9 +317,9 @@ namespace {
 // One device-side generation of L words per stream into device memory `out`.
 int generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
     if (L == 0) return MTGP_OK;
-    if (kind >= kKindBitmapBit0 &&
-        (ctx->engine != 0 || ctx->kernel == 1 || !ctx->planner || !ctx->planner->v2_supported()))
-        return fail(MTGP_EINVAL, "bitmap output needs the MTGP32 warp-team kernels");
+    if (kind >= kKindBitmapBit0 && (ctx->kernel == 1 || !ctx->planner || !ctx->planner->v2_supported() ||
+                                    (ctx->engine == 1 && (ctx->kernel == 5 || !ctx->planner->mt3_supported(kind, L, out)))))
+        return fail(MTGP_EINVAL, "bitmap output needs the register-resident warp-team kernels");
     // Engine::mt f64 (next_f64_01) rides the teams only on the register-resident kernel's shape
     const bool mt_teams = ctx->engine == 1 && ctx->kernel != 1 && ctx->planner && ctx->planner->v2_supported() &&
                           (kind != MTGP_F64_01 || ctx->kernel == 6 ||

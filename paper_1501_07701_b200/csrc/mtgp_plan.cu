@@ -457,10 +457,6 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     const bool reg_ok = !I.mt && r.L % 4 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 15) == 0;
     const bool v3_ok = I.M == 11213 && reg_ok;
     const bool bitmap = r.kind >= kKindBitmapBit0;
-    if (bitmap && (!v3_ok || (r.want_kernel != 0 && r.want_kernel != 3))) {
-        err = "bitmap output needs kernel v3 (mexp 11213, words_per_stream % 4 == 0)";
-        return cudaSuccess;
-    }
     // v5 (gen3 with 8 consecutive words per lane, one 256-bit store per step): 32-byte pieces
     const bool v5_ok = v3_ok && r.L % 8 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 31) == 0 && I.t0 % 8 == 0;
     const bool v4_ok = v4_supports(I.M, r.kind) && reg_ok;
@@ -488,6 +484,10 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         return cudaSuccess;
     }
     const bool use_mt3 = mt3_ok && r.want_kernel != 5;
+    if (bitmap && (I.mt ? !use_mt3 : (!v3_ok || (r.want_kernel != 0 && r.want_kernel != 3)))) {
+        err = "bitmap output needs kernel v3 (mexp 11213) or Engine::mt kernel 6, words_per_stream % 4 == 0";
+        return cudaSuccess;
+    }
     if (r.want_kernel == 3 && !v3_ok) {
         err = "kernel v3 needs mexp 11213, words_per_stream % 4 == 0 and 16-byte aligned output";
         return cudaSuccess;

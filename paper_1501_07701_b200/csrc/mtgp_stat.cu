@@ -609,10 +609,14 @@ void generate_chunk(mtgp_ctx* ctx, uint32_t* buf, uint64_t C) {
     if (rc) throw Failure{rc};
 }
 
-// The generator can write the bit-0 bitmap instead of words (gen3: MTGP32-11213 warp teams)
+// The generator can write the bit-0 bitmap instead of words: gen3 (MTGP32-11213) and mt_gen3
+// (Engine::mt, n = 624) warp teams
 bool bitmap_fusable(const mtgp_ctx* ctx, uint64_t C) {
-    return ctx->engine == 0 && ctx->mexp == 11213 && (ctx->kernel == 0 || ctx->kernel == 3) && ctx->planner &&
-           ctx->planner->v2_supported() && C % 4 == 0;
+    if (!ctx->planner || !ctx->planner->v2_supported() || C % 4 != 0) return false;
+    if (ctx->engine == 0) return ctx->mexp == 11213 && (ctx->kernel == 0 || ctx->kernel == 3);
+    // (the bitmap comes from cudaMalloc: any 256-byte aligned address stands in for it)
+    return (ctx->kernel == 0 || ctx->kernel == 6) &&
+           ctx->planner->mt3_supported(kKindBitmapBit0, C, reinterpret_cast<const void*>(uintptr_t{256}));
 }
 
 void launched(mtgp_ctx* ctx, const char* what) {

@@ -18,6 +18,7 @@
 //
 // Per 256-word step per warp: 20 operand SHFL + 16 table SHFL + 2 STG.128 (LSU data-pipe
 // wavefronts 44, vs 59 for the shared-memory ring of v2).
+#include "mtgp_bitmap.cuh"
 #include "mtgp_v2.cuh"
 
 namespace mtgpb {
@@ -158,32 +159,6 @@ __device__ __forceinline__ void fetch5(uint32_t W[5], const uint4& h1, const uin
     }
 }
 
-// Bitmap kind: the half-step's 128 words (lane t holds words 4t..4t+3 starting at piece word hs)
-// become their 128 bit-0s in word order. Each lane packs its 4 bits into nibble t % 8 of a word;
-// three OR butterflies over 8-lane groups leave bitmap word q (words 32q..32q+31) in lane 8q; the
-// word is shifted by the piece's bit offset (funnel with lane 8q - 8's word) and ORed into the
-// stream's bitmap (pieces share boundary words, hence atomicOr: one per 32 words). Lane 1 writes
-// the fifth, partial word of a shifted half-step.
-template <int KIND>
-__device__ __forceinline__ void bitmap_store(const V3Ctx& p, const uint32_t o[4], uint32_t hs, bool valid) {
-    uint32_t nib = 0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) nib |= (o[c] & 1u) << c;
-    uint32_t v = valid ? nib << (4 * (p.lane & 7u)) : 0u;
-    v |= __shfl_xor_sync(FULL, v, 1);
-    v |= __shfl_xor_sync(FULL, v, 2);
-    v |= __shfl_xor_sync(FULL, v, 4);
-    // lanes 8q: v = bitmap word q; prev = word q - 1 (0 for q = 0); lane 1 gets word 3 for the tail
-    const uint32_t sh = (uint32_t)(p.poff & 31u);
-    uint32_t prev = __shfl_sync(FULL, v, (p.lane - 8u) & 31u);
-    const uint32_t m3 = __shfl_sync(FULL, v, 24);
-    prev = p.lane < 8 ? 0u : prev;
-    const bool lead = (p.lane & 7u) == 0;
-    const uint32_t w = lead ? __funnelshift_l(prev, v, sh) : (p.lane == 1 ? __funnelshift_l(m3, 0u, sh) : 0u);
-    const uint32_t widx = lead ? (p.lane >> 3) : 4u;
-    if (w != 0) atomicOr(p.bm + ((p.poff + hs) >> 5) + widx, w);
-}
-
 // One 256-word step. Reads history (h1: older step's upper half; h2/h3: newer step's halves),
 // returns the new step's two halves in n0/n1. Stores outputs when the chunk is inside the piece.
 template <int RC, int KIND, bool CK, bool TAIL>
@@ -214,7 +189,7 @@ __device__ __forceinline__ void step3(const V3Ctx& p, const uint4& h1, const uin
 #endif
         const uint32_t w0 = n + 128 * u + 4 * p.lane;  // piece word of o[0]
         if constexpr (KIND >= kKindBitmapBit0) {
-            bitmap_store<KIND>(p, o, n + 128 * u, !TAIL || w0 < len);
+            bitmap_store_bit0(p.lane, p.bm, p.poff, o, n + 128 * u, !TAIL || w0 < len);
         } else if (!TAIL || w0 < len) {
             __stcs(reinterpret_cast<uint4*>(optr + w0), make_uint4(o[0], o[1], o[2], o[3]));
             if (CK) {
