@@ -370,6 +370,7 @@ int generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
         run.max_pieces = ctx->max_pieces;
         run.min_piece_words = ctx->min_piece_words;
         run.words_done = ctx->position.empty() ? 0 : *std::min_element(ctx->position.begin(), ctx->position.end());
+        run.pred = ctx->bm_pred;
         run.timing = ctx->timing ? &ctx->pool : nullptr;
         // Engine::mt contexts: 5 / 6 pick the warp-team kernel, the MTGP kernel numbers mean auto
         run.want_kernel = ctx->engine == 1 ? (ctx->kernel >= 5 ? ctx->kernel : 0) : ctx->kernel;
@@ -392,8 +393,9 @@ int mtgpb::ctx_generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
     return generate_device(ctx, kind, out, L);
 }
 
-int mtgpb::ctx_generate_bitmap(mtgp_ctx* ctx, uint32_t* bitmap, uint64_t L) {
-    return generate_device(ctx, kKindBitmapBit0, bitmap, L);
+int mtgpb::ctx_generate_bitmap(mtgp_ctx* ctx, int kind, uint32_t* bitmap, uint64_t L, const BitmapPred& pred) {
+    ctx->bm_pred = pred;
+    return generate_device(ctx, kind, bitmap, L);
 }
 
 namespace {

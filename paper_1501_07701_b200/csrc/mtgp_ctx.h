@@ -12,6 +12,7 @@
 #include "mtgp_mt.cuh"
 #include "mtgp_plan.h"
 
+using mtgpb::BitmapPred;
 using mtgpb::DevCksum;
 using mtgpb::DevMtParams;
 using mtgpb::DevParams;
@@ -38,6 +39,7 @@ struct mtgp_ctx {
     bool cksum = true;
     int kernel = 0;
     int jump_mode = 0;  // MTGP_OPT_JUMP
+    BitmapPred bm_pred;  // predicate of kKindBitmapRange (ctx_generate_bitmap)
     uint32_t stage_next = 0;  // host output: the staging buffer the next chunk uses (alternates across calls)
     uint32_t max_pieces = 0;
     uint64_t min_piece_words = 0;  // 0 = auto (pieces_wanted, mtgp_plan.cu)
@@ -91,8 +93,8 @@ int set_error(int code, const char* fmt, ...);
 int cuda_error(cudaError_t e, const char* what);
 // One device-side generation of L words per stream into device memory `out` (advances positions).
 int ctx_generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L);
-// The same L words per stream, but only bit 0 of each word into `bitmap` (kKindBitmapBit0; per
-// stream ceil(L / 32) words, which the caller zeroes). MTGP32-11213 warp-team contexts only
-// (gen3); MTGP_EINVAL elsewhere.
-int ctx_generate_bitmap(mtgp_ctx* ctx, uint32_t* bitmap, uint64_t L);
+// The same L words per stream, but only one predicate bit per word into `bitmap` (per stream
+// ceil(L / 32) words, which the caller zeroes): kKindBitmapBit0 / kKindBitmapRange with `pred`.
+// Register-resident warp-team contexts only (gen3, mt_gen3); MTGP_EINVAL elsewhere.
+int ctx_generate_bitmap(mtgp_ctx* ctx, int kind, uint32_t* bitmap, uint64_t L, const BitmapPred& pred);
 }  // namespace mtgpb

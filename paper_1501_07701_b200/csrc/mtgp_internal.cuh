@@ -23,11 +23,17 @@ struct alignas(16) DevParams {
     uint32_t tmp[16];
 };
 
-// Internal output kind (not in the ABI) for the device-side random-walk test: instead of the
-// words, one bit per word (bit 0 of the word) into a per-stream bitmap (stride ceil(L / 32)
-// words; bit j of the call's words at word j / 32, bit j % 32). Only gen3 (MTGP32-11213)
-// produces it; the walk pass falls back to words elsewhere.
-constexpr int kKindBitmapBit0 = 16;
+// Internal output kinds (not in the ABI) for the device-side stat tests: instead of the words,
+// one predicate bit per word into a per-stream bitmap (stride ceil(L / 32) words; bit j of the
+// call's words at word j / 32, bit j % 32). Only the register-resident team kernels produce
+// them (gen3: MTGP32-11213; mt_gen3: Engine::mt n = 624); the stat passes use words elsewhere.
+constexpr int kKindBitmapBit0 = 16;   // word & 1 (random walk)
+constexpr int kKindBitmapRange = 17;  // lo <= (word & mask) < hi (gap-test hits)
+struct BitmapPred {
+    uint32_t mask = 0xFFFFFFFFu;
+    uint32_t lo = 0;       // hit: ((word & mask) - lo) mod 2^32 <= span_m1, i.e.
+    uint32_t span_m1 = 0;  // lo <= (word & mask) < lo + span_m1 + 1 <= 2^32
+};
 
 struct DevCksum {
     unsigned long long sum64;

@@ -27,6 +27,7 @@ struct MtGenArgs {
     DevCksum* ck;
     uint32_t n;                        // state words (uniform over the context)
     bool pairs = false;                // two words per lane (L even, output 8-byte aligned)
+    BitmapPred pred;                   // kKindBitmapRange
 };
 // raw state words x_0 .. x_{len-1} of each row's stream (x_0..x_{n-1} = its window)
 cudaError_t launch_mt_prefix(const DevMtParams* params, const uint32_t* win, const uint32_t* sets, uint32_t n_rows,

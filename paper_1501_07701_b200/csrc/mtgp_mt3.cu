@@ -55,8 +55,9 @@ struct M6Ctx {
     uint32_t upper, a, b, c, u, l, mul_s, mul_t, hi_u, hi_l, one;
     uint32_t srcA0, srcA1, srcC0, srcC1;  // source lanes for carry e = 0 / 1
     bool pA0, pA1, pC0, pC1;              // "send the newer half-step of the pair"
-    uint32_t* bm;                         // kKindBitmapBit0: this stream's bitmap
-    unsigned long long poff;              // and the piece's first word within the call
+    uint32_t* bm;                         // bitmap kinds: this stream's bitmap,
+    unsigned long long poff;              // the piece's first word within the call, the predicate
+    BitmapPred pred;
 };
 
 __device__ __forceinline__ uint32_t comp6(const uint4& g, int c) {
@@ -119,8 +120,8 @@ __device__ __forceinline__ void step6(const M6Ctx& p, const uint4 (&Hs)[S6<NW>::
         o[c] = v;
     }
     const uint32_t w0 = n + 4 * p.lane;  // piece word of o[0]
-    if constexpr (KIND == kKindBitmapBit0) {
-        bitmap_store_bit0(p.lane, p.bm, p.poff, o, n, !TAIL || w0 < len);
+    if constexpr (KIND >= kKindBitmapBit0) {
+        bitmap_store<KIND>(p.lane, p.bm, p.poff, p.pred, o, n, !TAIL || w0 < len);
     } else if (!TAIL || w0 < len) {
         if (KIND == MTGP_F64_01) {
             // one 256-bit streaming store per lane (STG.E.EF.ENL2.256, sm_100): the warp's 1 KiB
@@ -251,9 +252,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MTGP6_MIN_CTAS) mt_gen3_ker
         // u32 words or doubles (2 words each): stream stride L samples, piece offset in samples
         constexpr uint32_t kW = KIND == MTGP_F64_01 ? 2 : 1;
         uint32_t* optr = reinterpret_cast<uint32_t*>(a.out) + kW * ((size_t)pc.set * a.L + pc.offset);
-        if (KIND == kKindBitmapBit0) {
+        if (KIND >= kKindBitmapBit0) {
             p.bm = reinterpret_cast<uint32_t*>(a.out) + (size_t)pc.set * ((a.L + 31) / 32);
             p.poff = pc.offset;
+            p.pred = a.pred;
         }
         const uint32_t len = (uint32_t)pc.len;
         const uint32_t* w0 = a.piece_win[pi];
@@ -294,7 +296,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MTGP6_MIN_CTAS) mt_gen3_ker
 }
 
 bool mt_gen3_supports(uint32_t n, uint32_t min_gap, int kind) {
-    return (kind == MTGP_U32 || kind == MTGP_F64_01 || kind == kKindBitmapBit0) && n == 624 && min_gap >= 129;
+    return (kind == MTGP_U32 || kind == MTGP_F64_01 || kind == kKindBitmapBit0 || kind == kKindBitmapRange) &&
+           n == 624 && min_gap >= 129;
 }
 
 template <int KIND, bool CK>
@@ -315,6 +318,10 @@ cudaError_t launch_mt_gen3(uint32_t n, int kind, bool cksum, const MtGenArgs& a,
         mt_gen3_kernel<624, kKindBitmapBit0, false><<<grid, block, 0, st>>>(a);
         return cudaGetLastError();
     }
+    if (kind == kKindBitmapRange) {
+        mt_gen3_kernel<624, kKindBitmapRange, false><<<grid, block, 0, st>>>(a);
+        return cudaGetLastError();
+    }
     switch ((kind == MTGP_F64_01 ? 2 : kind == MTGP_U32 ? 0 : 4) + (cksum ? 1 : 0)) {
         case 0: mt_gen3_kernel<624, MTGP_U32, false><<<grid, block, 0, st>>>(a); break;
         case 1: mt_gen3_kernel<624, MTGP_U32, true><<<grid, block, 0, st>>>(a); break;
@@ -330,6 +337,7 @@ int mt_gen3_ctas_per_sm(uint32_t n, int kind, bool cksum) {
     if (kind == MTGP_U32) return cksum ? mt3_occ<MTGP_U32, true>() : mt3_occ<MTGP_U32, false>();
     if (kind == MTGP_F64_01) return cksum ? mt3_occ<MTGP_F64_01, true>() : mt3_occ<MTGP_F64_01, false>();
     if (kind == kKindBitmapBit0) return mt3_occ<kKindBitmapBit0, false>();
+    if (kind == kKindBitmapRange) return mt3_occ<kKindBitmapRange, false>();
     return 0;
 }
 

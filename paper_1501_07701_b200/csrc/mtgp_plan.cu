@@ -574,6 +574,7 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         ma.ck = r.ck;
         ma.n = I.N;
         ma.pairs = r.L % 2 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 7) == 0;
+        ma.pred = r.pred;
         if (r.timing) r.timing->record(r.stream, &g0);
         e = use_mt3 ? launch_mt_gen3(I.N, r.kind, r.cksum, ma, r.stream)
                     : launch_mt_gen2(r.kind, r.cksum, ma, r.stream);
@@ -590,6 +591,7 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         ga.out = r.out;
         ga.L = r.L;
         ga.ck = r.ck;
+        ga.pred = r.pred;
         if (r.timing) r.timing->record(r.stream, &g0);
         e = use_v5   ? launch_gen5(r.kind, r.cksum, ga, r.stream)
             : use_v3 ? launch_gen3(r.kind, r.cksum, ga, r.stream)

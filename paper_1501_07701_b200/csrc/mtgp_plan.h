@@ -26,6 +26,7 @@ struct PlanRun {
     uint32_t max_pieces = 0;
     uint64_t min_piece_words = 0;  // 0 = auto
     uint64_t words_done = 0;       // words every stream has produced so far (few-stream splitting)
+    BitmapPred pred;               // kKindBitmapRange
     EventPool* timing = nullptr;  // non-null: record event pairs around the launches
     int want_kernel = 0;          // 0 auto, 2 force v2, 3 force v3, 4 v4; Engine::mt: 5 mt_gen2, 6 mt_gen3
     int version = 0;              // kernel that ran (2, 3, 4; 5 = Engine::mt warp teams)

@@ -353,6 +353,58 @@ __global__ void __launch_bounds__(kThreads) gap_count_kernel(const uint32_t* __r
     }
 }
 
+// The same per-tile summary from a hit bitmap the generator wrote directly (ctx_generate_bitmap,
+// kKindBitmapRange: lo <= (word & mask) < hi). One thread per bitmap word (128 per tile); bits at
+// or past the word budget are cleared here (in place, for the histogram pass).
+constexpr uint32_t kGapBmThreads = kGapTile / 32;  // 128
+__global__ void __launch_bounds__(kGapBmThreads) gap_count_bm_kernel(uint32_t* __restrict__ hits, uint64_t C,
+                                                                     uint64_t P, uint64_t budget,
+                                                                     const GapState* __restrict__ state,
+                                                                     GapTile* __restrict__ tiles, uint32_t T) {
+    __shared__ uint32_t wc[kGapBmThreads / 32];
+    __shared__ int32_t wf[kGapBmThreads / 32], wl[kGapBmThreads / 32];
+    const uint32_t st = blockIdx.y, tile = blockIdx.x;
+    if (state[st].done) {
+        if (threadIdx.x == 0) tiles[(size_t)st * T + tile] = GapTile{0, -1, -1};
+        return;
+    }
+    const uint32_t q = tile * kGapBmThreads + threadIdx.x;  // bitmap word within the stream's chunk
+    uint32_t* hw = hits + (size_t)st * (C / 32) + q;
+    uint32_t m = *hw;
+    const uint64_t g0 = P + 32ull * q;  // stream index of bit 0
+    if (g0 + 32 > budget) {
+        m = g0 >= budget ? 0u : (m & low_mask((uint32_t)(budget - g0)));
+        *hw = m;
+    }
+    uint32_t cnt = __popc(m);
+    int32_t first = m ? (int32_t)(32 * q + __ffs(m) - 1) : -1;
+    int32_t last = m ? (int32_t)(32 * q + 31 - __clz(m)) : -1;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        cnt += __shfl_xor_sync(kFull, cnt, s);
+        const int32_t f = __shfl_xor_sync(kFull, first, s);
+        const int32_t l = __shfl_xor_sync(kFull, last, s);
+        if (f >= 0 && (first < 0 || f < first)) first = f;
+        if (l > last) last = l;
+    }
+    const uint32_t warp = threadIdx.x >> 5;
+    if ((threadIdx.x & 31u) == 0) {
+        wc[warp] = cnt;
+        wf[warp] = first;
+        wl[warp] = last;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        GapTile t{0, -1, -1};
+        for (uint32_t i = 0; i < kGapBmThreads / 32; ++i) {
+            t.count += wc[i];
+            if (t.first < 0) t.first = wf[i];
+            if (wl[i] >= 0) t.last = wl[i];
+        }
+        tiles[(size_t)st * T + tile] = t;
+    }
+}
+
 // Per stream: exclusive scan of the chunk's tile counts -> the ordinal of each tile's first hit
 // and the hit before it; advances the carried {hits, last_hit} (done is set by gap_update_kernel
 // after the histogram pass, which still needs the old value).
@@ -609,6 +661,17 @@ void generate_chunk(mtgp_ctx* ctx, uint32_t* buf, uint64_t C) {
     if (rc) throw Failure{rc};
 }
 
+// Bitmap generation is ALU-heavier than word output, so it wants every team slot: while a fused
+// pass runs, auto-sized plans (min_piece_words == 0) cut pieces down to 2^19 words.
+struct FusedPieces {
+    mtgp_ctx* ctx;
+    uint64_t saved;
+    explicit FusedPieces(mtgp_ctx* c) : ctx(c), saved(c->min_piece_words) {
+        if (!saved) ctx->min_piece_words = 1ull << 19;
+    }
+    ~FusedPieces() { ctx->min_piece_words = saved; }
+};
+
 // The generator can write the bit-0 bitmap instead of words: gen3 (MTGP32-11213) and mt_gen3
 // (Engine::mt, n = 624) warp teams
 bool bitmap_fusable(const mtgp_ctx* ctx, uint64_t C) {
@@ -616,7 +679,7 @@ bool bitmap_fusable(const mtgp_ctx* ctx, uint64_t C) {
     if (ctx->engine == 0) return ctx->mexp == 11213 && (ctx->kernel == 0 || ctx->kernel == 3);
     // (the bitmap comes from cudaMalloc: any 256-byte aligned address stands in for it)
     return (ctx->kernel == 0 || ctx->kernel == 6) &&
-           ctx->planner->mt3_supported(kKindBitmapBit0, C, reinterpret_cast<const void*>(uintptr_t{256}));
+           ctx->planner->mt3_supported(MTGP_U32, C, reinterpret_cast<const void*>(uintptr_t{256}));
 }
 
 void launched(mtgp_ctx* ctx, const char* what) {
@@ -646,7 +709,17 @@ void run_walk(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res) {
     Arena ar;
     ar.add(counts, (size_t)S * (l + 1) * 8);
     if (bitmap_fusable(ctx, C)) {
-        // fused: the generator writes only the bit-0 bitmap (1/32 of the chunk's bytes)
+        // fused: the generator writes only the bit-0 bitmap (1/32 of the chunk's bytes), so the
+        // chunk can be 32x longer for the same memory: all walks in one call when they fit in
+        // 2^33 words over all streams (1 GB of bitmap). Long calls give every SM 6 CTAs of
+        // generator pieces (FusedPieces), amortise the jump-ahead and skip per-chunk launches.
+        uint32_t tpc_f = (uint32_t)std::min<uint64_t>(ceil_div(sp.n, wpt),
+                                                      std::max<uint64_t>(tpc, (1ull << 33) / S / tile_words));
+        tpc_f = std::max<uint32_t>(2, tpc_f + (tpc_f & 1));
+        const uint64_t C = (uint64_t)tpc_f * tile_words;
+        const uint64_t chunks = ceil_div(sp.n, (uint64_t)tpc_f * wpt);
+        const uint32_t tpc = tpc_f;
+        FusedPieces fp(ctx);
         const uint64_t bm_stride = (C + 31) / 32;
         uint32_t* const bm = ar.commit(ctx, (size_t)S * bm_stride * 4);
         check(cudaMemsetAsync(counts.p, 0, (size_t)S * (l + 1) * 8, ctx->stream), "memset");
@@ -655,7 +728,7 @@ void run_walk(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res) {
         check(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b), "smem attribute");
         for (uint64_t c = 0; c < chunks; ++c) {
             check(cudaMemsetAsync(bm, 0, (size_t)S * bm_stride * 4, ctx->stream), "memset bitmap");
-            const int rc = ctx_generate_bitmap(ctx, bm, C);
+            const int rc = ctx_generate_bitmap(ctx, kKindBitmapBit0, bm, C, BitmapPred{});
             if (rc) throw Failure{rc};
             kb<<<dim3(tpc, S), kThreads, smem_b, ctx->stream>>>(bm, bm_stride, l, wpt, c * tpc * wpt, sp.n,
                                                                counts.as<unsigned long long>());
@@ -778,10 +851,20 @@ void run_gap(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res) {
     const uint32_t S = ctx->n_sets;
     const stat::GapShape g = stat::gap_shape(sp);
     const uint32_t tcut = (uint32_t)g.tcut;
-    const uint64_t C = (chunk_target(S) + kGapTile - 1) / kGapTile * kGapTile;
+    const double p = sp.beta - sp.alpha;
+    uint64_t C = (chunk_target(S) + kGapTile - 1) / kGapTile * kGapTile;
+    // Fused: the generator writes the hit bitmap itself (1/32 of the chunk's bytes), so one call
+    // can cover the expected stream length (+5%) up to 2^33 words over all streams, with every SM
+    // full of generator pieces (FusedPieces). The 32-bit hit test needs hi - lo >= 1, hi <= 2^32.
+    const bool fused = bitmap_fusable(ctx, C) && g.hi > g.lo && g.hi <= (1ull << 32);
+    if (fused) {
+        const uint64_t want = (uint64_t)((double)(sp.n + 1) / p * 1.05) + kGapTile;
+        const uint64_t cap = std::max<uint64_t>(C, (1ull << 33) / S);
+        C = (std::min<uint64_t>(std::min<uint64_t>(std::max<uint64_t>(C, want), cap), g.budget + kGapTile - 1) +
+             kGapTile - 1) / kGapTile * kGapTile;
+    }
     const uint32_t T = (uint32_t)(C / kGapTile);
     const uint64_t max_chunks = ceil_div(g.budget, C);
-    const double p = sp.beta - sp.alpha;
     const uint64_t expected_chunks = std::max<uint64_t>(1, (uint64_t)((double)(sp.n + 1) / p / (double)C));
     const bool smem_hist = tcut + 1 <= 12288;
     const size_t smem = smem_hist ? 4 * ((size_t)tcut + 1) : 0;
@@ -793,10 +876,9 @@ void run_gap(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res) {
     ar.add(pre, (size_t)S * T * sizeof(GapPre));
     ar.add(state, (size_t)S * sizeof(GapState));
     ar.add(end, (size_t)S * 8);
-    // (the gap test stays on words: a generator-written hit bitmap measured 21.8 vs 20.5 ms for the
-    // desk test -- the bitmap step costs the generator more than the count pass it saves;
-    // DESIGN.md 4.5)
-    uint32_t* const wbuf = ar.commit(ctx, (size_t)S * C * 4);
+    uint32_t* const wbuf = ar.commit(ctx, fused ? 256 : (size_t)S * C * 4);
+    FusedPieces fp(ctx);
+    if (!fused) ctx->min_piece_words = fp.saved;
     check(cudaMemsetAsync(counts.p, 0, (size_t)S * (tcut + 1) * 8, ctx->stream), "memset");
     std::vector<GapState> hs(S, GapState{0, -1, 0, 0, 0});
     check(cudaMemcpyAsync(state.p, hs.data(), S * sizeof(GapState), cudaMemcpyHostToDevice, ctx->stream), "H2D state");
@@ -805,11 +887,24 @@ void run_gap(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res) {
         check(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attribute");
     for (uint64_t c = 0; c < max_chunks; ++c) {
         const uint64_t P = c * C;
-        generate_chunk(ctx, wbuf, C);
-        gap_count_kernel<<<dim3(T, S), kThreads, 0, ctx->stream>>>(wbuf, C, P, g.mask, g.lo, g.hi, g.budget,
-                                                                   state.as<GapState>(), tiles.as<GapTile>(), T,
-                                                                   hits.as<uint32_t>());
-        launched(ctx, "gap count kernel");
+        if (fused) {
+            check(cudaMemsetAsync(hits.p, 0, (size_t)S * (C / 32) * 4, ctx->stream), "memset hits");
+            BitmapPred pred;
+            pred.mask = g.mask;
+            pred.lo = (uint32_t)g.lo;
+            pred.span_m1 = (uint32_t)(g.hi - g.lo - 1);
+            const int rc = ctx_generate_bitmap(ctx, kKindBitmapRange, hits.as<uint32_t>(), C, pred);
+            if (rc) throw Failure{rc};
+            gap_count_bm_kernel<<<dim3(T, S), kGapBmThreads, 0, ctx->stream>>>(
+                hits.as<uint32_t>(), C, P, g.budget, state.as<GapState>(), tiles.as<GapTile>(), T);
+            launched(ctx, "gap count bitmap kernel");
+        } else {
+            generate_chunk(ctx, wbuf, C);
+            gap_count_kernel<<<dim3(T, S), kThreads, 0, ctx->stream>>>(wbuf, C, P, g.mask, g.lo, g.hi, g.budget,
+                                                                       state.as<GapState>(), tiles.as<GapTile>(), T,
+                                                                       hits.as<uint32_t>());
+            launched(ctx, "gap count kernel");
+        }
         gap_scan_kernel<<<S, kThreads, 0, ctx->stream>>>(tiles.as<GapTile>(), T, P, state.as<GapState>(),
                                                          pre.as<GapPre>());
         launched(ctx, "gap scan kernel");

@@ -16,9 +16,10 @@ struct GenArgs {
     uint32_t n_teams;
     const uint32_t* const* piece_win;  // per piece: start window (N words)
     uint32_t* win_out;                 // [n_sets][N] end windows
-    void* out;                         // per-stream stride L (bitmap kind: ceil(L / 32) words)
+    void* out;                         // per-stream stride L (bitmap kinds: ceil(L / 32) words)
     uint64_t L;
     DevCksum* ck;
+    BitmapPred pred;                   // kKindBitmapRange
 };
 
 struct JumpJob {

@@ -73,9 +73,10 @@ struct V3Ctx {
     bool pA0, pA1, pC0, pC1;              // "take the newer half-step" predicates
     uint32_t mA0, mA1, mC0, mC1;          // the same as 0/1 multipliers (MTGP3_SEL_IMAD)
     uint32_t nA0, nA1, nC0, nC1;          // 1 - m
-    // bitmap kind: this stream's bitmap, the piece's first word within the call
+    // bitmap kinds: this stream's bitmap, the piece's first word within the call, the predicate
     uint32_t* bm;
     unsigned long long poff;
+    BitmapPred pred;
 };
 
 __device__ __forceinline__ uint32_t comp4(const uint4& g, int c) {
@@ -189,7 +190,7 @@ __device__ __forceinline__ void step3(const V3Ctx& p, const uint4& h1, const uin
 #endif
         const uint32_t w0 = n + 128 * u + 4 * p.lane;  // piece word of o[0]
         if constexpr (KIND >= kKindBitmapBit0) {
-            bitmap_store_bit0(p.lane, p.bm, p.poff, o, n + 128 * u, !TAIL || w0 < len);
+            bitmap_store<KIND>(p.lane, p.bm, p.poff, p.pred, o, n + 128 * u, !TAIL || w0 < len);
         } else if (!TAIL || w0 < len) {
             __stcs(reinterpret_cast<uint4*>(optr + w0), make_uint4(o[0], o[1], o[2], o[3]));
             if (CK) {
@@ -323,6 +324,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MTGP3_MIN_CTAS) gen3_kernel
         if (KIND >= kKindBitmapBit0) {
             p.bm = reinterpret_cast<uint32_t*>(a.out) + (size_t)pc.set * ((a.L + 31) / 32);
             p.poff = pc.offset;
+            p.pred = a.pred;
         }
         const uint32_t len = (uint32_t)pc.len;
         const uint32_t* w0 = a.piece_win[pi];
@@ -398,6 +400,7 @@ cudaError_t launch_gen3(int kind, bool cksum, const GenArgs& a, cudaStream_t st)
     }
     // bitmap kinds carry no checksums (the words are never output)
     if (kind == kKindBitmapBit0) return launch3_t<kKindBitmapBit0, false>(a, st);
+    if (kind == kKindBitmapRange) return launch3_t<kKindBitmapRange, false>(a, st);
     return cudaErrorInvalidValue;
 }
 
@@ -411,6 +414,7 @@ int gen3_ctas_per_sm(int kind, bool cksum) {
         case 5: return occ3_t<MTGP_F32_01OC, true>();
     }
     if (kind == kKindBitmapBit0) return occ3_t<kKindBitmapBit0, false>();
+    if (kind == kKindBitmapRange) return occ3_t<kKindBitmapRange, false>();
     return 0;
 }
 
