@@ -286,7 +286,10 @@ __global__ void __launch_bounds__(kThreads) opso_kernel(const uint32_t* __restri
 // then the tile's gaps, (3) per-stream state update.
 constexpr uint32_t kGapTile = 4096;                   // words per CTA
 constexpr uint32_t kGapGroups = kGapTile / kThreads;  // 32-word groups per warp (16)
-constexpr uint32_t kGapHistCtas = 24;                 // histogram CTAs per stream
+#ifndef MTGP_GAP_HIST_CTAS
+#define MTGP_GAP_HIST_CTAS 48  // 24: 16.2 ms, 48: 16.1, 96: 16.0 for the fused desk gap (12: 17.5)
+#endif
+constexpr uint32_t kGapHistCtas = MTGP_GAP_HIST_CTAS;  // histogram CTAs per stream
 
 struct GapTile {
     uint32_t count;
