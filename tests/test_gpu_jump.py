@@ -87,3 +87,35 @@ def test_kara_jump_engine_mt(kernel):
         assert np.array_equal(outs[0][0][s], o.fill(300_000))
         o.fill(1_000_003)
         assert np.array_equal(outs[0][1][s], o.fill(2000))
+
+
+def test_few_stream_planning_short_and_long_lived(curand_sets):
+    """One stream (a GpuWordSource refill): a fresh stream is never split (no first-call
+    analysis); once it has produced 2^25 words, a 2^20-word call is split into jump-ahead pieces
+    over many warps (pieces_wanted, csrc/mtgp_plan.cu). Words exact either way."""
+    st = curand_sets[7]
+    L = 1 << 20
+    with mtgp.MtgpContext([st], [11]) as ctx:
+        a = ctx.fill_u32(L)
+        assert ctx.last_plan()[0] == 1
+        ctx.skip(1 << 25)
+        b = ctx.fill_u32(L)
+        pieces = ctx.last_plan()[0]
+    assert pieces > 16
+    o = oracle_py.MtgpOracle(st, 11)
+    assert np.array_equal(a[0], o.fill(L))
+    o.skip(1 << 25)
+    assert np.array_equal(b[0], o.fill(L))
+
+
+def test_few_stream_planning_engine_mt():
+    st = mtgp.mt19937_status()
+    L = 1 << 20
+    with mtgp.MtContext([st], [77]) as ctx:
+        ctx.fill_u32(1 << 12)
+        ctx.skip((1 << 25) - (1 << 12))
+        w = ctx.fill_u32(L)
+        assert ctx.last_plan()[0] > 16
+    o = oracle_py.MtOracle(None, 77)
+    o.fill(1 << 25)
+    assert np.array_equal(w[0], o.fill(L))
