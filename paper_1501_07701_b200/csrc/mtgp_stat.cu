@@ -290,6 +290,10 @@ constexpr uint32_t kGapGroups = kGapTile / kThreads;  // 32-word groups per warp
 #define MTGP_GAP_HIST_CTAS 48  // 24: 16.2 ms, 48: 16.1, 96: 16.0 for the fused desk gap (12: 17.5)
 #endif
 constexpr uint32_t kGapHistCtas = MTGP_GAP_HIST_CTAS;  // histogram CTAs per stream
+// histogram pass: 4 warps x 32 lanes, one 32-word group per lane, one 4096-word tile per CTA
+// iteration (8 warps with 16 active lanes each measured slower)
+constexpr uint32_t kHistThreads = 128, kHistWarps = kHistThreads / 32;
+static_assert(kHistWarps * 32 * 32 == kGapTile, "a tile is one CTA iteration");
 
 struct GapTile {
     uint32_t count;
@@ -473,20 +477,20 @@ __global__ void __launch_bounds__(kThreads) gap_scan_kernel(const GapTile* __res
 // Histogram pass: a CTA walks tiles blockIdx.x, +gridDim.x, ... of one stream (from the hit
 // bitmap, not the words), so each CTA zeroes and flushes its shared histogram once.
 template <bool SMEM_HIST>
-__global__ void __launch_bounds__(kThreads) gap_hist_kernel(const uint32_t* __restrict__ hits, uint64_t C, uint64_t P,
+__global__ void __launch_bounds__(kHistThreads) gap_hist_kernel(const uint32_t* __restrict__ hits, uint64_t C, uint64_t P,
                                                             const GapState* __restrict__ state,
                                                             const GapTile* __restrict__ tiles,
                                                             const GapPre* __restrict__ pre, uint32_t T, uint64_t n,
                                                             uint32_t tcut, unsigned long long* __restrict__ counts,
                                                             unsigned long long* __restrict__ end_pos) {
     extern __shared__ uint32_t hist[];
-    __shared__ uint32_t wc[kWarps];
-    __shared__ int32_t wl[kWarps];
+    __shared__ uint32_t wc[kHistWarps];
+    __shared__ int32_t wl[kHistWarps];
     const uint32_t st = blockIdx.y;
     if (state[st].done) return;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     if (SMEM_HIST)
-        for (uint32_t i = threadIdx.x; i <= tcut; i += kThreads) hist[i] = 0;
+        for (uint32_t i = threadIdx.x; i <= tcut; i += kHistThreads) hist[i] = 0;
     unsigned long long* cs = counts + (size_t)st * (tcut + 1);
     bool touched = false;
     for (uint32_t tile = blockIdx.x; tile < T; tile += gridDim.x) {
@@ -494,10 +498,10 @@ __global__ void __launch_bounds__(kThreads) gap_hist_kernel(const uint32_t* __re
         const GapPre tp = pre[(size_t)st * T + tile];
         if (tp.ord0 > n) break;  // ordinals only grow with the tile index
         touched = true;
-        const uint32_t base = tile * kGapTile + warp * (kGapGroups * 32);
-        // lane g < 16 owns group g (32 words) of the warp's 512: its hit mask, the number of hits
+        const uint32_t base = tile * kGapTile + warp * (32 * 32);
+        // lane g owns group g (32 words) of the warp's 1024: its hit mask, the number of hits
         // before it (exclusive scan) and the last hit before it (exclusive max scan)
-        const uint32_t m = lane < kGapGroups ? __ldg(hits + (size_t)st * (C / 32) + base / 32 + lane) : 0u;
+        const uint32_t m = __ldg(hits + (size_t)st * (C / 32) + base / 32 + lane);
         const uint32_t c = __popc(m);
         const int32_t lst = m ? (int32_t)(base + lane * 32 + 31 - __clz(m)) : -1;
         uint32_t ic = c;
@@ -546,7 +550,7 @@ __global__ void __launch_bounds__(kThreads) gap_hist_kernel(const uint32_t* __re
     }
     if (SMEM_HIST && touched) {
         __syncthreads();
-        for (uint32_t i = threadIdx.x; i <= tcut; i += kThreads)
+        for (uint32_t i = threadIdx.x; i <= tcut; i += kHistThreads)
             if (hist[i]) atomicAdd(cs + i, (unsigned long long)hist[i]);
     }
 }
@@ -911,7 +915,7 @@ void run_gap(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res) {
         gap_scan_kernel<<<S, kThreads, 0, ctx->stream>>>(tiles.as<GapTile>(), T, P, state.as<GapState>(),
                                                          pre.as<GapPre>());
         launched(ctx, "gap scan kernel");
-        hk<<<dim3(std::min<uint32_t>(T, kGapHistCtas), S), kThreads, smem, ctx->stream>>>(
+        hk<<<dim3(std::min<uint32_t>(T, kGapHistCtas), S), kHistThreads, smem, ctx->stream>>>(
                                                         hits.as<uint32_t>(), C, P, state.as<GapState>(),
                                                         tiles.as<GapTile>(), pre.as<GapPre>(), T, sp.n, tcut,
                                                         counts.as<unsigned long long>(), end.as<unsigned long long>());
