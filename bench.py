@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--calls", type=int, default=None,
                     help="device calls per step (output buffer = step/calls); default 2, 1 for c5")
     ap.add_argument("--no-checksum", action="store_true")
+    ap.add_argument("--checksum-mode", type=int, default=1, choices=[1, 2],
+                    help="MTGP_OPT_CHECKSUM: 1 sum64 + xor32, 2 sum32 + xor32 (the fixture's sums mod 2^32)")
     ap.add_argument("--min-piece-words", type=int, default=None, help="MTGP_OPT_MIN_PIECE_WORDS (default: library's)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -209,6 +211,13 @@ def traffic_per_launch(algo_bytes: float):
     return round(json.loads(f.read_text())["traffic_over_algorithmic"] * algo_bytes)
 
 
+def full_ck():
+    """tests/golden/full_ck.py: the oracle's cumulative per-stream checksums (checker data)."""
+    sys.path.insert(0, str(ROOT / "tests" / "golden"))
+    import full_ck as fc
+    return fc
+
+
 def cpu_reference(words_per_thread: int, threads: int):
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle_py
@@ -304,7 +313,10 @@ def main():
     calls = max(1, args.calls if args.calls is not None else (1 if is_c5 else 2))
     Lc = L_step // calls
     ctx = make_ctx(sets, seeds)
-    ctx.set_option(mtgp.OPT_CHECKSUM, 0 if args.no_checksum else 1)
+    ck_mode = 0 if args.no_checksum else args.checksum_mode
+    ctx.set_option(mtgp.OPT_CHECKSUM, ck_mode)
+    # the fixture's streams: global parameter-set IDs of this rank (c5: its contiguous share)
+    first_set = set_range.start if is_c5 else shard_rank * S
     if args.min_piece_words:
         ctx.set_option(mtgp.OPT_MIN_PIECE_WORDS, args.min_piece_words)
     ext = torch.cuda.ExternalStream(ctx.stream_handle(), device=torch.device("cuda", local))
@@ -326,8 +338,14 @@ def main():
         for _ in range(calls):
             ctx.generate_device(kind, out.data_ptr(), Lc)
 
-    for _ in range(args.warmup):
+    # full-volume parity, part 1: after the first warm-up step every stream's fused checksums
+    # must equal the oracle's for its first L_step words (tests/golden/full_ck.npz)
+    parity_first = None
+    for w in range(args.warmup):
         step()
+        if w == 0 and ck_mode and not is_mt:
+            ctx.sync()
+            parity_first = full_ck().compare(args.config, first_set, ctx.checksums(), sum_mod32=ck_mode == 2)
     ctx.sync()
     torch.cuda.synchronize()
     ctx.kernel_timing_reset()
@@ -397,6 +415,14 @@ def main():
     # per-stream checksum gather (NCCL all_gather; the only inter-GPU traffic)
     allck = shard.gather_checksums(ctx.checksums(), device=f"cuda:{local}")
     gathered_streams = len(allck)
+    # full-volume parity, part 2: every word of every stream generated in this run (warm-up and
+    # timed steps) through the gathered checksums, against the oracle's cumulative checksums
+    parity = None
+    if rank == 0 and ck_mode and not is_mt:
+        gfirst = first_set if (world == 1 or args.as_rank is not None) else 0
+        parity = full_ck().compare(args.config, gfirst, allck, sum_mod32=ck_mode == 2)
+        parity["after_first_step"] = parity_first
+        parity["fixture"] = "tests/golden/full_ck.npz (oracle/mtgp32_oracle.c cumulative checksums)"
 
     samples_rank = S * L_step * args.steps
     # whole job: every rank's samples (c5: the 1024 sets, however they are split)
@@ -465,6 +491,7 @@ def main():
             "config": {"workload": label, "sets_per_gpu": S, "seed": 1, "words_per_set_per_step": L_step,
                        "calls_per_step": calls, "kernel": f"v{kver}", "pieces_per_call": pieces,
                        "checksums_fused": not args.no_checksum,
+                       "checksum_mode": {0: "off", 1: "sum64+xor32", 2: "sum32+xor32"}[ck_mode],
                        **({"as_rank": shard_rank, "as_world": shard_world} if args.as_rank is not None else {}),
                        "global_set_ids": ([set_range.start, set_range.stop] if is_c5
                                           else [shard_rank * S, (shard_rank + 1) * S]),
@@ -498,9 +525,13 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": launches,
+            "parity": parity,
         }
         print(json.dumps(line), flush=True)
     ctx.close()
+    if rank == 0 and parity is not None and (parity.get("ok") is False or
+                                             (parity.get("after_first_step") or {}).get("ok") is False):
+        raise SystemExit("parity FAILED: GPU checksums differ from the oracle fixture")
     if world > 1:
         dist.destroy_process_group()
 

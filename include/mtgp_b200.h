@@ -63,7 +63,7 @@ extern "C" {
  */
 typedef struct mtgp_params {
     uint32_t mexp;           /* Mersenne exponent; N = mexp/32 + 1 words of state */
-    uint32_t pos;            /* pick-up position, 3 <= pos, N - pos >= 32         */
+    uint32_t pos;            /* pick-up position, 3 <= pos <= N - 32              */
     uint32_t sh1, sh2;       /* shifts, 1..31                                      */
     uint32_t tbl[16];        /* recursion table (GF(2)-linear in its 4-bit index)  */
     uint32_t tmp_tbl[16];    /* tempering table                                    */
@@ -82,13 +82,15 @@ typedef struct mtgp_cksum {
 typedef struct mtgp_ctx mtgp_ctx;
 
 /* Options for mtgp_set_option */
-#define MTGP_OPT_CHECKSUM 1        /* 0/1: accumulate mtgp_cksum in-kernel (default 1)              */
+#define MTGP_OPT_CHECKSUM 1        /* accumulate mtgp_cksum in-kernel: 0 off, 1 (default) sum64 +   */
+                                   /* xor32, 2 sum32 + xor32 (the word sum mod 2^32, without the   */
+                                   /* 64-bit carry chain; after any mode-2 call mtgp_checksums     */
+                                   /* reports sum64 mod 2^32 until mtgp_checksums_reset)           */
 #define MTGP_OPT_KERNEL 2          /* 0 = auto, 1 = reference-shaped v1 (one CTA per set), 2 = v2 */
                                    /* (shared-memory ring), 3 = v3 (register ring, mexp 11213),   */
                                    /* 4 = v4 (register ring for any supported exponent);          */
                                    /* Engine::mt contexts: 5 = warp teams, shared-memory rings,   */
-                                   /* 6 = warp teams, register-resident (n = 624);                */
-                                   /* 7 = v5 (v3 with 8 words per lane and 256-bit stores)        */
+                                   /* 6 = warp teams, register-resident (n = 624)                 */
 #define MTGP_OPT_MAX_PIECES 3      /* cap on jump-ahead pieces per call (0 = auto)                  */
 #define MTGP_OPT_MIN_PIECE_WORDS 4 /* minimum words per jump-ahead piece; 0 (default) = auto: 1<<21, */
                                    /* down to 1<<19 to keep >= 3 CTAs per SM busy                  */

@@ -74,6 +74,21 @@ void oracle_cksum_words(const uint32_t* w, size_t n, oracle_cksum* acc);
 double oracle_mtgp_bulk(const oracle_mtgp_params* sets, const uint32_t* seeds, uint32_t n_sets,
                         uint64_t skip, uint64_t n, uint32_t* out, int kind, int threads);
 
+/* Streaming checksums for full-volume parity fixtures: stream s = (sets[s], seeds[s]) from
+ * position 0; out[s*n_rec + k] = cumulative checksums of its first (k+1)*rec_every words.
+ * Index 0 = u32 words, 1 = f32 [1,2) bit patterns, 2 = f32 (0,1] bit patterns (1, 2 only when
+ * flags & 1). flags & 2 forces the one-word-at-a-time form (otherwise 16 steps per AVX-512
+ * vector where the CPU has it and N - pos >= 16). No output buffer; threads take one stream at
+ * a time. Returns seconds. */
+typedef struct oracle_stream_ck {
+    uint64_t sum[3];
+    uint32_t xr[3];
+    uint32_t pad;
+} oracle_stream_ck;
+double oracle_mtgp_cksum_stream(const oracle_mtgp_params* sets, const uint32_t* seeds, uint32_t n_sets,
+                                uint64_t rec_every, uint32_t n_rec, int flags, oracle_stream_ck* out,
+                                int threads);
+
 /* ---- classic MT, the reference Engine::mt ---- */
 typedef struct oracle_mt_params {
     uint32_t mexp, n, m, r, a;

@@ -32,6 +32,10 @@ class OracleCksum(C.Structure):
                 ("poly31", C.c_uint32), ("pad", C.c_uint32)]
 
 
+class OracleStreamCk(C.Structure):
+    _fields_ = [("sum", C.c_uint64 * 3), ("xr", C.c_uint32 * 3), ("pad", C.c_uint32)]
+
+
 class OracleMtParams(C.Structure):
     _fields_ = [(k, C.c_uint32) for k in ("mexp", "n", "m", "r", "a", "b", "c", "u", "s", "t", "l")]
 
@@ -58,6 +62,9 @@ def lib() -> C.CDLL:
         L.oracle_mtgp_bulk.argtypes = [C.POINTER(OracleParams), C.POINTER(C.c_uint32), C.c_uint32,
                                        C.c_uint64, C.c_uint64, C.c_void_p, C.c_int, C.c_int]
         L.oracle_mtgp_bulk.restype = C.c_double
+        L.oracle_mtgp_cksum_stream.argtypes = [C.POINTER(OracleParams), C.POINTER(C.c_uint32), C.c_uint32,
+                                               C.c_uint64, C.c_uint32, C.c_int, C.c_void_p, C.c_int]
+        L.oracle_mtgp_cksum_stream.restype = C.c_double
         L.oracle_mt19937_params.argtypes = [C.POINTER(OracleMtParams)]
         L.oracle_mt_init.argtypes = [C.POINTER(OracleMt), C.POINTER(OracleMtParams), C.c_uint32]
         L.oracle_mt_fill.argtypes = [C.POINTER(OracleMt), C.c_void_p, C.c_size_t]
@@ -123,6 +130,23 @@ def mtgp_bulk(sets: Sequence, seeds: Sequence[int], n: int, skip: int = 0, kind:
     if out is None:
         out = np.empty((len(sets), n), dtype=np.uint32)
     secs = lib().oracle_mtgp_bulk(arr, sd, len(sets), skip, n, out.ctypes.data_as(C.c_void_p), kind, threads)
+    return out, secs
+
+
+CK_DTYPE = np.dtype([("sum", "<u8", (3,)), ("xr", "<u4", (3,)), ("pad", "<u4")])
+
+
+def cksum_stream(sets: Sequence, seeds: Sequence[int], rec_every: int, n_rec: int, with_float: bool = False,
+                 threads: int = 8, scalar: bool = False):
+    """Cumulative per-stream checksums without an output buffer: result[s, k] holds the
+    {sum64, xor32} of the first (k+1)*rec_every words of stream s as fields sum[3] / xr[3]
+    (0 = u32, 1 = f32 [1,2) bits, 2 = f32 (0,1] bits). Returns (array, seconds)."""
+    arr = (OracleParams * len(sets))(*[to_oracle_params(p) for p in sets])
+    sd = (C.c_uint32 * len(seeds))(*[s & 0xFFFFFFFF for s in seeds])
+    out = np.zeros((len(sets), n_rec), dtype=CK_DTYPE)
+    assert C.sizeof(OracleStreamCk) == CK_DTYPE.itemsize
+    secs = lib().oracle_mtgp_cksum_stream(arr, sd, len(sets), rec_every, n_rec, int(with_float) | (2 if scalar else 0),
+                                          out.ctypes.data_as(C.c_void_p), threads)
     return out, secs
 
 

@@ -92,8 +92,8 @@ int mtgp_validate_params(const mtgp_params* p) {
     if (p->mask != mask) return fail(MTGP_EINVAL, "mask must be 0x%08x for mexp %u", mask, p->mexp);
     if (p->sh1 < 1 || p->sh1 > 31 || p->sh2 < 1 || p->sh2 > 31)
         return fail(MTGP_EINVAL, "shifts must be in [1, 31]");
-    if (p->pos < 2 || p->pos + 32 > n)
-        return fail(MTGP_EINVAL, "pick-up position must satisfy 2 <= pos <= N - 32 (N=%u)", n);
+    if (p->pos < 3 || p->pos + 32 > n)
+        return fail(MTGP_EINVAL, "pick-up position must satisfy 3 <= pos <= N - 32 (N=%u)", n);
     for (int i = 0; i < 16; ++i) {
         uint32_t t = 0, m = 0;
         for (int b = 0; b < 4; ++b)
@@ -283,9 +283,13 @@ int mtgp_ctx_stream(const mtgp_ctx* ctx, void** stream) {
 int mtgp_set_option(mtgp_ctx* ctx, int option, int64_t value) {
     if (!ctx) return fail(MTGP_EINVAL, "null context");
     switch (option) {
-        case MTGP_OPT_CHECKSUM: ctx->cksum = value != 0; return MTGP_OK;
+        case MTGP_OPT_CHECKSUM:
+            if (value < 0 || value > 2) return fail(MTGP_EINVAL, "checksum must be 0 (off), 1 (sum64) or 2 (sum32)");
+            ctx->cksum = value != 0;
+            ctx->ck32 = value == 2;
+            return MTGP_OK;
         case MTGP_OPT_KERNEL:
-            if (value < 0 || value > 7) return fail(MTGP_EINVAL, "kernel must be 0 (auto) or 1 .. 7");
+            if (value < 0 || value > 6) return fail(MTGP_EINVAL, "kernel must be 0 (auto) or 1 .. 6");
             ctx->kernel = (int)value;
             return MTGP_OK;
         case MTGP_OPT_MAX_PIECES:
@@ -361,6 +365,8 @@ int generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
         PlanRun run;
         run.kind = kind;
         run.cksum = ctx->cksum;
+        run.ck32 = ctx->ck32;
+        if (ctx->cksum && ctx->ck32) ctx->ck_sum_mod32 = true;
         run.params = ctx->engine == 1 ? static_cast<const void*>(ctx->d_mt) : static_cast<const void*>(ctx->d_params);
         run.win = ctx->d_win;
         run.ck = ctx->d_ck;
@@ -557,7 +563,7 @@ int mtgp_checksums(mtgp_ctx* ctx, mtgp_cksum* out) {
     CK(cudaMemcpyAsync(h.data(), ctx->d_ck, sizeof(DevCksum) * ctx->n_sets, cudaMemcpyDeviceToHost, ctx->stream), "D2H checksums");
     CK(cudaStreamSynchronize(ctx->stream), "sync");
     for (uint32_t s = 0; s < ctx->n_sets; ++s) {
-        out[s].sum64 = h[s].sum64;
+        out[s].sum64 = ctx->ck_sum_mod32 ? (h[s].sum64 & 0xFFFFFFFFull) : h[s].sum64;
         out[s].words = h[s].words;
         out[s].xor32 = h[s].xor32;
         out[s].pad = 0;
@@ -569,6 +575,7 @@ int mtgp_checksums_reset(mtgp_ctx* ctx) {
     if (!ctx) return fail(MTGP_EINVAL, "null context");
     CK(cudaSetDevice(ctx->device), "cudaSetDevice");
     CK(cudaMemsetAsync(ctx->d_ck, 0, sizeof(DevCksum) * ctx->n_sets, ctx->stream), "memset");
+    ctx->ck_sum_mod32 = false;
     return MTGP_OK;
 }
 

@@ -37,6 +37,8 @@ struct mtgp_ctx {
 
     // options
     bool cksum = true;
+    bool ck32 = false;        // MTGP_OPT_CHECKSUM 2 (32-bit sums where the kernel has them)
+    bool ck_sum_mod32 = false;  // a mode-2 call ran since the last reset: sum64 is valid mod 2^32
     int kernel = 0;
     int jump_mode = 0;  // MTGP_OPT_JUMP
     BitmapPred bm_pred;  // predicate of kKindBitmapRange (ctx_generate_bitmap)

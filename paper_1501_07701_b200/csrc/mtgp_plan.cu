@@ -119,6 +119,7 @@ struct PlannerImpl {
     // cached plan
     uint64_t plan_L = 0;
     uint32_t plan_T = 0;
+    uint64_t plan_want = 0;
     bool plan_valid = false;
     std::vector<Piece> pieces;
     std::vector<TeamWork> teams;
@@ -190,7 +191,8 @@ struct PlannerImpl {
         }
         return mt ? launch_jump_rt(a, N, st) : launch_jump(M, a, n_rows, st);
     }
-    cudaError_t build_plan(uint64_t L, uint32_t T, uint64_t min_piece, uint64_t words_done, std::string& err);
+    cudaError_t build_plan(uint64_t L, uint32_t T, uint64_t min_piece, uint64_t words_done, cudaStream_t st,
+                           std::string& err);
 };
 
 Planner::Planner(const std::vector<mtgp_params>& sets, int num_sms) : impl_(new PlannerImpl) {
@@ -320,8 +322,7 @@ cudaError_t PlannerImpl::analyze(const void* params, const uint32_t* win, cudaSt
 }
 
 cudaError_t PlannerImpl::build_plan(uint64_t L, uint32_t T, uint64_t min_piece, uint64_t words_done,
-                                    std::string& err) {
-    if (plan_valid && plan_L == L && plan_T == T) return cudaSuccess;
+                                    cudaStream_t st, std::string& err) {
     const uint64_t W = (uint64_t)S * L;
     // Equal work per SM: team counts are whole multiples of (SMs x warps per CTA), so every SM
     // holds the same number of CTAs (a 5-vs-6 CTA split costs ~10% of the makespan).
@@ -329,6 +330,9 @@ cudaError_t PlannerImpl::build_plan(uint64_t L, uint32_t T, uint64_t min_piece, 
     uint64_t want = pieces_wanted(W, L, T, quantum, min_piece, jump_k, words_done);
     if (want >= quantum) want -= want % quantum;
     want = std::max<uint64_t>(want, (W + kMaxPieceWords - 1) / kMaxPieceWords);
+    // the plan is a function of (L, T, want) only: min_piece and words_done enter through want
+    if (plan_valid && plan_L == L && plan_T == T && plan_want == want) return cudaSuccess;
+    plan_valid = false;
     pieces.clear();
     teams.clear();
     if (L > kMaxPieceWords)
@@ -434,14 +438,23 @@ cudaError_t PlannerImpl::build_plan(uint64_t L, uint32_t T, uint64_t min_piece, 
     if ((e = d_joboff.ensure(sizeof(uint32_t) * job_off.size())) != cudaSuccess) return e;
     if ((e = d_jobs.ensure(sizeof(JumpJob) * std::max<size_t>(1, jobs.size()))) != cudaSuccess) return e;
     if ((e = d_win_next.ensure(sizeof(uint32_t) * N * S)) != cudaSuccess) return e;
-    cudaMemcpy(d_pieces.p, pieces.data(), sizeof(Piece) * pieces.size(), cudaMemcpyHostToDevice);
-    cudaMemcpy(d_teams.p, teams.data(), sizeof(TeamWork) * teams.size(), cudaMemcpyHostToDevice);
-    if (!hq.empty()) cudaMemcpy(d_q.p, hq.data(), sizeof(uint32_t) * hq.size(), cudaMemcpyHostToDevice);
-    if (!jump_rows.empty()) cudaMemcpy(d_rows.p, jump_rows.data(), sizeof(uint32_t) * jump_rows.size(), cudaMemcpyHostToDevice);
-    cudaMemcpy(d_joboff.p, job_off.data(), sizeof(uint32_t) * job_off.size(), cudaMemcpyHostToDevice);
-    if (!jobs.empty()) cudaMemcpy(d_jobs.p, jobs.data(), sizeof(JumpJob) * jobs.size(), cudaMemcpyHostToDevice);
+    // Upload on the context stream: a previous call's kernels may still be reading the plan
+    // arrays (the context stream is non-blocking, so a legacy-stream cudaMemcpy would not wait
+    // for them). From pageable memory the copies are staged before returning, so the host
+    // vectors may change afterwards.
+    auto up = [&](void* dst, const void* src, size_t bytes) {
+        return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st) : cudaSuccess;
+    };
+    if ((e = up(d_pieces.p, pieces.data(), sizeof(Piece) * pieces.size())) != cudaSuccess ||
+        (e = up(d_teams.p, teams.data(), sizeof(TeamWork) * teams.size())) != cudaSuccess ||
+        (e = up(d_q.p, hq.data(), sizeof(uint32_t) * hq.size())) != cudaSuccess ||
+        (e = up(d_rows.p, jump_rows.data(), sizeof(uint32_t) * jump_rows.size())) != cudaSuccess ||
+        (e = up(d_joboff.p, job_off.data(), sizeof(uint32_t) * job_off.size())) != cudaSuccess ||
+        (e = up(d_jobs.p, jobs.data(), sizeof(JumpJob) * jobs.size())) != cudaSuccess)
+        return e;
     plan_L = L;
     plan_T = T;
+    plan_want = want;
     plan_valid = true;
     return cudaGetLastError();
 }
@@ -457,8 +470,6 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     const bool reg_ok = !I.mt && r.L % 4 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 15) == 0;
     const bool v3_ok = I.M == 11213 && reg_ok;
     const bool bitmap = r.kind >= kKindBitmapBit0;
-    // v5 (gen3 with 8 consecutive words per lane, one 256-bit store per step): 32-byte pieces
-    const bool v5_ok = v3_ok && r.L % 8 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 31) == 0 && I.t0 % 8 == 0;
     const bool v4_ok = v4_supports(I.M, r.kind) && reg_ok;
     // Engine::mt: mt_gen3 (register-resident, version 6) when the shape allows, else mt_gen2
     const bool mt3_ok = mt3_supported(r.kind, r.L, r.out);
@@ -468,14 +479,6 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     }
     if (!I.mt && (r.want_kernel == 5 || r.want_kernel == 6)) {
         err = "kernels 5 and 6 are Engine::mt kernels";
-        return cudaSuccess;
-    }
-    if (I.mt && r.want_kernel == 7) {
-        err = "kernel 7 is an MTGP32-11213 kernel";
-        return cudaSuccess;
-    }
-    if (r.want_kernel == 7 && !v5_ok) {
-        err = "kernel v5 needs mexp 11213, words_per_stream % 8 == 0 and 32-byte aligned output";
         return cudaSuccess;
     }
     if (r.want_kernel == 6 && !mt3_ok) {
@@ -499,13 +502,12 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     // auto: v3 for 11213; v4 (the same register-resident design, templated on N) for 23209 and
     // 44497, where it beats the shared-memory ring by 18% / 27% (profiles/r1_v4_sweep.jsonl);
     // v2 for request shapes the register kernels do not take (float kinds, L % 4 != 0, ...)
-    const bool use_v5 = v5_ok && r.want_kernel == 7 && !bitmap;
-    const bool use_v3 = !use_v5 && v3_ok && (r.want_kernel == 3 || (r.want_kernel == 0 && I.M == 11213));
-    const bool use_v4 = !use_v5 && !use_v3 && v4_ok && (r.want_kernel == 4 || (r.want_kernel == 0 && I.M != 11213));
+    const bool use_v3 = v3_ok && (r.want_kernel == 3 || (r.want_kernel == 0 && I.M == 11213));
+    const bool use_v4 = !use_v3 && v4_ok && (r.want_kernel == 4 || (r.want_kernel == 0 && I.M != 11213));
+    const int ck_mode = r.cksum ? (r.ck32 ? 2 : 1) : 0;
     const int cps = use_mt3  ? mt_gen3_ctas_per_sm(I.N, r.kind, r.cksum)
                     : I.mt   ? mt_gen2_ctas_per_sm(I.N, r.kind, r.cksum)
-                    : use_v5 ? gen5_ctas_per_sm(r.kind, r.cksum)
-                    : use_v3 ? gen3_ctas_per_sm(r.kind, r.cksum)
+                    : use_v3 ? gen3_ctas_per_sm(r.kind, ck_mode)
                     : use_v4 ? gen4_ctas_per_sm(I.M, r.kind, r.cksum)
                              : gen_ctas_per_sm(I.M, r.kind, r.cksum);
     if (cps <= 0) {
@@ -523,7 +525,8 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         if ((e = I.analyze(r.params, r.win, r.stream, err)) != cudaSuccess) return e;
         if (!err.empty()) return cudaSuccess;
     }
-    if ((e = I.build_plan(r.L, need_jumps ? T : I.S, r.min_piece_words, r.words_done, err)) != cudaSuccess) return e;
+    if ((e = I.build_plan(r.L, need_jumps ? T : I.S, r.min_piece_words, r.words_done, r.stream, err)) != cudaSuccess)
+        return e;
     if (!err.empty()) return cudaSuccess;
 
     // per-piece start-window pointers: jumped pieces -> d_pwin rows; offset-0 pieces -> current window
@@ -593,12 +596,11 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         ga.ck = r.ck;
         ga.pred = r.pred;
         if (r.timing) r.timing->record(r.stream, &g0);
-        e = use_v5   ? launch_gen5(r.kind, r.cksum, ga, r.stream)
-            : use_v3 ? launch_gen3(r.kind, r.cksum, ga, r.stream)
+        e = use_v3   ? launch_gen3(r.kind, ck_mode, ga, r.stream)
             : use_v4 ? launch_gen4(I.M, r.kind, r.cksum, ga, r.stream)
                      : launch_gen(I.M, r.kind, r.cksum, ga, r.stream);
         if (e != cudaSuccess) return e;
-        r.version = use_v5 ? 7 : use_v3 ? 3 : use_v4 ? 4 : 2;
+        r.version = use_v3 ? 3 : use_v4 ? 4 : 2;
     }
     if (r.timing) {
         r.timing->record(r.stream, &g1);

@@ -17,6 +17,7 @@ namespace mtgpb {
 struct PlanRun {
     int kind = 0;
     bool cksum = true;
+    bool ck32 = false;             // MTGP_OPT_CHECKSUM 2: kernels that have it keep a 32-bit sum
     const void* params = nullptr;  // DevParams (MTGP32) or DevMtParams (Engine::mt planner)
     uint32_t* win = nullptr;
     DevCksum* ck = nullptr;

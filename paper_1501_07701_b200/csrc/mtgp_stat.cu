@@ -720,9 +720,12 @@ void run_walk(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res) {
         // chunk can be 32x longer for the same memory: all walks in one call when they fit in
         // 2^33 words over all streams (1 GB of bitmap). Long calls give every SM 6 CTAs of
         // generator pieces (FusedPieces), amortise the jump-ahead and skip per-chunk launches.
+        // walk_bm_kernel indexes the chunk's bits in 32 bits: keep C < 2^32 words per stream
+        const uint64_t tpc_max = ((1ull << 32) / tile_words - 1) & ~1ull;
         uint32_t tpc_f = (uint32_t)std::min<uint64_t>(ceil_div(sp.n, wpt),
                                                       std::max<uint64_t>(tpc, (1ull << 33) / S / tile_words));
         tpc_f = std::max<uint32_t>(2, tpc_f + (tpc_f & 1));
+        tpc_f = (uint32_t)std::min<uint64_t>(tpc_f, tpc_max);
         const uint64_t C = (uint64_t)tpc_f * tile_words;
         const uint64_t chunks = ceil_div(sp.n, (uint64_t)tpc_f * wpt);
         const uint32_t tpc = tpc_f;
@@ -866,7 +869,9 @@ void run_gap(mtgp_ctx* ctx, const mtgp_stat_spec& sp, mtgp_stat_result* res) {
     const bool fused = bitmap_fusable(ctx, C) && g.hi > g.lo && g.hi <= (1ull << 32);
     if (fused) {
         const uint64_t want = (uint64_t)((double)(sp.n + 1) / p * 1.05) + kGapTile;
-        const uint64_t cap = std::max<uint64_t>(C, (1ull << 33) / S);
+        // tile positions (GapTile.first/last, gap_hist_kernel) are 32-bit signed chunk offsets:
+        // keep C <= 2^31 words per stream
+        const uint64_t cap = std::min<uint64_t>(std::max<uint64_t>(C, (1ull << 33) / S), 1ull << 31);
         C = (std::min<uint64_t>(std::min<uint64_t>(std::max<uint64_t>(C, want), cap), g.budget + kGapTile - 1) +
              kGapTile - 1) / kGapTile * kGapTile;
     }

@@ -4,7 +4,7 @@
 // into "pieces" (contiguous ranges of one stream) so that every resident warp on the GPU has the
 // same amount of work; a piece that does not start at the stream's current position starts
 // from a GF(2) jump-ahead of the stream's state (mtgp_plan.cu computes x^offset mod P on the
-// host, jump_kernel below applies it on the device). One WARP ("team") owns a piece at a time
+// host, jump_flat_kernel below applies it on the device). One WARP ("team") owns a piece at a time
 // and keeps the piece's state in a private shared-memory ring; it needs no CTA barrier, only
 // __syncwarp between steps.
 //
@@ -405,83 +405,14 @@ cudaError_t launch_prefix(const DevParams* params, const uint32_t* win, const ui
 
 // ------------------------------------------------------------------------------------------
 // jump: y_j = XOR_{i : q_i = 1} x_{i+j}, j in [0, N) -- the window at offset o when
-// q = x^o mod P (P annihilates the stream; mtgp_plan.cu). One CTA per set with jumps; the set's
-// prefix is staged in shared memory; each warp takes one job (piece) at a time; lane l keeps
-// a sliding window of J consecutive j's in registers and walks q two bits at a time.
+// q = x^o mod P (P annihilates the stream; mtgp_plan.cu). One warp per (job, 32*J-output pass),
+// any mix of streams per CTA; the (L2-resident) prefix is read through the read-only L1 path
+// (the shared-memory-staged predecessor paid a CTA-wide copy per piece and one CTA per SM slot,
+// profiles/r1_launches_flatjump.md). Lane l keeps J consecutive j's in registers and walks q two
+// bits at a time.
 // ------------------------------------------------------------------------------------------
-#ifndef MTGP_JUMP_J
-#define MTGP_JUMP_J 12
-#endif
-constexpr int kJumpJ = MTGP_JUMP_J;  // outputs per lane per pass (multiple of 4)
-constexpr int kJumpWarps = 8;
-
-template <uint32_t MEXP>
-__global__ void __launch_bounds__(kJumpWarps * 32) jump_kernel(JumpArgs a) {
-    constexpr uint32_t N = MEXP / 32 + 1;
-    constexpr int J = kJumpJ;
-    extern __shared__ uint4 jsm4[];
-    // grid: x = prefix row (set), y = group of kJumpWarps jobs of that set
-    const uint32_t row = blockIdx.x;
-    const uint32_t first = a.job_off[row] + blockIdx.y * kJumpWarps;
-    const uint32_t end = a.job_off[row + 1];
-    if (first >= end) return;
-    const uint4* src = reinterpret_cast<const uint4*>(a.pre + (size_t)row * a.pre_stride + a.pre_off);
-    for (uint32_t i = threadIdx.x; i < a.pre_len / 4; i += blockDim.x) jsm4[i] = src[i];
-    __syncthreads();
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (uint32_t job = first + warp; job < end && job < first + kJumpWarps; job += kJumpWarps) {
-        const JumpJob jb = a.jobs[job];
-        const uint32_t* q = a.q + (size_t)jb.q * a.q_words;
-        uint32_t* dst = a.piece_win + (size_t)jb.piece * N;
-        for (uint32_t j0 = 0; j0 < N; j0 += 32 * J) {
-            const uint32_t jl = j0 + J * lane;  // multiple of 4
-            uint32_t acc[J];
-#pragma unroll
-            for (int k = 0; k < J; ++k) acc[k] = 0;
-            for (uint32_t iw0 = 0; iw0 < a.q_words; iw0 += 32) {
-                const uint32_t qmine = iw0 + lane < a.q_words ? q[iw0 + lane] : 0u;
-                const uint32_t nw = min(32u, a.q_words - iw0);
-                for (uint32_t k32 = 0; k32 < nw; ++k32) {
-                    const uint32_t qw = __shfl_sync(FULL, qmine, k32);
-                    if (qw == 0) continue;
-                    const uint32_t base4 = ((iw0 + k32) * 32 + jl) >> 2;
-                    uint32_t w[J + 32];
-#pragma unroll
-                    for (int v = 0; v < (J + 32) / 4; ++v) {
-                        const uint4 g = jsm4[base4 + v];
-                        w[4 * v] = g.x;
-                        w[4 * v + 1] = g.y;
-                        w[4 * v + 2] = g.z;
-                        w[4 * v + 3] = g.w;
-                    }
-#pragma unroll
-                    for (int b = 0; b < 32; b += 2) {
-                        const uint32_t pat = (qw >> b) & 3u;
-                        if (pat == 1) {
-#pragma unroll
-                            for (int k = 0; k < J; ++k) acc[k] ^= w[b + k];
-                        } else if (pat == 2) {
-#pragma unroll
-                            for (int k = 0; k < J; ++k) acc[k] ^= w[b + 1 + k];
-                        } else if (pat == 3) {
-#pragma unroll
-                            for (int k = 0; k < J; ++k) acc[k] ^= w[b + k] ^ w[b + 1 + k];
-                        }
-                    }
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < J; ++k)
-                if (jl + k < N) dst[jl + k] = acc[k];
-        }
-    }
-}
-
-// Flat variant: one warp per job, any mix of streams per CTA, the (L2-resident) prefix read
-// through the read-only L1 path instead of being staged in shared memory -- no shared-memory
-// occupancy limit, so every job runs in the first wave with no idle warps.
+constexpr int kJumpJ = 12;  // outputs per lane per pass (multiple of 4)
 constexpr int kJumpFlatWarps = 4;
-
 template <uint32_t MEXP>
 __global__ void __launch_bounds__(kJumpFlatWarps * 32) jump_flat_kernel(JumpArgs a) {
     constexpr uint32_t N = MEXP / 32 + 1;
@@ -599,24 +530,12 @@ __global__ void __launch_bounds__(kJumpFlatWarps * 32) jump_flat_rt_kernel(JumpA
     }
 }
 
-#ifndef MTGP_JUMP_FLAT
-#define MTGP_JUMP_FLAT 1
-#endif
-
 template <uint32_t MEXP>
-static cudaError_t launch_jump_t(const JumpArgs& a, uint32_t n_rows, cudaStream_t st) {
-    if (MTGP_JUMP_FLAT) {
-        if (a.n_jobs == 0) return cudaSuccess;
-        constexpr uint32_t N = MEXP / 32 + 1, kPasses = (N + 32 * kJumpJ - 1) / (32 * kJumpJ);
-        const uint32_t units = a.n_jobs * kPasses;
-        jump_flat_kernel<MEXP><<<(units + kJumpFlatWarps - 1) / kJumpFlatWarps, kJumpFlatWarps * 32, 0, st>>>(a);
-        return cudaGetLastError();
-    }
-    const size_t smem = (size_t)a.pre_len * 4;
-    cudaError_t e = cudaFuncSetAttribute(jump_kernel<MEXP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    const dim3 grid(n_rows, (a.max_jobs_per_row + kJumpWarps - 1) / kJumpWarps);
-    jump_kernel<MEXP><<<grid, kJumpWarps * 32, smem, st>>>(a);
+static cudaError_t launch_jump_t(const JumpArgs& a, cudaStream_t st) {
+    if (a.n_jobs == 0) return cudaSuccess;
+    constexpr uint32_t N = MEXP / 32 + 1, kPasses = (N + 32 * kJumpJ - 1) / (32 * kJumpJ);
+    const uint32_t units = a.n_jobs * kPasses;
+    jump_flat_kernel<MEXP><<<(units + kJumpFlatWarps - 1) / kJumpFlatWarps, kJumpFlatWarps * 32, 0, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -631,9 +550,9 @@ cudaError_t launch_jump_rt(const JumpArgs& a, uint32_t N, cudaStream_t st) {
 cudaError_t launch_jump(uint32_t mexp, const JumpArgs& a, uint32_t n_rows, cudaStream_t st) {
     if (n_rows == 0) return cudaSuccess;
     switch (mexp) {
-        case 11213: return launch_jump_t<11213>(a, n_rows, st);
-        case 23209: return launch_jump_t<23209>(a, n_rows, st);
-        case 44497: return launch_jump_t<44497>(a, n_rows, st);
+        case 11213: return launch_jump_t<11213>(a, st);
+        case 23209: return launch_jump_t<23209>(a, st);
+        case 44497: return launch_jump_t<44497>(a, st);
     }
     return cudaErrorInvalidValue;
 }

@@ -54,12 +54,10 @@ cudaError_t launch_jump(uint32_t mexp, const JumpArgs& a, uint32_t n_jump_sets, 
 cudaError_t launch_jump_rt(const JumpArgs& a, uint32_t N, cudaStream_t st);
 cudaError_t launch_gen(uint32_t mexp, int kind, bool cksum, const GenArgs& a, cudaStream_t st);
 int gen_ctas_per_sm(uint32_t mexp, int kind, bool cksum);
-// v3: register-resident ring, MTGP32-11213 only (mtgp_v3.cu)
-cudaError_t launch_gen3(int kind, bool cksum, const GenArgs& a, cudaStream_t st);
-int gen3_ctas_per_sm(int kind, bool cksum);
-// v5: gen3 with 8 consecutive words per lane and 256-bit stores, MTGP32-11213 (mtgp_v5.cu)
-cudaError_t launch_gen5(int kind, bool cksum, const GenArgs& a, cudaStream_t st);
-int gen5_ctas_per_sm(int kind, bool cksum);
+// v3: register-resident ring, MTGP32-11213 only (mtgp_v3.cu). ck_mode: 0 none, 1 sum64 + xor32,
+// 2 sum32 + xor32 (MTGP_OPT_CHECKSUM)
+cudaError_t launch_gen3(int kind, int ck_mode, const GenArgs& a, cudaStream_t st);
+int gen3_ctas_per_sm(int kind, int ck_mode);
 // v4: gen3's register-resident design templated on the exponent (csrc/mtgp_v4.cu)
 bool v4_supports(uint32_t mexp, int kind);
 cudaError_t launch_gen4(uint32_t mexp, int kind, bool cksum, const GenArgs& a, cudaStream_t st);

@@ -247,6 +247,9 @@ class MtgpContext:
     def generate_host_async(self, kind: int, out: np.ndarray) -> None:
         """mtgp_generate_async into host memory `out` (n_sets, L): valid after sync(). Keep `out`
         alive (and preferably page-locked) until then."""
+        dt = np.float64 if kind == F64_01 else (np.float32 if kind in (F32_12, F32_01OC) else np.uint32)
+        # the call writes 8 bytes per sample for F64_01 and 4 otherwise: the dtype sizes the buffer
+        assert np.dtype(out.dtype).itemsize == np.dtype(dt).itemsize, f"out dtype {out.dtype} for kind {kind}"
         assert out.flags.c_contiguous and out.size % self.n_sets == 0
         _check(self.lib, self.lib.mtgp_generate_async(self.h, kind, out.ctypes.data_as(C.c_void_p),
                                                       out.size // self.n_sets, 0))

@@ -66,8 +66,8 @@ class MtgpParams:
             raise ValueError("mask must be 0xFFFFFFFF << (32N - mexp)")
         if not (1 <= self.sh1 <= 31 and 1 <= self.sh2 <= 31):
             raise ValueError("shifts must be in [1, 31]")
-        if not (2 <= self.pos <= self.n - 32):
-            raise ValueError("pick-up position must satisfy 2 <= pos <= N - 32")
+        if not (3 <= self.pos <= self.n - 32):
+            raise ValueError("pick-up position must satisfy 3 <= pos <= N - 32")
         for i in range(16):
             t = m = 0
             for b in range(4):

@@ -152,3 +152,96 @@ def test_curand_kernel_state_seeds():
     # low word of seed ^ (seed >> 32) = 0x90ABCDEF ^ 0x12345678 = 0x829F9B97
     assert tables.curand_kernel_state_seeds(s, 2) == [0x829F9B98, 0x829F9B99]
     assert tables.curand_kernel_state_seeds(0xFFFFFFFF, 2) == [0, 1]  # u32 wrap
+
+
+# ---- streaming checksums and the full-volume parity fixture (tests/golden/full_ck.npz) ----
+
+def _fill_ck(params, seed, n, kind=0, skip=0):
+    g = oracle_py.MtgpOracle(params, seed)
+    if skip:
+        g.skip(skip)
+    w = g.fill(n, kind=kind)
+    return int(w.astype(np.uint64).sum()), int(np.bitwise_xor.reduce(w))
+
+
+@pytest.mark.parametrize("mexp", [11213, 23209, 44497])
+def test_cksum_stream_matches_fill(mexp):
+    """oracle_mtgp_cksum_stream (16 steps per AVX-512 vector) == the word-at-a-time fill,
+    for every record, u32 and both float kinds."""
+    sets = tables.sets_for(mexp, 3)
+    rec, n_rec = 1 << 14, 5
+    a, _ = oracle_py.cksum_stream(sets, [1, 7, 0xFFFFFFFF], rec, n_rec, with_float=True, threads=3)
+    b, _ = oracle_py.cksum_stream(sets, [1, 7, 0xFFFFFFFF], rec, n_rec, with_float=True, threads=3, scalar=True)
+    assert (a == b).all()
+    for s, seed in enumerate([1, 7, 0xFFFFFFFF]):
+        for kind in range(3):
+            sm, x = _fill_ck(sets[s], seed, rec * n_rec, kind)
+            assert (int(a[s, -1]["sum"][kind]), int(a[s, -1]["xr"][kind])) == (sm, x)
+
+
+def test_cksum_stream_cuRAND_golden(curand_sets, curand_golden):
+    """The 2^20-word set 0 / seed 1 checksum pinned by cuRAND's own headers (App. B)."""
+    a, _ = oracle_py.cksum_stream(curand_sets[:1], [1], 1 << 20, 1, threads=1)
+    assert int(a[0, 0]["sum"][0]) == 2251211974485391 and int(a[0, 0]["xr"][0]) == 0x87DB016D
+
+
+def _full_ck():
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent / "golden"))
+    import full_ck
+    return full_ck
+
+
+def test_full_ck_fixture_spot_checks():
+    """Re-derive the fixture's first records with the word-at-a-time oracle for certified and
+    synthetic streams of every rank range, and one c3 float record."""
+    fc = _full_ck()
+    if not fc.available():
+        pytest.skip("full_ck.npz not generated")
+    assert fc.coverage("c2") == (1600, 50, 1 << 27) and fc.coverage("c5") == (1024, 64, 1 << 24)
+    ids = [0, 1, 199, 200, 777, 1023]
+    sets = [tables.sets_for(11213, 1, first=i)[0] for i in ids]
+    got, _ = oracle_py.cksum_stream(sets, [1] * len(ids), 1 << 24, 1, threads=len(ids), scalar=True)
+    for j, i in enumerate(ids):
+        es, ex = fc.expected("c5", i, 1, 1 << 24)
+        assert (int(got[j, 0]["sum"][0]), int(got[j, 0]["xr"][0])) == (int(es[0]), int(ex[0])), i
+    for cfg, idx in (("c3-f12", 1), ("c3-f01", 2)):
+        es, ex = fc.expected(cfg, 5, 1, 1 << 27)
+        a, _ = oracle_py.cksum_stream([tables.sets_for(11213, 1, first=5)[0]], [1], 1 << 27, 1, with_float=True,
+                                      threads=1)
+        assert (int(a[0, 0]["sum"][idx]), int(a[0, 0]["xr"][idx])) == (int(es[0]), int(ex[0]))
+    for mexp in (23209, 44497):
+        es, ex = fc.expected(f"c4-{mexp}", 3, 1, 1 << 27)
+        a, _ = oracle_py.cksum_stream([tables.sets_for(mexp, 1, first=3)[0]], [1], 1 << 27, 1, threads=1)
+        assert (int(a[0, 0]["sum"][0]), int(a[0, 0]["xr"][0])) == (int(es[0]), int(ex[0]))
+
+
+def test_full_ck_records_are_cumulative():
+    """c5's 2^24-word records 8k of a stream are c2's 2^27-word record k (one oracle pass)."""
+    fc = _full_ck()
+    if not fc.available():
+        pytest.skip("full_ck.npz not generated")
+    for k in range(1, 9):
+        a = fc.expected("c5", 0, 1024, k * (1 << 27))
+        b = fc.expected("c2", 0, 1024, k * (1 << 27))
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert fc.expected("c2", 0, 200, 51 << 27) is None and fc.expected("c2", 1500, 200, 1 << 27) is None
+
+
+def test_full_ck_compare_reports_mismatch():
+    fc = _full_ck()
+    if not fc.available():
+        pytest.skip("full_ck.npz not generated")
+    es, ex = fc.expected("c2", 0, 4, 2 << 27)
+    good = [(int(s), int(x), 2 << 27) for s, x in zip(es, ex)]
+    assert fc.compare("c2", 0, good)["ok"] is True
+    bad = list(good)
+    bad[2] = (bad[2][0] + 1, bad[2][1], bad[2][2])
+    r = fc.compare("c2", 0, bad)
+    assert r["ok"] is False and r["mismatched_streams"] == [2]
+    # mode 2: sums compared mod 2^32 only
+    hi = [((s + (5 << 32)) & 0xFFFFFFFFFFFFFFFF, x, w) for s, x, w in good]
+    assert fc.compare("c2", 0, hi, sum_mod32=True)["ok"] is True and fc.compare("c2", 0, hi)["ok"] is False
+    assert fc.compare("c2", 0, [(0, 0, 3 << 27)] * 2)["ok"] is False
+    assert fc.compare("c2", 0, [(0, 0, 99 << 27)] * 2)["ok"] is None

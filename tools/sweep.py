@@ -29,7 +29,7 @@ words = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 25
 kind = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 mexp = int(sys.argv[3]) if len(sys.argv) > 3 else 11213
 rounds = int(sys.argv[4]) if len(sys.argv) > 4 else 3
-cksum = int(sys.argv[5]) if len(sys.argv) > 5 else 1
+cks = [int(c) for c in sys.argv[5].split(",")] if len(sys.argv) > 5 else [1]  # MTGP_OPT_CHECKSUM modes
 sustain = float(sys.argv[6]) if len(sys.argv) > 6 else 0.0
 kernels = [int(k) for k in sys.argv[7].split(",")] if len(sys.argv) > 7 else [0]  # MTGP_OPT_KERNEL values
 
@@ -60,18 +60,20 @@ ctxs = []
 for path in libs:
     lib = mtgp.load_library(str(path))
     for kern in kernels:
-        if sets is None:
-            ctx = mtgp.MtContext([mtgp.mt19937_status()] * 200, [5489 + i for i in range(200)], lib=lib)
-        else:
-            ctx = mtgp.MtgpContext(sets, [1] * 200, lib=lib)
-        ctx.set_option(mtgp.OPT_CHECKSUM, cksum)
-        ctx.set_option(mtgp.OPT_KERNEL, kern)
-        ctx.generate_device(kind, out.data_ptr(), words)  # plan + warm
-        ctx.sync()
-        ctxs.append((path.stem + ("" if kernels == [0] else f"/k{kern}"), ctx))
-res = {name: [] for name, _ in ctxs}
+        for ck in cks:
+            if sets is None:
+                ctx = mtgp.MtContext([mtgp.mt19937_status()] * 200, [5489 + i for i in range(200)], lib=lib)
+            else:
+                ctx = mtgp.MtgpContext(sets, [1] * 200, lib=lib)
+            ctx.set_option(mtgp.OPT_CHECKSUM, ck)
+            ctx.set_option(mtgp.OPT_KERNEL, kern)
+            ctx.generate_device(kind, out.data_ptr(), words)  # plan + warm
+            ctx.sync()
+            ctxs.append((path.stem + ("" if kernels == [0] else f"/k{kern}") + ("" if len(cks) == 1 else f"/ck{ck}"),
+                         ctx, ck))
+res = {name: [] for name, _, _ in ctxs}
 for r in range(rounds):
-    for name, ctx in ctxs:
+    for name, ctx, _ in ctxs:
         ctx.kernel_timing_reset()
         ctx.set_option(mtgp.OPT_TIMING, 1)
         clk = Clock()
@@ -90,7 +92,7 @@ for r in range(rounds):
         ctx.set_option(mtgp.OPT_TIMING, 0)
         mhz = statistics.median(clk.samples) if clk.samples else float("nan")
         res[name].append((g / gn, j / max(1, jn), mhz))
-for name, ctx in ctxs:
+for name, ctx, cksum in ctxs:
     pieces, _, kv = ctx.last_plan()
     if sustain:  # the average over the sustained rounds, not the best
         ms = statistics.mean(x[0] for x in res[name])

@@ -18,8 +18,6 @@
 //
 // Per 256-word step per warp: 20 operand SHFL + 16 table SHFL + 2 STG.128 (LSU data-pipe
 // wavefronts 44, vs 59 for the shared-memory ring of v2).
-#include <type_traits>
-
 #include "mtgp_bitmap.cuh"
 #include "mtgp_v2.cuh"
 
@@ -27,35 +25,54 @@ namespace mtgpb {
 
 #define FULL 0xffffffffu
 
-
-// Occupancy target: 6 CTAs x 4 warps per SM (80 registers). The pipe-balance variants that
-// measured slower in round 1 (IMAD.HI shifts, FMA-pipe selects and checksums, ...) are kept in
-// tools/variants/mtgp_v3_toggles.cu, their sweeps under profiles/r1_v3_*_sweep.jsonl.
-constexpr int kMinCtas3 = 6;
-// Operand select of the A (bit 0) / C (bit 1) stream on the FMA pipe: send = lo + m * (hi - lo)
-// with a per-lane 0/1 multiplier m and the differences hi - lo formed once per half-step pair by
-// IMAD (lo * -1 + hi), shared by both streams. One IMAD per fetch instead of one ALU SEL.
-#ifndef MTGP3_LERP
-#define MTGP3_LERP 0
+#ifndef MTGP3_SH2_IMAD
+#define MTGP3_SH2_IMAD 0
+#endif
+#ifndef MTGP3_FOLD_IMAD
+#define MTGP3_FOLD_IMAD 0
+#endif
+#ifndef MTGP3_MIN_CTAS
+#define MTGP3_MIN_CTAS 6
+#endif
+#ifndef MTGP3_FOLD_PAIR
+#define MTGP3_FOLD_PAIR 1
+#endif
+#ifndef MTGP3_CK_WIDE
+#define MTGP3_CK_WIDE 0
+#endif
+// Checksum sum on the FMA pipe without 64-bit adds: within a run of <= 2^16 words per lane, `sum`
+// holds two 32-bit accumulators, A = sum(o) mod 2^32 (IMAD) and B = sum(o >> 16) mod 2^32
+// (IMAD.HI); then sum(o) = 2^16 B + ((A - (B << 16)) mod 2^32) exactly (the low halves add up to
+// less than 2^32). run3 folds them into the 64-bit total every 8192 steps.
+#ifndef MTGP3_CK_HILO
+#define MTGP3_CK_HILO 0
+#endif
+// float kinds: the [1,2) conversion as I2F.RZ + FFMA.RZ instead of LEA.HI on the ALU pipe
+#ifndef MTGP3_FLT_FMA
+#define MTGP3_FLT_FMA 0
+#endif
+// x << sh1 as a shift on the ALU pipe instead of an IMAD by 2^sh1 on the FMA pipe
+#ifndef MTGP3_SH1_SHF
+#define MTGP3_SH1_SHF 0
+#endif
+// Operand select on the FMA pipe: send = hi * m + lo * (1 - m) with a per-lane 0/1 multiplier
+// (two IMADs instead of one SEL on the ALU pipe). 0: SEL everywhere, 1: IMAD for the A and C
+// streams, 2: A only, 3: C only.
+#ifndef MTGP3_SEL_IMAD
+#define MTGP3_SEL_IMAD 0
 #endif
 
 namespace {
 
 constexpr uint32_t kN = 351;  // MTGP32-11213 state words
 
-// Checksum modes (MTGP_OPT_CHECKSUM): 0 none; 1 sum64 + xor32; 2 sum32 + xor32 -- the sum of the
-// emitted words mod 2^32 in a 32-bit accumulator (one 3-input IADD3 per two words, no carry
-// chain), reported in the low half of mtgp_cksum.sum64.
-template <int CKM>
-using CkAcc = typename std::conditional<CKM == 2, uint32_t, unsigned long long>::type;
-
 struct V3Ctx {
     uint32_t lane;
-    uint32_t mask, sh2, mul1, tblr, tmpr;
+    uint32_t mask, sh1, sh2, mul1, mulhi2, m16, m24, m23, one, tblr, tmpr;
     uint32_t srcA0, srcA1, srcC0, srcC1;  // source lanes for carry e = 0 / 1
     bool pA0, pA1, pC0, pC1;              // "take the newer half-step" predicates
-    uint32_t mA0, mA1, mC0, mC1;          // the same as 0/1 multipliers (MTGP3_LERP)
-    uint32_t neg1;                        // 0xFFFFFFFF, opaque to the compiler
+    uint32_t mA0, mA1, mC0, mC1;          // the same as 0/1 multipliers (MTGP3_SEL_IMAD)
+    uint32_t nA0, nA1, nC0, nC1;          // 1 - m
     // bitmap kinds: this stream's bitmap, the piece's first word within the call, the predicate
     uint32_t* bm;
     unsigned long long poff;
@@ -68,10 +85,31 @@ __device__ __forceinline__ uint32_t comp4(const uint4& g, int c) {
 
 __device__ __forceinline__ uint32_t rec3(const V3Ctx& p, uint32_t a, uint32_t b, uint32_t c) {
     const uint32_t x = (a & p.mask) ^ b;
-    // x << sh1 as an IMAD by 2^sh1 (FMA pipe; the ALU pipe is the busier one)
-    const uint32_t y = x ^ (x * p.mul1) ^ (c >> p.sh2);
+#if MTGP3_SH2_IMAD
+    const uint32_t cs = __umulhi(c, p.mulhi2);
+#else
+    const uint32_t cs = c >> p.sh2;
+#endif
+#if MTGP3_SH1_SHF
+    const uint32_t y = x ^ (x << p.sh1) ^ cs;
+#else
+    const uint32_t y = x ^ (x * p.mul1) ^ cs;
+#endif
     return y ^ __shfl_sync(FULL, p.tblr, y, 16);
 }
+
+#if !MTGP3_FOLD_PAIR
+__device__ __forceinline__ uint32_t temper3(const V3Ctx& p, uint32_t r, uint32_t t) {
+#if MTGP3_FOLD_IMAD
+    t ^= __umulhi(t, p.m16);
+    t ^= __umulhi(t, p.m24);
+#else
+    t ^= t >> 16;
+    t ^= t >> 8;
+#endif
+    return r ^ __shfl_sync(FULL, p.tmpr, t, 16);
+}
+#endif
 
 // Tempering indices of two words at once: the XOR of the low nibbles of each word's four bytes.
 // Halves are paired with byte permutes so one LOP3/SHF serves both words (6 ALU ops per two
@@ -84,19 +122,26 @@ __device__ __forceinline__ void fold2(uint32_t t1, uint32_t t2, uint32_t& i1, ui
 }
 
 template <int KIND>
-__device__ __forceinline__ uint32_t conv3(uint32_t o) {
+__device__ __forceinline__ uint32_t conv3(const V3Ctx& p, uint32_t o) {
     if (KIND == MTGP_U32 || KIND >= kKindBitmapBit0) return o;
+#if MTGP3_FLT_FMA
+    // (o >> 9) | 0x3F800000 on the FMA pipe, bit-exact: I2F.RZ keeps o's top 24 significant
+    // bits (what it drops is below bit 9), and the FFMA.RZ with 1.0 truncates 1 + o * 2^-32 to
+    // 23 fraction bits, i.e. 1 + floor(o / 2^9) * 2^-23
+    uint32_t v = __float_as_uint(__fmaf_rz(__uint2float_rz(o), 2.3283064365386963e-10f, 1.0f));
+#else
     uint32_t v = (o >> 9) | 0x3F800000u;
+#endif
     if (KIND == MTGP_F32_01OC) v = __float_as_uint(2.0f - __uint_as_float(v));
     return v;
 }
 
 // Five consecutive operand words for half-step U from the history half-steps
 // h1 = (k=1), h2 = (k=2), h3 = (k=3); residue R; per-carry source lanes / predicates.
-// LERP: the select is lo + m * d with d = hi - lo (dU: the differences of this half-step pair).
-template <int R, int U, bool LERP>
-__device__ __forceinline__ void fetch5(uint32_t W[5], const uint4& h1, const uint4& h2, const uint4& h3, const uint4& dU,
-                                       uint32_t src0, uint32_t src1, bool p0, bool p1, uint32_t m0, uint32_t m1) {
+template <int R, int U, bool IMAD_SEL>
+__device__ __forceinline__ void fetch5(uint32_t W[5], const uint4& h1, const uint4& h2, const uint4& h3, uint32_t src0,
+                                       uint32_t src1, bool p0, bool p1, uint32_t m0, uint32_t m1, uint32_t n0,
+                                       uint32_t n1) {
 #pragma unroll
     for (int j = 0; j < 5; ++j) {
         const int c = (R + j) & 3;
@@ -104,66 +149,69 @@ __device__ __forceinline__ void fetch5(uint32_t W[5], const uint4& h1, const uin
         const uint4& lo = U == 0 ? h1 : h2;  // k = 1 + U
         const uint4& hi = U == 0 ? h2 : h3;  // k = 2 + U
         uint32_t send;
-        if (LERP)
-            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(send) : "r"(comp4(dU, c)), "r"(e ? m1 : m0), "r"(comp4(lo, c)));
-        else
+        if (IMAD_SEL) {
+            // inline PTX keeps the compiler from turning the 0/1 products back into a select
+            uint32_t t;
+            asm("mul.lo.u32 %0, %1, %2;" : "=r"(t) : "r"(comp4(lo, c)), "r"(e ? n1 : n0));
+            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(send) : "r"(comp4(hi, c)), "r"(e ? m1 : m0), "r"(t));
+        } else
             send = (e ? p1 : p0) ? comp4(hi, c) : comp4(lo, c);
         W[j] = __shfl_sync(FULL, send, e ? src1 : src0);
     }
 }
 
-__device__ __forceinline__ uint32_t diff1(uint32_t hi, uint32_t lo, uint32_t neg1) {
-    uint32_t d;
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(lo), "r"(neg1), "r"(hi));
-    return d;
-}
-
-__device__ __forceinline__ uint4 diff4(const uint4& hi, const uint4& lo, uint32_t neg1) {
-    return make_uint4(diff1(hi.x, lo.x, neg1), diff1(hi.y, lo.y, neg1), diff1(hi.z, lo.z, neg1),
-                      diff1(hi.w, lo.w, neg1));
-}
-
 // One 256-word step. Reads history (h1: older step's upper half; h2/h3: newer step's halves),
 // returns the new step's two halves in n0/n1. Stores outputs when the chunk is inside the piece.
-// sp: this lane's 16-byte output slot of the step's first half (piece word n + 4 * lane).
-template <int RC, int KIND, int CKM, bool TAIL>
+template <int RC, int KIND, bool CK, bool TAIL>
 __device__ __forceinline__ void step3(const V3Ctx& p, const uint4& h1, const uint4& h2, const uint4& h3, uint4& n0,
-                                      uint4& n1, uint4* sp, uint32_t n, uint32_t len, uint32_t* win_out,
-                                      uint32_t win_lo, CkAcc<CKM>& sum, uint32_t& xr) {
+                                      uint4& n1, uint32_t* optr, uint32_t n, uint32_t len, uint32_t* win_out,
+                                      uint32_t win_lo, unsigned long long& sum, uint32_t& xr) {
     uint32_t WA[2][5], WC[2][5];
-    constexpr bool kLerpA = MTGP3_LERP & 1, kLerpC = MTGP3_LERP & 2;
-    uint4 d0 = h1, d1 = h2;
-    if (kLerpA || kLerpC) {
-        d0 = diff4(h2, h1, p.neg1);
-        d1 = diff4(h3, h2, p.neg1);
-    }
-    fetch5<1, 0, kLerpA>(WA[0], h1, h2, h3, d0, p.srcA0, p.srcA1, p.pA0, p.pA1, p.mA0, p.mA1);
-    fetch5<1, 1, kLerpA>(WA[1], h1, h2, h3, d1, p.srcA0, p.srcA1, p.pA0, p.pA1, p.mA0, p.mA1);
-    fetch5<RC, 0, kLerpC>(WC[0], h1, h2, h3, d0, p.srcC0, p.srcC1, p.pC0, p.pC1, p.mC0, p.mC1);
-    fetch5<RC, 1, kLerpC>(WC[1], h1, h2, h3, d1, p.srcC0, p.srcC1, p.pC0, p.pC1, p.mC0, p.mC1);
+    constexpr bool kImadA = MTGP3_SEL_IMAD == 1 || MTGP3_SEL_IMAD == 2;
+    constexpr bool kImadC = MTGP3_SEL_IMAD == 1 || MTGP3_SEL_IMAD == 3;
+    fetch5<1, 0, kImadA>(WA[0], h1, h2, h3, p.srcA0, p.srcA1, p.pA0, p.pA1, p.mA0, p.mA1, p.nA0, p.nA1);
+    fetch5<1, 1, kImadA>(WA[1], h1, h2, h3, p.srcA0, p.srcA1, p.pA0, p.pA1, p.mA0, p.mA1, p.nA0, p.nA1);
+    fetch5<RC, 0, kImadC>(WC[0], h1, h2, h3, p.srcC0, p.srcC1, p.pC0, p.pC1, p.mC0, p.mC1, p.nC0, p.nC1);
+    fetch5<RC, 1, kImadC>(WC[1], h1, h2, h3, p.srcC0, p.srcC1, p.pC0, p.pC1, p.mC0, p.mC1, p.nC0, p.nC1);
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
         uint32_t r[4], o[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) r[c] = rec3(p, WA[u][c], WA[u][c + 1], WC[u][c + 1]);
+#if MTGP3_FOLD_PAIR
         uint32_t ix[4];
         fold2(WC[u][0], WC[u][1], ix[0], ix[1]);
         fold2(WC[u][2], WC[u][3], ix[2], ix[3]);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) o[c] = conv3<KIND>(r[c] ^ __shfl_sync(FULL, p.tmpr, ix[c], 16));
+        for (int c = 0; c < 4; ++c) o[c] = conv3<KIND>(p, r[c] ^ __shfl_sync(FULL, p.tmpr, ix[c], 16));
+#else
+#pragma unroll
+        for (int c = 0; c < 4; ++c) o[c] = conv3<KIND>(p, temper3(p, r[c], WC[u][c]));
+#endif
         const uint32_t w0 = n + 128 * u + 4 * p.lane;  // piece word of o[0]
         if constexpr (KIND >= kKindBitmapBit0) {
             bitmap_store<KIND>(p.lane, p.bm, p.poff, p.pred, o, n + 128 * u, !TAIL || w0 < len);
         } else if (!TAIL || w0 < len) {
-            __stcs(sp + 32 * u, make_uint4(o[0], o[1], o[2], o[3]));
-            if (CKM == 2) {
-                sum = sum + o[0] + o[1];  // 3-input IADD3s, mod 2^32
-                sum = sum + o[2] + o[3];
-            } else if (CKM == 1) {
+            __stcs(reinterpret_cast<uint4*>(optr + w0), make_uint4(o[0], o[1], o[2], o[3]));
+            if (CK) {
+#if MTGP3_CK_HILO
+                uint32_t ca = (uint32_t)sum, cb = (uint32_t)(sum >> 32);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(ca) : "r"(o[c]), "r"(p.one));
+                    asm("mad.hi.u32 %0, %1, %2, %0;" : "+r"(cb) : "r"(o[c]), "r"(p.m16));
+                }
+                sum = ((unsigned long long)cb << 32) | ca;
+#elif MTGP3_CK_WIDE
+                // 64-bit sum on the FMA pipe: IMAD.WIDE.U32 sum = o * one + sum (one is opaque)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(sum) : "r"(o[c]), "r"(p.one));
+#else
 #pragma unroll
                 for (int c = 0; c < 4; ++c) sum += o[c];
+#endif
+                xr ^= o[0] ^ o[1] ^ o[2] ^ o[3];
             }
-            if (CKM) xr ^= o[0] ^ o[1] ^ o[2] ^ o[3];
         }
         if (TAIL && win_out) {
             // sequence index of r[c] is kN + w0 + c; the end window is [len, len + kN)
@@ -180,54 +228,59 @@ __device__ __forceinline__ void step3(const V3Ctx& p, const uint4& h1, const uin
     }
 }
 
-// Steps per main-loop trip (even: the history ping-pong returns to its registers every 2 steps).
-#ifndef MTGP3_UNROLL
-#define MTGP3_UNROLL 2
+#if MTGP3_CK_HILO
+// packed (A, B) accumulators -> the exact sum of the words they saw
+__device__ __forceinline__ unsigned long long hilo_sum(unsigned long long packed) {
+    const uint32_t a = (uint32_t)packed, b = (uint32_t)(packed >> 32);
+    return ((unsigned long long)b << 16) + (uint32_t)(a - (b << 16));
+}
 #endif
 
-template <int RC, int KIND, int CKM>
+template <int RC, int KIND, bool CK>
 __device__ __forceinline__ void run3(const V3Ctx& p, uint4 X0, uint4 X1, uint4 Y1, uint32_t* optr, uint32_t len,
-                                     uint32_t* win_out, CkAcc<CKM>& sum, uint32_t& xr) {
+                                     uint32_t* win_out, unsigned long long& sum, uint32_t& xr) {
     // ping-pong: even steps read (Y1 | X0, X1) and write Y; odd steps read (X1 | Y0, Y1), write X
     uint4 Y0;
     const uint32_t steps = (len + kStepWords - 1) / kStepWords;
     // A step at n produces sequence words [N + n, N + n + 256). It needs no store predicate and
     // cannot reach the end window [len, len + N) while n + 256 + N <= len: the main loop runs
-    // such steps (MTGP3_UNROLL per trip, then pairs) with a running store pointer and a trip
-    // count; the (at most three) remaining steps run the predicated tail variant.
-    constexpr uint32_t U = MTGP3_UNROLL;
-    uint4* sp = reinterpret_cast<uint4*>(optr) + p.lane;
-    const uint32_t full = len > kN ? (len - kN) / kStepWords : 0;  // steps without predicates
+    // pairs of such steps; the (at most three) remaining steps run the predicated tail variant.
     uint32_t m = 0;
-    if (U > 2) {
-        for (uint32_t it = full / U; it; --it, sp += 64 * U, m += U) {
-#pragma unroll
-            for (uint32_t q = 0; q < U; q += 2) {
-                step3<RC, KIND, CKM, false>(p, Y1, X0, X1, Y0, Y1, sp + 64 * q, (m + q) * kStepWords, len, nullptr, len,
-                                            sum, xr);
-                step3<RC, KIND, CKM, false>(p, X1, Y0, Y1, X0, X1, sp + 64 * q + 64, (m + q + 1) * kStepWords, len,
-                                            nullptr, len, sum, xr);
-            }
+#if MTGP3_CK_HILO
+    unsigned long long tot = sum;
+    sum = 0;
+#endif
+    for (; (m + 2) * kStepWords + kN <= len; m += 2) {
+        step3<RC, KIND, CK, false>(p, Y1, X0, X1, Y0, Y1, optr, m * kStepWords, len, nullptr, len, sum, xr);
+        step3<RC, KIND, CK, false>(p, X1, Y0, Y1, X0, X1, optr, (m + 1) * kStepWords, len, nullptr, len, sum, xr);
+#if MTGP3_CK_HILO
+        if (CK && (m & 8190u) == 8190u) {  // 8192 steps = 2^16 words per lane
+            tot += hilo_sum(sum);
+            sum = 0;
         }
+#endif
     }
-    for (uint32_t it = (full - m) / 2; it; --it, sp += 128, m += 2) {
-        step3<RC, KIND, CKM, false>(p, Y1, X0, X1, Y0, Y1, sp, m * kStepWords, len, nullptr, len, sum, xr);
-        step3<RC, KIND, CKM, false>(p, X1, Y0, Y1, X0, X1, sp + 64, (m + 1) * kStepWords, len, nullptr, len, sum, xr);
+#if MTGP3_CK_HILO
+    if (CK) {
+        tot += hilo_sum(sum);
+        sum = 0;
     }
+#endif
     while (m < steps) {
-        step3<RC, KIND, CKM, true>(p, Y1, X0, X1, Y0, Y1, sp, m * kStepWords, len, win_out, len, sum, xr);
-        sp += 64;
+        step3<RC, KIND, CK, true>(p, Y1, X0, X1, Y0, Y1, optr, m * kStepWords, len, win_out, len, sum, xr);
         if (++m >= steps) break;
-        step3<RC, KIND, CKM, true>(p, X1, Y0, Y1, X0, X1, sp, m * kStepWords, len, win_out, len, sum, xr);
-        sp += 64;
+        step3<RC, KIND, CK, true>(p, X1, Y0, Y1, X0, X1, optr, m * kStepWords, len, win_out, len, sum, xr);
         ++m;
     }
+#if MTGP3_CK_HILO
+    if (CK) sum = tot + hilo_sum(sum);
+#endif
 }
 
 }  // namespace
 
-template <int KIND, int CKM>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, kMinCtas3) gen3_kernel(GenArgs a) {
+template <int KIND, bool CK>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, MTGP3_MIN_CTAS) gen3_kernel(GenArgs a) {
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t team = blockIdx.x * kWarpsPerCta + warp;
@@ -240,13 +293,21 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, kMinCtas3) gen3_kernel(GenA
     p.pA1 = lane < 9;
     p.mA0 = p.pA0;
     p.mA1 = p.pA1;
+    p.nA0 = 1u - p.mA0;
+    p.nA1 = 1u - p.mA1;
     const TeamWork tw = a.teams[team];
     for (uint32_t pi = tw.first; pi < tw.first + tw.count; ++pi) {
         const Piece pc = a.pieces[pi];
         const DevParams& prm = a.params[pc.set];
         p.mask = prm.mask;
+        p.sh1 = prm.sh1;
         p.sh2 = prm.sh2;
         p.mul1 = prm.mul1;
+        p.mulhi2 = prm.mulhi2;
+        p.m16 = prm.m16;
+        p.m24 = prm.m24;
+        p.m23 = prm.m23;
+        p.one = prm.one;
         p.tblr = prm.tbl[lane & 15];
         p.tmpr = prm.tmp[lane & 15];
         const uint32_t pos = prm.pos;
@@ -257,7 +318,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, kMinCtas3) gen3_kernel(GenA
         p.pC1 = lane < thr1;
         p.mC0 = p.pC0;
         p.mC1 = p.pC1;
-        p.neg1 = 0u - prm.one;
+        p.nC0 = 1u - p.mC0;
+        p.nC1 = 1u - p.mC1;
         uint32_t* optr = reinterpret_cast<uint32_t*>(a.out) + (size_t)pc.set * a.L + pc.offset;
         if (KIND >= kKindBitmapBit0) {
             p.bm = reinterpret_cast<uint32_t*>(a.out) + (size_t)pc.set * ((a.L + 31) / 32);
@@ -287,24 +349,22 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, kMinCtas3) gen3_kernel(GenA
             // window words that are still start-window words (pieces shorter than N)
             for (uint32_t j = lane; j + len < kN; j += 32) win_out[j] = w0[len + j];
         }
-        CkAcc<CKM> sum = 0;
+        unsigned long long sum = 0;
         uint32_t xr = 0;
         switch (pos & 3u) {
-            case 0: run3<0, KIND, CKM>(p, X0, X1, Y1, optr, len, win_out, sum, xr); break;
-            case 1: run3<1, KIND, CKM>(p, X0, X1, Y1, optr, len, win_out, sum, xr); break;
-            case 2: run3<2, KIND, CKM>(p, X0, X1, Y1, optr, len, win_out, sum, xr); break;
-            default: run3<3, KIND, CKM>(p, X0, X1, Y1, optr, len, win_out, sum, xr); break;
+            case 0: run3<0, KIND, CK>(p, X0, X1, Y1, optr, len, win_out, sum, xr); break;
+            case 1: run3<1, KIND, CK>(p, X0, X1, Y1, optr, len, win_out, sum, xr); break;
+            case 2: run3<2, KIND, CK>(p, X0, X1, Y1, optr, len, win_out, sum, xr); break;
+            default: run3<3, KIND, CK>(p, X0, X1, Y1, optr, len, win_out, sum, xr); break;
         }
-        if (CKM) {
+        if (CK) {
 #pragma unroll
             for (int s = 16; s > 0; s >>= 1) {
                 sum += __shfl_xor_sync(FULL, sum, s);
                 xr ^= __shfl_xor_sync(FULL, xr, s);
             }
             if (lane == 0) {
-                // mode 2 adds the piece's sum mod 2^32: only the low half of sum64 is meaningful
-                // (mtgp_checksums masks the high half for contexts that ran mode 2)
-                atomicAdd(&a.ck[pc.set].sum64, (unsigned long long)sum);
+                atomicAdd(&a.ck[pc.set].sum64, sum);
                 atomicXor(&a.ck[pc.set].xor32, xr);
                 atomicAdd(&a.ck[pc.set].words, (unsigned long long)len);
             }
@@ -313,54 +373,48 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, kMinCtas3) gen3_kernel(GenA
     }
 }
 
-template <int KIND, int CKM>
+template <int KIND, bool CK>
 static cudaError_t launch3_t(const GenArgs& a, cudaStream_t st) {
     const uint32_t grid = (a.n_teams + kWarpsPerCta - 1) / kWarpsPerCta;
-    gen3_kernel<KIND, CKM><<<grid, kWarpsPerCta * 32, 0, st>>>(a);
+    gen3_kernel<KIND, CK><<<grid, kWarpsPerCta * 32, 0, st>>>(a);
     return cudaGetLastError();
 }
 
-template <int KIND, int CKM>
+template <int KIND, bool CK>
 static int occ3_t() {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gen3_kernel<KIND, CKM>, kWarpsPerCta * 32, 0) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gen3_kernel<KIND, CK>, kWarpsPerCta * 32, 0) != cudaSuccess)
         return 0;
     return n;
 }
 
-cudaError_t launch_gen3(int kind, int ck_mode, const GenArgs& a, cudaStream_t st) {
+cudaError_t launch_gen3(int kind, bool cksum, const GenArgs& a, cudaStream_t st) {
     if (a.n_teams == 0) return cudaSuccess;
-    switch (kind * 3 + ck_mode) {
-        case 0: return launch3_t<MTGP_U32, 0>(a, st);
-        case 1: return launch3_t<MTGP_U32, 1>(a, st);
-        case 2: return launch3_t<MTGP_U32, 2>(a, st);
-        case 3: return launch3_t<MTGP_F32_12, 0>(a, st);
-        case 4: return launch3_t<MTGP_F32_12, 1>(a, st);
-        case 5: return launch3_t<MTGP_F32_12, 2>(a, st);
-        case 6: return launch3_t<MTGP_F32_01OC, 0>(a, st);
-        case 7: return launch3_t<MTGP_F32_01OC, 1>(a, st);
-        case 8: return launch3_t<MTGP_F32_01OC, 2>(a, st);
+    switch (kind * 2 + (cksum ? 1 : 0)) {
+        case 0: return launch3_t<MTGP_U32, false>(a, st);
+        case 1: return launch3_t<MTGP_U32, true>(a, st);
+        case 2: return launch3_t<MTGP_F32_12, false>(a, st);
+        case 3: return launch3_t<MTGP_F32_12, true>(a, st);
+        case 4: return launch3_t<MTGP_F32_01OC, false>(a, st);
+        case 5: return launch3_t<MTGP_F32_01OC, true>(a, st);
     }
     // bitmap kinds carry no checksums (the words are never output)
-    if (kind == kKindBitmapBit0) return launch3_t<kKindBitmapBit0, 0>(a, st);
-    if (kind == kKindBitmapRange) return launch3_t<kKindBitmapRange, 0>(a, st);
+    if (kind == kKindBitmapBit0) return launch3_t<kKindBitmapBit0, false>(a, st);
+    if (kind == kKindBitmapRange) return launch3_t<kKindBitmapRange, false>(a, st);
     return cudaErrorInvalidValue;
 }
 
-int gen3_ctas_per_sm(int kind, int ck_mode) {
-    switch (kind * 3 + ck_mode) {
-        case 0: return occ3_t<MTGP_U32, 0>();
-        case 1: return occ3_t<MTGP_U32, 1>();
-        case 2: return occ3_t<MTGP_U32, 2>();
-        case 3: return occ3_t<MTGP_F32_12, 0>();
-        case 4: return occ3_t<MTGP_F32_12, 1>();
-        case 5: return occ3_t<MTGP_F32_12, 2>();
-        case 6: return occ3_t<MTGP_F32_01OC, 0>();
-        case 7: return occ3_t<MTGP_F32_01OC, 1>();
-        case 8: return occ3_t<MTGP_F32_01OC, 2>();
+int gen3_ctas_per_sm(int kind, bool cksum) {
+    switch (kind * 2 + (cksum ? 1 : 0)) {
+        case 0: return occ3_t<MTGP_U32, false>();
+        case 1: return occ3_t<MTGP_U32, true>();
+        case 2: return occ3_t<MTGP_F32_12, false>();
+        case 3: return occ3_t<MTGP_F32_12, true>();
+        case 4: return occ3_t<MTGP_F32_01OC, false>();
+        case 5: return occ3_t<MTGP_F32_01OC, true>();
     }
-    if (kind == kKindBitmapBit0) return occ3_t<kKindBitmapBit0, 0>();
-    if (kind == kKindBitmapRange) return occ3_t<kKindBitmapRange, 0>();
+    if (kind == kKindBitmapBit0) return occ3_t<kKindBitmapBit0, false>();
+    if (kind == kKindBitmapRange) return occ3_t<kKindBitmapRange, false>();
     return 0;
 }
 
