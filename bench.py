@@ -11,9 +11,15 @@ Multi-GPU (torchrun): weak scaling. Rank r owns parameter sets [200r, 200r+200) 
 sets for r=0, deterministic synthetic MTGP-11213 sets beyond), no collective on the hot path;
 after timing, the per-stream checksums are gathered over NCCL (the only collective).
 
---impl reference: the reference's own CPU generator (oracle/_ref: proj/src/{generator,params,
-word_source}.cpp compiled from its sources) filling MT19937 streams through
-make_word_source()/WordSource::fill on every host core, rank 0 only.
+--impl reference: the CPU implementation of the same path on the box's host cores, rank 0 only,
+same config, metric and unit. The reference implements no MTGP32, so for the
+MTGP32 configs this is the MTGP32 CPU port (oracle/mtgp32_oracle.c, the restatement the
+parity fixtures come from): the config's parameter sets and seeds, every stream filled through
+a reused 2^20-word buffer (WordSource::fill semantics), one stream per thread at a time on all
+cores, a bounded sample of each stream per step (cpu_baseline.kind "port"). The reference's own
+generator (oracle/_ref: proj/src/{generator,params,word_source}.cpp compiled from its sources,
+MT19937 through make_word_source()/WordSource::fill) is timed beside it as a side field, and is
+the arm itself for --config mt19937.
 """
 import argparse
 import json
@@ -60,12 +66,15 @@ def parse():
     ap.add_argument("--calls", type=int, default=None,
                     help="device calls per step (output buffer = step/calls); default 2, 1 for c5")
     ap.add_argument("--no-checksum", action="store_true")
-    ap.add_argument("--checksum-mode", type=int, default=1, choices=[1, 2],
+    ap.add_argument("--checksum-mode", type=int, default=2, choices=[1, 2],
                     help="MTGP_OPT_CHECKSUM: 1 sum64 + xor32, 2 sum32 + xor32 (the fixture's sums mod 2^32)")
     ap.add_argument("--min-piece-words", type=int, default=None, help="MTGP_OPT_MIN_PIECE_WORDS (default: library's)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-words-per-thread", type=int, default=1 << 28)
+    ap.add_argument("--cpu-words-per-thread", type=int, default=1 << 28,
+                    help="MT19937 reference (oracle/_ref): words per thread per step")
+    ap.add_argument("--cpu-words-per-stream", type=int, default=1 << 22,
+                    help="MTGP32 CPU port: words of every stream per step (a bounded sample of the step)")
     ap.add_argument("--as-rank", type=int, default=None,
                     help="single process: generate rank R's shard of a multi-GPU run (its parameter sets / seeds), "
                          "to time every rank's workload alone on one GPU")
@@ -225,48 +234,81 @@ def cpu_reference(words_per_thread: int, threads: int):
     return threads * words_per_thread / secs / 1e9, secs
 
 
-def cpu_mtgp_port(sets, seeds, threads: int, n: int = 1 << 24, min_secs: float = 1.0):
-    """The oracle's MTGP32 bulk fill, one set per thread, repeated into the same buffer until
-    about `min_secs` of wall time (a bounded sample: ~threads x min_secs of CPU work)."""
+def config_sets(args, shard_rank: int = 0, shard_world: int = 1):
+    """(parameter sets, seeds, global first set) of a config for one rank, as the GPU arm uses."""
+    from paper_1501_07701_b200 import mtgp, shard, tables
+    mexp, _, _, _ = CONFIGS[args.config]
+    S = args.sets
+    if args.config in MT_CONFIGS:
+        return [mtgp.mt19937_status()] * S, [5489 + shard_rank * S + i for i in range(S)], shard_rank * S
+    if args.config == "c5":
+        r = shard.status_range(C5_SETS, shard_rank, shard_world)
+        return tables.sets_for(mexp, len(r), first=r.start), [1] * len(r), r.start
+    return shard.sets_for_rank(mexp, S, shard_rank), [1] * S, shard_rank * S
+
+
+def cpu_port_step(sets, seeds, n: int, kind: int, cores: int):
+    """One step of the CPU port: every stream's next n words (fill() into a reused buffer)."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle_py
-    k = min(threads, len(sets))
-    out = np.empty((k, n), dtype=np.uint32)
-    secs, reps = 0.0, 0
-    while secs < min_secs and reps < 64:
-        _, s = oracle_py.mtgp_bulk(sets[:k], seeds[:k], n, threads=k, out=out)
-        secs += s
-        reps += 1
-    return k * n * reps / secs / 1e9, secs, n * reps
+    secs = oracle_py.fill_bulk(sets, seeds, n, 1 << 20, kind, cores)
+    return len(sets) * n / secs / 1e9, secs
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
     cores = len(os.sched_getaffinity(0))
-    wpt = args.cpu_words_per_thread
-    for _ in range(args.warmup):
-        cpu_reference(wpt // 8, cores)
-    vals, secs = [], []
-    for _ in range(args.steps):
-        v, s = cpu_reference(wpt, cores)
-        vals.append(v)
-        secs.append(s)
-    v = float(np.median(vals))
     mexp, kind, L, label = CONFIGS[args.config]
+    is_mt = args.config in MT_CONFIGS
+    vals, secs = [], []
+    if is_mt:
+        wpt = args.cpu_words_per_thread
+        for _ in range(args.warmup):
+            cpu_reference(wpt // 8, cores)
+        for _ in range(args.steps):
+            v, sec = cpu_reference(wpt, cores)
+            vals.append(v)
+            secs.append(sec)
+        sample = f"{cores} threads x {wpt} MT19937 words in 2^18-word fill() calls per step"
+        kind_s, impl = "reference", "oracle/_ref: the reference's MtWordSource::fill compiled from its sources"
+        S = args.sets
+    else:
+        sets, seeds, _ = config_sets(args)
+        S = len(sets)
+        n = min(args.cpu_words_per_stream, L)
+        for _ in range(args.warmup):
+            cpu_port_step(sets, seeds, max(1, n // 8), kind, cores)
+        for _ in range(args.steps):
+            v, sec = cpu_port_step(sets, seeds, n, kind, cores)
+            vals.append(v)
+            secs.append(sec)
+        sample = (f"all {S} streams of the config x the first {n} words each per step (of {L} per step on the GPU), "
+                  f"2^20-word fill() buffer reused per thread, {cores} threads")
+        kind_s, impl = "port", "oracle/mtgp32_oracle.c (MTGP32 CPU port; the reference implements no MTGP32)"
+    v = float(np.median(vals))
     line = {
         "impl": "reference",
         "metric": "Gsamples/s (uint32 & float) per GPU and at 1/2/4/8 B200; % of HBM write peak",
         "value": round(v, 4), "unit": "Gsamples/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1000 * float(np.median(secs)), 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "higher_is_better": True, "scaling": "strong" if args.config == "c5" else "weak", "vs_baseline": None,
+        "dtype": ["u32", "f32", "f32"][kind],
         "data": "synthetic (seeded generator streams; no input data)",
-        "config": {"workload": label, "reference_generator": "MT19937 via make_word_source/WordSource::fill "
-                   "(the reference implements no MTGP32; SURVEY.md §0)"},
-        "cpu_baseline": {"value": round(v, 4), "unit": "Gsamples/s", "cores": cores, "kind": "reference",
-                         "sample": f"{cores} threads x {wpt} MT19937 words in 2^18-word fill() calls per step"},
+        "config": {"workload": label, "sets_per_gpu": S, "seed": 1 if not is_mt else "5489+i",
+                   "words_per_set_per_step": L, "implementation": impl},
+        "cpu_baseline": {"value": round(v, 4), "unit": "Gsamples/s", "cores": cores, "kind": kind_s, "sample": sample},
         "e2e": {"value": round(v, 4), "unit": "Gsamples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not is_mt:  # the reference's own generator (a different recurrence) beside it
+        try:
+            rv, rs = cpu_reference(args.cpu_words_per_thread, cores)
+            line["mt19937_reference"] = {
+                "value": round(rv, 4), "unit": "Gsamples/s", "cores": cores, "kind": "reference",
+                "sample": f"oracle/_ref MtWordSource::fill (MT19937) x {cores} threads x {args.cpu_words_per_thread} "
+                          f"words, {rs:.2f} s"}
+        except Exception as e:  # noqa: BLE001
+            line["mt19937_reference"] = {"value": None, "error": str(e)[:200]}
     print(json.dumps(line), flush=True)
 
 
@@ -438,17 +480,22 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cores = len(os.sched_getaffinity(0))
-            v, secs = cpu_reference(args.cpu_words_per_thread, cores)
-            cpu = {"value": round(v, 4), "unit": "Gsamples/s", "cores": cores, "kind": "reference",
-                   "sample": f"reference MtWordSource::fill (MT19937) x {cores} pinned threads x "
-                             f"{args.cpu_words_per_thread} words, {secs:.2f} s wall; the reference has no MTGP32"}
-            # the CPU MTGP32 restatement (oracle port) timed the same way, one
-            # certified set per core, so the MTGP32-vs-MT19937 CPU cost is visible next to the GPU
-            if not is_mt:  # the reference itself is the MT19937 baseline; add the MTGP32 port's cost
-                pv, psecs, pn = cpu_mtgp_port(sets, seeds, cores)
-                cpu["mtgp32_port"] = {"value": round(pv, 4), "unit": "Gsamples/s", "cores": cores, "kind": "port",
-                                      "sample": f"oracle/mtgp32_oracle.c bulk fill, {cores} sets x {pn} words "
-                                                f"(one thread per set), {psecs:.2f} s wall"}
+            if is_mt:  # the reference itself implements this generator
+                v, secs = cpu_reference(args.cpu_words_per_thread, cores)
+                cpu = {"value": round(v, 4), "unit": "Gsamples/s", "cores": cores, "kind": "reference",
+                       "sample": f"reference MtWordSource::fill (MT19937) x {cores} pinned threads x "
+                                 f"{args.cpu_words_per_thread} words, {secs:.2f} s wall"}
+            else:  # the MTGP32 CPU port on the same sets and seeds
+                n = min(args.cpu_words_per_stream, L_step)
+                v, secs = cpu_port_step(sets, seeds, n, kind, cores)
+                cpu = {"value": round(v, 4), "unit": "Gsamples/s", "cores": cores, "kind": "port",
+                       "sample": f"oracle/mtgp32_oracle.c: all {len(sets)} streams x first {n} words, 2^20-word fill() "
+                                 f"buffer per thread, {cores} threads, {secs:.2f} s wall"}
+                rv, rs = cpu_reference(args.cpu_words_per_thread, cores)
+                cpu["mt19937_reference"] = {
+                    "value": round(rv, 4), "unit": "Gsamples/s", "cores": cores, "kind": "reference",
+                    "sample": f"oracle/_ref MtWordSource::fill (MT19937), the reference's own generator, {cores} "
+                              f"threads x {args.cpu_words_per_thread} words, {rs:.2f} s wall"}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "error": str(e)[:200]}
 

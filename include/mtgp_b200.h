@@ -257,6 +257,38 @@ int mtgp_mt_charpoly_digest(mtgp_ctx* ctx, char* out);
 int mtgp_gf2_is_irreducible(const uint8_t* coeff_bits, uint64_t n, int32_t* out);
 
 /* ------------------------------------------------------------------------------------------
+ * Several GPUs in one process (north_star (5)).
+ *
+ * The reference's only parallelism is a pool of worker threads over independent statuses
+ * (proj/src/sieve.cpp:170-177; one generator per worker). mtgp_multi splits
+ * n_sets parameter sets into contiguous balanced ID ranges, one per device (mtgp_shard_range),
+ * owns one context per device, and runs every generation call with one host thread per device
+ * (no collective on the hot path). The per-stream checksums are all-gathered once, over NCCL
+ * (ncclCommInitAll + ncclAllGather on the devices' streams; libnccl is dlopen'ed) when it loads
+ * and the devices are distinct, else by host concatenation.
+ * ------------------------------------------------------------------------------------------ */
+typedef struct mtgp_multi mtgp_multi;
+
+/* Set IDs [*first, *first + *count) of `rank` when n_sets are split over `world` ranks: the
+   first n_sets % world ranks get one more (the split bench.py's config 5 uses). */
+int mtgp_shard_range(uint32_t n_sets, uint32_t world, uint32_t rank, uint32_t* first, uint32_t* count);
+
+/* Contexts for sets[first_r .. first_r + count_r) on devices[r], seeded with the matching seeds.
+   gather: 0 = NCCL when possible else host, 1 = NCCL required, 2 = host. */
+int mtgp_multi_create(mtgp_multi** out, const int* devices, uint32_t n_devices, const mtgp_params* sets,
+                      uint32_t n_sets, const uint32_t* seeds, int gather);
+int mtgp_multi_destroy(mtgp_multi* m);
+/* *nccl = 1 when the checksum gather runs over NCCL. */
+int mtgp_multi_info(const mtgp_multi* m, uint32_t* n_devices, int* nccl);
+/* The context of `rank` (options, timing, positions) and its set range. Owned by m. */
+int mtgp_multi_context(mtgp_multi* m, uint32_t rank, mtgp_ctx** ctx, uint32_t* first_set, uint32_t* n_sets);
+/* words_per_stream words of every stream: device r writes its streams, per-stream contiguous,
+   into device memory outs[r] (on devices[r]); one host thread per device; returns when done. */
+int mtgp_multi_generate(mtgp_multi* m, int kind, void* const* outs, uint64_t words_per_stream);
+/* Per-stream checksums of all n_sets streams in global set order (the gather). */
+int mtgp_multi_checksums(mtgp_multi* m, mtgp_cksum* out);
+
+/* ------------------------------------------------------------------------------------------
  * Device-side statistical tests (GPU-fed consumers).
  *
  * The reference runs each campaign cell (status, seed, test) as run_test(BufferedStream over a

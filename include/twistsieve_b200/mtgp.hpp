@@ -29,6 +29,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "mtgp_b200.h"
@@ -163,6 +164,35 @@ private:
     std::uint32_t n_sets_ = 0, n_ = 0;
 };
 
+/// Several GPUs in one process (C-ABI mtgp_multi): n sets split into contiguous balanced ID
+/// ranges, one context and one host thread per device, no collective on the hot path, the
+/// per-stream checksums all-gathered over NCCL (north_star (5)). The reference's
+/// parallelism is its worker pool over independent statuses (proj/src/sieve.cpp:170-177).
+class MultiGpuBatch {
+public:
+    enum class Gather { automatic = 0, nccl = 1, host = 2 };
+    MultiGpuBatch(const std::vector<MtgpStatus>& sets, const std::vector<std::uint32_t>& seeds,
+                  const std::vector<int>& devices, Gather gather = Gather::automatic);
+    ~MultiGpuBatch();
+    MultiGpuBatch(const MultiGpuBatch&) = delete;
+    MultiGpuBatch& operator=(const MultiGpuBatch&) = delete;
+    std::uint32_t devices() const { return n_dev_; }
+    bool nccl() const { return nccl_; }
+    /// global set IDs [first, first + count) of device slot r
+    std::pair<std::uint32_t, std::uint32_t> range(std::uint32_t r) const;
+    /// words_per_stream outputs of every stream; device slot r writes its streams into device
+    /// memory outs[r] (per-stream contiguous). Returns when every device is done.
+    void generate_device(OutputKind kind, const std::vector<void*>& outs, std::uint64_t words_per_stream);
+    /// all streams' checksums in global set order (the all-gather)
+    std::vector<mtgp_cksum> checksums();
+    mtgp_ctx* context(std::uint32_t r);
+
+private:
+    mtgp_multi* m_ = nullptr;
+    std::uint32_t n_dev_ = 0, n_sets_ = 0;
+    bool nccl_ = false;
+};
+
 /// One MTGP32 stream served from device-generated chunks -- the GPU counterpart of
 /// MtWordSource (word_source.hpp:27-37): fill() returns the next words of the stream exactly
 /// as successive next_u32() calls would.
@@ -207,5 +237,22 @@ bool verify_digest(const MtStatus& status, const std::string& digest, int device
 /// Factory with the reference's shape (word_source.cpp:5-16).
 std::unique_ptr<WordSource> make_word_source(const MtgpStatus& params, std::uint32_t seed);
 std::unique_ptr<WordSource> make_word_source(const MtStatus& params, std::uint32_t seed);
+
+#ifdef TWISTSIEVE_B200_WITH_REFERENCE
+/// The recurrence fields of a reference status (proj/include/twistsieve/params.hpp:21-42).
+MtStatus from_reference(const twistsieve::ParameterizedStatus& p);
+
+/// The reference's own factory signature (word_source.hpp:75-76), dispatching on
+/// ParameterizedStatus::engine like proj/src/word_source.cpp:5-16, with the Engine::mt branch
+/// served by the GPU: a GpuWordSource over the status's own recurrence, word for word what
+/// MtWordSource would fill. The planted calibration engines (constant, lfsr16) go to the
+/// reference's make_word_source unchanged. MTGP32 parameter sets have no Engine value in the
+/// reference; the MtgpStatus overload above is their tag. Throws std::invalid_argument for an
+/// invalid status (the reference's own ParameterizedStatus::validate), std::runtime_error when
+/// no sm_100 device is usable (there is no CPU fallback). Call it qualified
+/// (twistsieve_b200::make_word_source): argument-dependent lookup also finds the reference's.
+std::unique_ptr<twistsieve::WordSource> make_word_source(const twistsieve::ParameterizedStatus& params,
+                                                         std::uint32_t seed);
+#endif
 
 }  // namespace twistsieve_b200

@@ -15,6 +15,7 @@
 #include "oracle.h"
 
 #include <pthread.h>
+#include <stdlib.h>
 #include <string.h>
 #include <time.h>
 
@@ -320,5 +321,57 @@ double oracle_mtgp_cksum_stream(const oracle_mtgp_params* sets, const uint32_t* 
     for (int t = 0; t < threads; ++t) pthread_create(&th[t], NULL, ck_worker, &job);
     for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
     clock_gettime(CLOCK_MONOTONIC, &t1);
+    return (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
+}
+
+/* ---- CPU baseline: every stream filled through a reused fill() buffer (WordSource::fill) ----
+ * Threads take streams dynamically; each stream is seeded, then filled `chunk` words at a time
+ * into the thread's private buffer (word_source.hpp:21-25 semantics: the caller owns the span)
+ * until it has produced n words. The buffer's checksum is folded into *sink so no work can be
+ * elided. Returns seconds. */
+typedef struct fill_job {
+    const oracle_mtgp_params* sets;
+    const uint32_t* seeds;
+    uint32_t n_sets;
+    uint64_t n, chunk;
+    int kind;
+    uint32_t* next;
+    uint64_t sink;
+} fill_job;
+
+static void* fill_worker(void* arg) {
+    fill_job* j = (fill_job*)arg;
+    uint32_t* buf = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)j->chunk);
+    oracle_mtgp g;
+    uint64_t acc = 0;
+    for (;;) {
+        const uint32_t s = __atomic_fetch_add(j->next, 1u, __ATOMIC_RELAXED);
+        if (s >= j->n_sets) break;
+        oracle_mtgp_init(&g, &j->sets[s], j->seeds[s]);
+        for (uint64_t done = 0; done < j->n; done += j->chunk) {
+            const uint64_t c = j->n - done < j->chunk ? j->n - done : j->chunk;
+            oracle_mtgp_fill(&g, buf, (size_t)c, j->kind);
+            acc += buf[c - 1];
+        }
+    }
+    free(buf);
+    __atomic_fetch_add(&j->sink, acc, __ATOMIC_RELAXED);
+    return NULL;
+}
+
+double oracle_mtgp_fill_bulk(const oracle_mtgp_params* sets, const uint32_t* seeds, uint32_t n_sets, uint64_t n,
+                             uint64_t chunk, int kind, int threads, uint64_t* sink) {
+    if (threads < 1) threads = 1;
+    if (threads > 1024) threads = 1024;
+    if (chunk < 1) chunk = 1;
+    pthread_t th[1024];
+    uint32_t next = 0;
+    fill_job job = {sets, seeds, n_sets, n, chunk, kind, &next, 0};
+    struct timespec t0, t1;
+    clock_gettime(CLOCK_MONOTONIC, &t0);
+    for (int t = 0; t < threads; ++t) pthread_create(&th[t], NULL, fill_worker, &job);
+    for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+    clock_gettime(CLOCK_MONOTONIC, &t1);
+    if (sink) *sink = job.sink;
     return (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
 }

@@ -89,6 +89,12 @@ double oracle_mtgp_cksum_stream(const oracle_mtgp_params* sets, const uint32_t* 
                                 uint64_t rec_every, uint32_t n_rec, int flags, oracle_stream_ck* out,
                                 int threads);
 
+/* CPU baseline of the generation path: every stream seeded and filled `chunk` words at a time
+ * into a reused per-thread buffer until it has produced n words (WordSource::fill semantics,
+ * word_source.hpp:21-25), streams handed to threads dynamically. Returns seconds. */
+double oracle_mtgp_fill_bulk(const oracle_mtgp_params* sets, const uint32_t* seeds, uint32_t n_sets, uint64_t n,
+                             uint64_t chunk, int kind, int threads, uint64_t* sink);
+
 /* ---- classic MT, the reference Engine::mt ---- */
 typedef struct oracle_mt_params {
     uint32_t mexp, n, m, r, a;

@@ -65,6 +65,9 @@ def lib() -> C.CDLL:
         L.oracle_mtgp_cksum_stream.argtypes = [C.POINTER(OracleParams), C.POINTER(C.c_uint32), C.c_uint32,
                                                C.c_uint64, C.c_uint32, C.c_int, C.c_void_p, C.c_int]
         L.oracle_mtgp_cksum_stream.restype = C.c_double
+        L.oracle_mtgp_fill_bulk.argtypes = [C.POINTER(OracleParams), C.POINTER(C.c_uint32), C.c_uint32, C.c_uint64,
+                                            C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint64)]
+        L.oracle_mtgp_fill_bulk.restype = C.c_double
         L.oracle_mt19937_params.argtypes = [C.POINTER(OracleMtParams)]
         L.oracle_mt_init.argtypes = [C.POINTER(OracleMt), C.POINTER(OracleMtParams), C.c_uint32]
         L.oracle_mt_fill.argtypes = [C.POINTER(OracleMt), C.c_void_p, C.c_size_t]
@@ -148,6 +151,16 @@ def cksum_stream(sets: Sequence, seeds: Sequence[int], rec_every: int, n_rec: in
     secs = lib().oracle_mtgp_cksum_stream(arr, sd, len(sets), rec_every, n_rec, int(with_float) | (2 if scalar else 0),
                                           out.ctypes.data_as(C.c_void_p), threads)
     return out, secs
+
+
+def fill_bulk(sets: Sequence, seeds: Sequence[int], n: int, chunk: int = 1 << 20, kind: int = 0,
+              threads: int = 8) -> float:
+    """CPU baseline: every stream's first n words through a reused chunk-word fill buffer per
+    thread (WordSource::fill semantics); returns seconds."""
+    arr = (OracleParams * len(sets))(*[to_oracle_params(p) for p in sets])
+    sd = (C.c_uint32 * len(seeds))(*[s & 0xFFFFFFFF for s in seeds])
+    sink = C.c_uint64()
+    return lib().oracle_mtgp_fill_bulk(arr, sd, len(sets), n, chunk, kind, threads, C.byref(sink))
 
 
 def cksum(words: np.ndarray):

@@ -508,7 +508,7 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     const int cps = use_mt3  ? mt_gen3_ctas_per_sm(I.N, r.kind, r.cksum)
                     : I.mt   ? mt_gen2_ctas_per_sm(I.N, r.kind, r.cksum)
                     : use_v3 ? gen3_ctas_per_sm(r.kind, ck_mode)
-                    : use_v4 ? gen4_ctas_per_sm(I.M, r.kind, r.cksum)
+                    : use_v4 ? gen4_ctas_per_sm(I.M, r.kind, ck_mode)
                              : gen_ctas_per_sm(I.M, r.kind, r.cksum);
     if (cps <= 0) {
         err = "generation kernel cannot be resident";
@@ -597,7 +597,7 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         ga.pred = r.pred;
         if (r.timing) r.timing->record(r.stream, &g0);
         e = use_v3   ? launch_gen3(r.kind, ck_mode, ga, r.stream)
-            : use_v4 ? launch_gen4(I.M, r.kind, r.cksum, ga, r.stream)
+            : use_v4 ? launch_gen4(I.M, r.kind, ck_mode, ga, r.stream)
                      : launch_gen(I.M, r.kind, r.cksum, ga, r.stream);
         if (e != cudaSuccess) return e;
         r.version = use_v3 ? 3 : use_v4 ? 4 : 2;

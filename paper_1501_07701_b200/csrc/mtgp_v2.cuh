@@ -60,7 +60,7 @@ cudaError_t launch_gen3(int kind, int ck_mode, const GenArgs& a, cudaStream_t st
 int gen3_ctas_per_sm(int kind, int ck_mode);
 // v4: gen3's register-resident design templated on the exponent (csrc/mtgp_v4.cu)
 bool v4_supports(uint32_t mexp, int kind);
-cudaError_t launch_gen4(uint32_t mexp, int kind, bool cksum, const GenArgs& a, cudaStream_t st);
-int gen4_ctas_per_sm(uint32_t mexp, int kind, bool cksum);
+cudaError_t launch_gen4(uint32_t mexp, int kind, int ck_mode, const GenArgs& a, cudaStream_t st);
+int gen4_ctas_per_sm(uint32_t mexp, int kind, int ck_mode);
 
 }  // namespace mtgpb

@@ -9,23 +9,23 @@ bool v4_supports(uint32_t mexp, int kind) {
     return kind == MTGP_U32 && (mexp == 11213 || mexp == 23209 || mexp == 44497);
 }
 
-cudaError_t launch_gen4(uint32_t mexp, int kind, bool cksum, const GenArgs& a, cudaStream_t st) {
+cudaError_t launch_gen4(uint32_t mexp, int kind, int ck_mode, const GenArgs& a, cudaStream_t st) {
     if (a.n_teams == 0) return cudaSuccess;
     if (kind != MTGP_U32) return cudaErrorInvalidValue;
     switch (mexp) {
-        case 11213: return launch_gen4_11213(cksum, a, st);
-        case 23209: return launch_gen4_23209(cksum, a, st);
-        case 44497: return launch_gen4_44497(cksum, a, st);
+        case 11213: return launch_gen4_11213(ck_mode, a, st);
+        case 23209: return launch_gen4_23209(ck_mode, a, st);
+        case 44497: return launch_gen4_44497(ck_mode, a, st);
     }
     return cudaErrorInvalidValue;
 }
 
-int gen4_ctas_per_sm(uint32_t mexp, int kind, bool cksum) {
+int gen4_ctas_per_sm(uint32_t mexp, int kind, int ck_mode) {
     if (kind != MTGP_U32) return 0;
     switch (mexp) {
-        case 11213: return gen4_ctas_11213(cksum);
-        case 23209: return gen4_ctas_23209(cksum);
-        case 44497: return gen4_ctas_44497(cksum);
+        case 11213: return gen4_ctas_11213(ck_mode);
+        case 23209: return gen4_ctas_23209(ck_mode);
+        case 44497: return gen4_ctas_44497(ck_mode);
     }
     return 0;
 }

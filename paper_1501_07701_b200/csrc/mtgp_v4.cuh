@@ -19,9 +19,15 @@
 //
 // Requires N - pos >= 256 for every set (all cuRAND sets; synthetic sets are built that way).
 #pragma once
+
+#include <type_traits>
 #include "mtgp_v2.cuh"
 
 namespace mtgpb {
+
+// checksum accumulator of MTGP_OPT_CHECKSUM mode CKM (2: the word sum mod 2^32 in 32 bits)
+template <int CKM>
+using CkAcc4 = typename std::conditional<CKM == 2, uint32_t, unsigned long long>::type;
 
 // Steps per main-loop trip: 0 = K (the history shift is pure register renaming, but the code is
 // K times larger); otherwise the shift costs register moves (IMAD.MOV, FMA pipe) at the loop
@@ -109,10 +115,10 @@ __device__ __forceinline__ void fetch(uint32_t W[5], const uint4 (&Hs)[NH], uint
     }
 }
 
-template <uint32_t MEXP, int RC, int AC, int KIND, bool CK, bool TAIL>
+template <uint32_t MEXP, int RC, int AC, int KIND, int CKM, bool TAIL>
 __device__ __forceinline__ void step4(const V4Ctx& p, const uint4 (&Hs)[S4<MEXP>::H], uint4& n0, uint4& n1,
                                       uint32_t* optr, uint32_t n, uint32_t len, uint32_t* win_out,
-                                      unsigned long long& sum, uint32_t& xr) {
+                                      CkAcc4<CKM>& sum, uint32_t& xr) {
     using S = S4<MEXP>;
     uint32_t WA[2][5], WC[2][5];
     fetch<S::RA, S::AA, S::H>(WA[0], Hs, p.srcA0, p.srcA1, p.pA0, p.pA1);
@@ -131,11 +137,14 @@ __device__ __forceinline__ void step4(const V4Ctx& p, const uint4 (&Hs)[S4<MEXP>
         const uint32_t w0 = n + 128 * u + 4 * p.lane;  // piece word of o[0]
         if (!TAIL || w0 < len) {
             __stcs(reinterpret_cast<uint4*>(optr + w0), make_uint4(o[0], o[1], o[2], o[3]));
-            if (CK) {
+            if (CKM == 2) {
+                sum = sum + o[0] + o[1];  // 3-input IADD3s, mod 2^32 (MTGP_OPT_CHECKSUM 2)
+                sum = sum + o[2] + o[3];
+            } else if (CKM == 1) {
 #pragma unroll
                 for (int c = 0; c < 4; ++c) sum += o[c];
-                xr ^= o[0] ^ o[1] ^ o[2] ^ o[3];
             }
+            if (CKM) xr ^= o[0] ^ o[1] ^ o[2] ^ o[3];
         }
         if (TAIL && win_out) {
             // sequence index of r[c] is N + w0 + c; the end window is [len, len + N)
@@ -157,9 +166,9 @@ __device__ __forceinline__ void shift2(uint4 (&Hs)[NH], const uint4& n0, const u
     Hs[NH - 1] = n1;
 }
 
-template <uint32_t MEXP, int RC, int AC, int KIND, bool CK>
+template <uint32_t MEXP, int RC, int AC, int KIND, int CKM>
 __device__ __forceinline__ void run4(const V4Ctx& p, uint4 (&Hs)[S4<MEXP>::H], uint32_t* optr, uint32_t len,
-                                  uint32_t* win_out, unsigned long long& sum, uint32_t& xr) {
+                                  uint32_t* win_out, CkAcc4<CKM>& sum, uint32_t& xr) {
     using S = S4<MEXP>;
     const uint32_t steps = (len + kStepWords - 1) / kStepWords;
     // A step at n produces sequence words [N + n, N + n + 256): no store predicate and no end
@@ -170,42 +179,42 @@ __device__ __forceinline__ void run4(const V4Ctx& p, uint4 (&Hs)[S4<MEXP>::H], u
 #pragma unroll
         for (uint32_t k = 0; k < S::U; ++k) {
             uint4 n0, n1;
-            step4<MEXP, RC, AC, KIND, CK, false>(p, Hs, n0, n1, optr, (m + k) * kStepWords, len, nullptr, sum, xr);
+            step4<MEXP, RC, AC, KIND, CKM, false>(p, Hs, n0, n1, optr, (m + k) * kStepWords, len, nullptr, sum, xr);
             shift2(Hs, n0, n1);
         }
     }
     for (; m < steps; ++m) {
         uint4 n0, n1;
-        step4<MEXP, RC, AC, KIND, CK, true>(p, Hs, n0, n1, optr, m * kStepWords, len, win_out, sum, xr);
+        step4<MEXP, RC, AC, KIND, CKM, true>(p, Hs, n0, n1, optr, m * kStepWords, len, win_out, sum, xr);
         shift2(Hs, n0, n1);
     }
 }
 
-template <uint32_t MEXP, int AC, int KIND, bool CK>
+template <uint32_t MEXP, int AC, int KIND, int CKM>
 __device__ __forceinline__ void run_rc(int rc, const V4Ctx& p, uint4 (&Hs)[S4<MEXP>::H], uint32_t* optr, uint32_t len,
-                                       uint32_t* win_out, unsigned long long& sum, uint32_t& xr) {
+                                       uint32_t* win_out, CkAcc4<CKM>& sum, uint32_t& xr) {
     switch (rc) {
-        case 0: run4<MEXP, 0, AC, KIND, CK>(p, Hs, optr, len, win_out, sum, xr); break;
-        case 1: run4<MEXP, 1, AC, KIND, CK>(p, Hs, optr, len, win_out, sum, xr); break;
-        case 2: run4<MEXP, 2, AC, KIND, CK>(p, Hs, optr, len, win_out, sum, xr); break;
-        default: run4<MEXP, 3, AC, KIND, CK>(p, Hs, optr, len, win_out, sum, xr); break;
+        case 0: run4<MEXP, 0, AC, KIND, CKM>(p, Hs, optr, len, win_out, sum, xr); break;
+        case 1: run4<MEXP, 1, AC, KIND, CKM>(p, Hs, optr, len, win_out, sum, xr); break;
+        case 2: run4<MEXP, 2, AC, KIND, CKM>(p, Hs, optr, len, win_out, sum, xr); break;
+        default: run4<MEXP, 3, AC, KIND, CKM>(p, Hs, optr, len, win_out, sum, xr); break;
     }
 }
 
-template <uint32_t MEXP, int AC, int KIND, bool CK>
+template <uint32_t MEXP, int AC, int KIND, int CKM>
 __device__ __forceinline__ void run_ac(int ac, int rc, const V4Ctx& p, uint4 (&Hs)[S4<MEXP>::H], uint32_t* optr,
-                                       uint32_t len, uint32_t* win_out, unsigned long long& sum, uint32_t& xr) {
+                                       uint32_t len, uint32_t* win_out, CkAcc4<CKM>& sum, uint32_t& xr) {
     if constexpr (AC <= (int)S4<MEXP>::AC_MAX) {
         if (ac == AC)
-            run_rc<MEXP, AC, KIND, CK>(rc, p, Hs, optr, len, win_out, sum, xr);
+            run_rc<MEXP, AC, KIND, CKM>(rc, p, Hs, optr, len, win_out, sum, xr);
         else
-            run_ac<MEXP, AC + 1, KIND, CK>(ac, rc, p, Hs, optr, len, win_out, sum, xr);
+            run_ac<MEXP, AC + 1, KIND, CKM>(ac, rc, p, Hs, optr, len, win_out, sum, xr);
     }
 }
 
 }  // namespace
 
-template <uint32_t MEXP, int KIND, bool CK>
+template <uint32_t MEXP, int KIND, int CKM>
 __global__ void __launch_bounds__(S4<MEXP>::WARPS * 32, S4<MEXP>::MIN_CTAS * kWarpsPerCta / S4<MEXP>::WARPS)
     gen4_kernel(GenArgs a) {
     using S = S4<MEXP>;
@@ -257,17 +266,17 @@ __global__ void __launch_bounds__(S4<MEXP>::WARPS * 32, S4<MEXP>::MIN_CTAS * kWa
             win_out = a.win_out + (size_t)pc.set * S::N;
             for (uint32_t j = lane; j + len < S::N; j += 32) win_out[j] = w0[len + j];  // pieces shorter than N
         }
-        unsigned long long sum = 0;
+        CkAcc4<CKM> sum = 0;
         uint32_t xr = 0;
-        run_ac<MEXP, (int)S::AC_MIN, KIND, CK>(ac, rc, p, Hs, optr, len, win_out, sum, xr);
-        if (CK) {
+        run_ac<MEXP, (int)S::AC_MIN, KIND, CKM>(ac, rc, p, Hs, optr, len, win_out, sum, xr);
+        if (CKM) {
 #pragma unroll
             for (int s = 16; s > 0; s >>= 1) {
                 sum += __shfl_xor_sync(kFull4, sum, s);
                 xr ^= __shfl_xor_sync(kFull4, xr, s);
             }
             if (lane == 0) {
-                atomicAdd(&a.ck[pc.set].sum64, sum);
+                atomicAdd(&a.ck[pc.set].sum64, (unsigned long long)sum);
                 atomicXor(&a.ck[pc.set].xor32, xr);
                 atomicAdd(&a.ck[pc.set].words, (unsigned long long)len);
             }
@@ -276,29 +285,29 @@ __global__ void __launch_bounds__(S4<MEXP>::WARPS * 32, S4<MEXP>::MIN_CTAS * kWa
     }
 }
 
-template <uint32_t MEXP, int KIND, bool CK>
+template <uint32_t MEXP, int KIND, int CKM>
 static cudaError_t launch4_t(const GenArgs& a, cudaStream_t st) {
     constexpr uint32_t W = S4<MEXP>::WARPS;
     const uint32_t grid = (a.n_teams + W - 1) / W;
-    gen4_kernel<MEXP, KIND, CK><<<grid, W * 32, 0, st>>>(a);
+    gen4_kernel<MEXP, KIND, CKM><<<grid, W * 32, 0, st>>>(a);
     return cudaGetLastError();
 }
 
-template <uint32_t MEXP, int KIND, bool CK>
+template <uint32_t MEXP, int KIND, int CKM>
 static int occ4_t() {
     int n = 0;
     constexpr uint32_t W = S4<MEXP>::WARPS;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gen4_kernel<MEXP, KIND, CK>, W * 32, 0) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gen4_kernel<MEXP, KIND, CKM>, W * 32, 0) != cudaSuccess)
         return 0;
     return n * (int)(W / kWarpsPerCta);  // in the planner's unit: resident 4-warp teams groups
 }
 
 // Per-exponent entry points (one translation unit each: mtgp_v4_<mexp>.cu), u32 output only.
-cudaError_t launch_gen4_11213(bool cksum, const GenArgs& a, cudaStream_t st);
-cudaError_t launch_gen4_23209(bool cksum, const GenArgs& a, cudaStream_t st);
-cudaError_t launch_gen4_44497(bool cksum, const GenArgs& a, cudaStream_t st);
-int gen4_ctas_11213(bool cksum);
-int gen4_ctas_23209(bool cksum);
-int gen4_ctas_44497(bool cksum);
+cudaError_t launch_gen4_11213(int ck_mode, const GenArgs& a, cudaStream_t st);
+cudaError_t launch_gen4_23209(int ck_mode, const GenArgs& a, cudaStream_t st);
+cudaError_t launch_gen4_44497(int ck_mode, const GenArgs& a, cudaStream_t st);
+int gen4_ctas_11213(int ck_mode);
+int gen4_ctas_23209(int ck_mode);
+int gen4_ctas_44497(int ck_mode);
 
 }  // namespace mtgpb

@@ -3,10 +3,13 @@
 
 namespace mtgpb {
 
-cudaError_t launch_gen4_11213(bool cksum, const GenArgs& a, cudaStream_t st) {
-    return cksum ? launch4_t<11213, MTGP_U32, true>(a, st) : launch4_t<11213, MTGP_U32, false>(a, st);
+cudaError_t launch_gen4_11213(int ck_mode, const GenArgs& a, cudaStream_t st) {
+    return ck_mode == 2 ? launch4_t<11213, MTGP_U32, 2>(a, st)
+         : ck_mode == 1 ? launch4_t<11213, MTGP_U32, 1>(a, st) : launch4_t<11213, MTGP_U32, 0>(a, st);
 }
 
-int gen4_ctas_11213(bool cksum) { return cksum ? occ4_t<11213, MTGP_U32, true>() : occ4_t<11213, MTGP_U32, false>(); }
+int gen4_ctas_11213(int ck_mode) {
+    return ck_mode == 2 ? occ4_t<11213, MTGP_U32, 2>() : ck_mode == 1 ? occ4_t<11213, MTGP_U32, 1>() : occ4_t<11213, MTGP_U32, 0>();
+}
 
 }  // namespace mtgpb

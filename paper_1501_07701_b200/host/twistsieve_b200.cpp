@@ -591,6 +591,49 @@ std::uint32_t GpuWordSource::next_u32() {
     return buf_[cur_][pos_++];
 }
 
+MultiGpuBatch::MultiGpuBatch(const std::vector<MtgpStatus>& sets, const std::vector<std::uint32_t>& seeds,
+                             const std::vector<int>& devices, Gather gather) {
+    if (sets.size() != seeds.size()) throw std::invalid_argument("one seed per parameter set");
+    std::vector<mtgp_params> c;
+    c.reserve(sets.size());
+    for (const auto& s : sets) c.push_back(s.to_c());
+    check(mtgp_multi_create(&m_, devices.data(), static_cast<std::uint32_t>(devices.size()), c.data(),
+                            static_cast<std::uint32_t>(c.size()), seeds.data(), static_cast<int>(gather)),
+          "mtgp_multi_create");
+    int nccl = 0;
+    check(mtgp_multi_info(m_, &n_dev_, &nccl), "mtgp_multi_info");
+    nccl_ = nccl != 0;
+    n_sets_ = static_cast<std::uint32_t>(sets.size());
+}
+
+MultiGpuBatch::~MultiGpuBatch() {
+    if (m_) mtgp_multi_destroy(m_);
+}
+
+std::pair<std::uint32_t, std::uint32_t> MultiGpuBatch::range(std::uint32_t r) const {
+    mtgp_ctx* ctx = nullptr;
+    std::uint32_t f = 0, n = 0;
+    check(mtgp_multi_context(m_, r, &ctx, &f, &n), "mtgp_multi_context");
+    return {f, n};
+}
+
+mtgp_ctx* MultiGpuBatch::context(std::uint32_t r) {
+    mtgp_ctx* ctx = nullptr;
+    check(mtgp_multi_context(m_, r, &ctx, nullptr, nullptr), "mtgp_multi_context");
+    return ctx;
+}
+
+void MultiGpuBatch::generate_device(OutputKind kind, const std::vector<void*>& outs, std::uint64_t words_per_stream) {
+    if (outs.size() != n_dev_) throw std::invalid_argument("one output buffer per device");
+    check(mtgp_multi_generate(m_, static_cast<int>(kind), outs.data(), words_per_stream), "mtgp_multi_generate");
+}
+
+std::vector<mtgp_cksum> MultiGpuBatch::checksums() {
+    std::vector<mtgp_cksum> out(n_sets_);
+    check(mtgp_multi_checksums(m_, out.data()), "mtgp_multi_checksums");
+    return out;
+}
+
 std::unique_ptr<WordSource> make_word_source(const MtgpStatus& params, std::uint32_t seed) {
     return std::make_unique<GpuWordSource>(params, seed);
 }
@@ -598,5 +641,31 @@ std::unique_ptr<WordSource> make_word_source(const MtgpStatus& params, std::uint
 std::unique_ptr<WordSource> make_word_source(const MtStatus& params, std::uint32_t seed) {
     return std::make_unique<GpuWordSource>(params, seed);
 }
+
+#ifdef TWISTSIEVE_B200_WITH_REFERENCE
+MtStatus from_reference(const twistsieve::ParameterizedStatus& p) {
+    MtStatus s;
+    s.id = p.id;
+    s.mexp = p.mexp;
+    s.n = p.n;
+    s.m = p.m;
+    s.r = p.r;
+    s.a = p.a;
+    s.temper_b = p.temper_b;
+    s.temper_c = p.temper_c;
+    s.temper_u = p.temper_u;
+    s.temper_s = p.temper_s;
+    s.temper_t = p.temper_t;
+    s.temper_l = p.temper_l;
+    return s;
+}
+
+std::unique_ptr<twistsieve::WordSource> make_word_source(const twistsieve::ParameterizedStatus& params,
+                                                         std::uint32_t seed) {
+    if (params.engine != twistsieve::Engine::mt) return twistsieve::make_word_source(params, seed);
+    params.validate();  // the reference's own invariants and messages (proj/src/params.cpp:23-39)
+    return std::make_unique<GpuWordSource>(from_reference(params), seed);
+}
+#endif
 
 }  // namespace twistsieve_b200

@@ -38,6 +38,8 @@ EXPORTS = (
     "mtgp_poisson_sf", "mtgp_poisson_pmf", "mtgp_binomial_log_pmf", "mtgp_binomial_upper_tail",
     "mtgp_classify_pvalue", "mtgp_certify", "mtgp_mt_charpoly_digest", "mtgp_gf2_is_irreducible",
     "mtgp_host_alloc", "mtgp_host_free", "mtgp_generate_async",
+    "mtgp_shard_range", "mtgp_multi_create", "mtgp_multi_destroy", "mtgp_multi_info", "mtgp_multi_context",
+    "mtgp_multi_generate", "mtgp_multi_checksums",
 )
 
 
@@ -143,6 +145,15 @@ def load_library(path: Optional[str] = None) -> C.CDLL:
     lib.mtgp_certify.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
     lib.mtgp_mt_charpoly_digest.argtypes = [C.c_void_p, C.c_char_p]
     lib.mtgp_gf2_is_irreducible.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_int32)]
+    pu = C.POINTER(C.c_uint32)
+    lib.mtgp_shard_range.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, pu, pu]
+    lib.mtgp_multi_create.argtypes = [C.POINTER(C.c_void_p), C.POINTER(C.c_int), C.c_uint32, C.POINTER(MtgpParamsC),
+                                      C.c_uint32, pu, C.c_int]
+    lib.mtgp_multi_destroy.argtypes = [C.c_void_p]
+    lib.mtgp_multi_info.argtypes = [C.c_void_p, pu, C.POINTER(C.c_int)]
+    lib.mtgp_multi_context.argtypes = [C.c_void_p, C.c_uint32, C.POINTER(C.c_void_p), pu, pu]
+    lib.mtgp_multi_generate.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.c_uint64]
+    lib.mtgp_multi_checksums.argtypes = [C.c_void_p, C.POINTER(MtgpCksumC)]
     if path is None:
         _lib = lib
     return lib
@@ -172,6 +183,68 @@ def validate(p: MtgpParams) -> None:
     lib = load_library()
     arr = to_c_params([p])
     _check(lib, lib.mtgp_validate_params(arr))
+
+
+def shard_range(n_sets: int, world: int, rank: int):
+    """mtgp_shard_range: the contiguous balanced set-ID range of `rank`."""
+    lib = load_library()
+    f, c = C.c_uint32(), C.c_uint32()
+    _check(lib, lib.mtgp_shard_range(n_sets, world, rank, C.byref(f), C.byref(c)))
+    return range(f.value, f.value + c.value)
+
+
+class MultiGpu:
+    """mtgp_multi: n_sets streams split over `devices` (one context and host thread per device),
+    checksums all-gathered over NCCL (gather 0 auto / 1 NCCL / 2 host)."""
+
+    def __init__(self, sets: Sequence[MtgpParams], seeds: Sequence[int], devices: Sequence[int], gather: int = 0,
+                 lib: Optional[C.CDLL] = None):
+        self.lib = lib if lib is not None else load_library()
+        self.n_sets = len(sets)
+        self._params = to_c_params(sets)
+        self._seeds = (C.c_uint32 * len(seeds))(*[int(s) & 0xFFFFFFFF for s in seeds])
+        self._devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        _check(self.lib, self.lib.mtgp_multi_create(C.byref(h), self._devs, len(devices), self._params, self.n_sets,
+                                                    self._seeds, gather))
+        self.h = h
+        n, nccl = C.c_uint32(), C.c_int()
+        _check(self.lib, self.lib.mtgp_multi_info(self.h, C.byref(n), C.byref(nccl)))
+        self.n_devices, self.nccl = n.value, bool(nccl.value)
+
+    def ranges(self):
+        out = []
+        for r in range(self.n_devices):
+            ctx, f, c = C.c_void_p(), C.c_uint32(), C.c_uint32()
+            _check(self.lib, self.lib.mtgp_multi_context(self.h, r, C.byref(ctx), C.byref(f), C.byref(c)))
+            out.append(range(f.value, f.value + c.value))
+        return out
+
+    def generate_device(self, kind: int, ptrs: Sequence[int], words_per_stream: int) -> None:
+        arr = (C.c_void_p * len(ptrs))(*ptrs)
+        _check(self.lib, self.lib.mtgp_multi_generate(self.h, kind, arr, words_per_stream))
+
+    def checksums(self):
+        arr = (MtgpCksumC * self.n_sets)()
+        _check(self.lib, self.lib.mtgp_multi_checksums(self.h, arr))
+        return [(a.sum64, a.xor32, a.words) for a in arr]
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.mtgp_multi_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
 
 
 class MtgpContext:

@@ -29,3 +29,13 @@ def curand_golden():
 @pytest.fixture(scope="session")
 def mt_golden():
     return json.loads((GOLDEN / "mt_reference.json").read_text())
+
+
+@pytest.fixture(scope="session")
+def large_golden():
+    """cuRAND-driven known answers at MTGP32-23209 / -44497 (tests/golden/make_goldens.py)."""
+    from paper_1501_07701_b200 import tables
+    d = json.loads((GOLDEN / "mtgp32_large_curand.json").read_text())
+    for c in d["cases"]:
+        c["set"] = tables.MtgpParams(certified=False, **c["params"])
+    return d["cases"]

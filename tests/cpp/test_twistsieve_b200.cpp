@@ -14,6 +14,13 @@
 #include <string>
 #include <vector>
 
+#include <atomic>
+#include <chrono>
+#include <thread>
+
+#include <cuda_runtime.h>
+
+#include "oracle.h"
 #include "twistsieve_b200/mtgp.hpp"
 
 using namespace twistsieve_b200;
@@ -239,6 +246,101 @@ int main(int argc, char** argv) {
             const auto ck = batch.checksums();
             CHECK(ck[0].words == 1000);
         });
+        test_case("MultiGpuBatch: set ranges per device, checksums gathered == one context's", [&] {
+            std::vector<std::uint32_t> seeds(sets.size());
+            for (std::size_t i = 0; i < seeds.size(); ++i) seeds[i] = 1000 + static_cast<std::uint32_t>(i);
+            StreamBatch one(sets, seeds);
+            const std::uint64_t L = 1 << 16;
+            void* d = nullptr;
+            CHECK(mtgp_host_alloc(sets.size() * L * 4, &d) == MTGP_OK);  // host output for the reference batch
+            one.generate_host(OutputKind::u32, d, L);
+            const auto want = one.checksums();
+            mtgp_host_free(d);
+            for (auto mode : {MultiGpuBatch::Gather::nccl, MultiGpuBatch::Gather::host}) {
+                const std::vector<int> devs = mode == MultiGpuBatch::Gather::nccl ? std::vector<int>{0}
+                                                                                   : std::vector<int>{0, 0, 0};
+                MultiGpuBatch mb(sets, seeds, devs, mode);
+                CHECK(mb.nccl() == (mode == MultiGpuBatch::Gather::nccl));
+                std::vector<void*> outs;
+                for (std::uint32_t r = 0; r < mb.devices(); ++r) {
+                    void* o = nullptr;
+                    CHECK(cudaMalloc(&o, mb.range(r).second * L * 4) == cudaSuccess);
+                    outs.push_back(o);
+                }
+                mb.generate_device(OutputKind::u32, outs, L);
+                const auto got = mb.checksums();
+                CHECK(got.size() == want.size());
+                bool same = true;
+                for (std::size_t i = 0; i < got.size(); ++i)
+                    same &= got[i].sum64 == want[i].sum64 && got[i].xor32 == want[i].xor32 && got[i].words == L;
+                CHECK(same);
+                for (void* o : outs) cudaFree(o);
+            }
+        });
+
+        // The reference's concurrency model: one generator per worker thread, never shared
+        // (the std::thread pool of sieve.cpp:170-177). T host threads each own a
+        // make_word_source() stream on the same GPU -- half MTGP32 (certified sets), half
+        // Engine::mt (MT19937) -- and read it with the reference's 4096-word BufferedStream
+        // fills. Every word is then checked against the oracle (oracle/*.c, test infrastructure).
+        for (unsigned T : {8u, 16u}) {
+            const std::string name = "threading model: " + std::to_string(T) +
+                                     " host threads, one make_word_source() each, 4096-word fills";
+            test_case(name.c_str(), [&] {
+                const std::size_t W = std::size_t{1} << 24;
+                std::vector<std::vector<std::uint32_t>> got(T, std::vector<std::uint32_t>(W));
+                std::vector<std::unique_ptr<WordSource>> srcs(T);
+                for (unsigned t = 0; t < T; ++t)
+                    srcs[t] = (t % 2 == 0) ? make_word_source(sets[t], 100 + t) : make_word_source(mt19937_status(), 5489 + t);
+                std::atomic<int> errors{0};
+                const auto t0 = std::chrono::steady_clock::now();
+                std::vector<std::thread> pool;
+                for (unsigned t = 0; t < T; ++t)
+                    pool.emplace_back([&, t] {
+                        try {
+                            for (std::size_t i = 0; i < W; i += 4096)
+                                srcs[t]->fill(std::span<std::uint32_t>(got[t].data() + i, 4096));
+                        } catch (...) {
+                            ++errors;
+                        }
+                    });
+                for (auto& th : pool) th.join();
+                const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                CHECK(errors == 0);
+                std::atomic<int> bad{0};
+                std::vector<std::thread> check;
+                for (unsigned t = 0; t < T; ++t)
+                    check.emplace_back([&, t] {
+                        std::vector<std::uint32_t> ref(W);
+                        if (t % 2 == 0) {
+                            oracle_mtgp_params op{};
+                            op.mexp = sets[t].mexp;
+                            op.pos = sets[t].pos;
+                            op.sh1 = sets[t].sh1;
+                            op.sh2 = sets[t].sh2;
+                            op.mask = sets[t].mask;
+                            std::memcpy(op.tbl, sets[t].tbl, 64);
+                            std::memcpy(op.tmp_tbl, sets[t].tmp_tbl, 64);
+                            std::memcpy(op.flt_tmp_tbl, sets[t].flt_tmp_tbl, 64);
+                            auto g = std::make_unique<oracle_mtgp>();
+                            oracle_mtgp_init(g.get(), &op, 100 + t);
+                            oracle_mtgp_fill(g.get(), ref.data(), W, 0);
+                        } else {
+                            oracle_mt_params mp;
+                            oracle_mt19937_params(&mp);
+                            auto g = std::make_unique<oracle_mt>();
+                            oracle_mt_init(g.get(), &mp, 5489 + t);
+                            oracle_mt_fill(g.get(), ref.data(), W);
+                        }
+                        if (ref != got[t]) ++bad;
+                    });
+                for (auto& th : check) th.join();
+                CHECK(bad == 0);
+                std::printf("  THREADS %u: %zu words per thread in 4096-word fills, %.3f s wall, %.3f G words/s "
+                            "aggregate, every word == oracle: %s\n",
+                            T, W, secs, T * (double)W / secs / 1e9, bad == 0 ? "yes" : "NO");
+            });
+        }
     }
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail ? 1 : 0;

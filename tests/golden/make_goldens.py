@@ -2,7 +2,10 @@
 
 1. mtgp32_11213_curand.json -- oracle/_ref/curand_pin: cuRAND's MTGP32 headers compiled
    host-side (independent implementation of the same published algorithm).
-2. mt_reference.json -- the UNMODIFIED reference generator compiled from /root/reference
+2. mtgp32_large_curand.json -- oracle/_ref/curand_pin --large: cuRAND's own mtgp32_init_state,
+   para_rec, temper and temper_single driven at N = 726 / 1391 (MTGP32-23209 / -44497, which
+   cuRAND ships no tables for) over synthetic parameter sets chosen to cover every pos mod 4.
+3. mt_reference.json -- the UNMODIFIED reference generator compiled from /root/reference
    (oracle/_ref/libtwistsieve_ref.so): MT19937 seed 5489 words and checksums, temper goldens.
 
     make -C oracle && python tests/golden/make_goldens.py
@@ -25,6 +28,7 @@ def main():
     out = subprocess.run([str(ROOT / "oracle/_ref/curand_pin")], check=True, capture_output=True, text=True).stdout
     d = json.loads(out)
     (ROOT / "tests/golden/mtgp32_11213_curand.json").write_text(json.dumps(d, indent=1) + "\n")
+    large_goldens()
 
     ref = {}
     w = oracle_py.ref_fill(1 << 20, 5489)
@@ -52,6 +56,39 @@ def main():
     (ROOT / "tests/golden/mt_reference.json").write_text(json.dumps(ref, indent=1) + "\n")
     stat_goldens()
     print("goldens written")
+
+
+def large_pick(mexp):
+    """Synthetic sets covering every pos residue mod 4 (the register kernels' C-stream variants)
+    and the largest pos among the first 64 (the deepest C-stream history register)."""
+    from paper_1501_07701_b200 import tables
+    cand = tables.sets_for(mexp, 64)
+    pick = []
+    for r in range(4):
+        pick.append(next(i for i, p in enumerate(cand) if p.pos % 4 == r))
+    pick.append(max(range(64), key=lambda i: cand[i].pos))
+    return sorted(set(pick)), cand
+
+
+def large_goldens():
+    out = {"cases": []}
+    for mexp in (23209, 44497):
+        idx, cand = large_pick(mexp)
+        sets = [cand[i] for i in idx]
+        inp = "\n".join(" ".join(str(v) for v in [p.mexp, p.pos, p.sh1, p.sh2, p.mask, *p.tbl, *p.tmp_tbl,
+                                                     *p.flt_tmp_tbl]) for p in sets) + "\n"
+        r = subprocess.run([str(ROOT / "oracle/_ref/curand_pin"), "--large"], input=inp, check=True,
+                           capture_output=True, text=True).stdout
+        d = json.loads(r)
+        out["source"] = d["source"]
+        for c in d["cases"]:
+            p = sets[c["set"]]
+            c["synthetic_index"] = idx[c["set"]]
+            c["params"] = {"mexp": p.mexp, "pos": p.pos, "sh1": p.sh1, "sh2": p.sh2, "mask": p.mask,
+                           "tbl": list(p.tbl), "tmp_tbl": list(p.tmp_tbl), "flt_tmp_tbl": list(p.flt_tmp_tbl)}
+            del c["set"]
+            out["cases"].append(c)
+    (ROOT / "tests/golden/mtgp32_large_curand.json").write_text(json.dumps(out, indent=1) + "\n")
 
 
 STAT_CASES = [  # (spec fields, streams): small enough for the CPU suite

@@ -24,7 +24,10 @@ def _build(tmp_path, name, srcs, extra=()):
 def layer_exe(tmp_path_factory):
     d = tmp_path_factory.mktemp("cpp")
     return _build(d, "test_twistsieve_b200", [ROOT / "tests/cpp/test_twistsieve_b200.cpp"],
-                  ["-L", str(PKG), "-ltwistsieve_b200", "-lmtgp_b200", f"-Wl,-rpath,{PKG}"])
+                  ["-x", "c", str(ROOT / "oracle/mtgp32_oracle.c"), str(ROOT / "oracle/mt_oracle.c"), "-x", "none",
+                   "-I", "/usr/local/cuda/include", "-L", str(PKG), "-ltwistsieve_b200", "-lmtgp_b200",
+                   f"-Wl,-rpath,{PKG}", "-L", "/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath,/usr/local/cuda/lib64",
+                   "-lpthread"])
 
 
 def _pyfile(tmp_path):
@@ -47,6 +50,8 @@ def test_cpp_layer_gpu(layer_exe, tmp_path):
     r = subprocess.run([str(layer_exe), str(ROOT / "tests/golden/mtgp32_11213_curand.json"), "--gpu",
                         str(_pyfile(tmp_path))], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
+    # the threading-model cases report their aggregate rate (profiles/r2_threading.txt)
+    assert r.stdout.count("every word == oracle: yes") == 2, r.stdout
 
 
 def test_gf2_jump_algebra(tmp_path):

@@ -92,3 +92,23 @@ def test_c5_every_rank_of_every_world(torch_cuda, world):
     for rank in range(world):
         r = shard.status_range(1024, rank, world)
         _run(torch_cuda, "c5", r.start, len(r), 25)
+
+
+@pytest.mark.parametrize("devices,gather", [([0], 1), ([0, 0, 0], 2)])
+def test_multi_gpu_batch_c5(torch_cuda, devices, gather):
+    """The single-process multi-GPU batch (C-ABI mtgp_multi: one context + host thread per
+    device, contiguous set ranges, checksum all-gather over NCCL) on config 5's 1024 sets,
+    every word checked through the gathered checksums. gpurun exposes one GPU: one rank with a
+    real (single-rank) NCCL communicator, and three ranks sharing device 0 with the host gather."""
+    sets = tables.sets_for(11213, 1024)
+    with mtgp.MultiGpu(sets, [1] * 1024, devices, gather=gather) as m:
+        assert m.nccl == (gather == 1) and m.n_devices == len(devices)
+        rs = m.ranges()
+        assert [r.start for r in rs] == [shard.status_range(1024, i, len(devices)).start for i in range(len(devices))]
+        bufs = [torch_cuda.empty((len(r), 1 << 24), dtype=torch_cuda.int32, device=f"cuda:{d}")
+                for r, d in zip(rs, devices)]
+        for k in range(3):
+            m.generate_device(mtgp.U32, [b.data_ptr() for b in bufs], 1 << 24)
+            r = full_ck.compare("c5", 0, m.checksums())
+            assert r["ok"] and r["words_per_stream"] == (k + 1) << 24, r
+        del bufs

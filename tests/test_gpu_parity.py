@@ -391,3 +391,35 @@ def test_async_host_generation_into_pinned_buffers(curand_sets):
                 lib.mtgp_host_free(p)
     ref, _ = oracle_py.mtgp_bulk(sets, [3, 4], 2 * L, threads=2)
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("mexp", [23209, 44497])
+@pytest.mark.parametrize("kernel", [0, 1, 2, 4])
+def test_large_mexp_pinned_by_curand(large_golden, mexp, kernel):
+    """23209 / 44497 against cuRAND's own init / para_rec / temper run at N = 726 / 1391
+    (tests/golden/mtgp32_large_curand.json), not only against the builder's restatement:
+    every kernel that takes the shape (0 auto = v4, 1 CTA per stream, 2 shared ring, 4 v4),
+    2^20 words per stream as 2^19 + 2^19 so the second call starts from jumped pieces."""
+    cases = [c for c in large_golden if c["mexp"] == mexp]
+    sets, seeds = [c["set"] for c in cases], [c["seed"] for c in cases]
+    with _ctx(sets, seeds, kernel, {mtgp.OPT_MIN_PIECE_WORDS: 1 << 15}) as ctx:
+        w = np.concatenate([ctx.fill_u32(1 << 19), ctx.fill_u32(1 << 19)], axis=1)
+        ck = ctx.checksums()
+        pieces = ctx.last_plan()[0]
+    if kernel != 1:
+        assert pieces > len(cases)  # the second call ran jumped pieces
+    for i, c in enumerate(cases):
+        assert w[i, :32].tolist() == c["u32"], (c["synthetic_index"], c["seed"])
+        assert (int(w[i].astype(np.uint64).sum()), int(np.bitwise_xor.reduce(w[i])), int(w[i, -1])) == (
+            c["sum64"], c["xor32"], c["last"])
+        assert ck[i] == (c["sum64"], c["xor32"], c["n"])
+
+
+@pytest.mark.parametrize("mexp", [23209, 44497])
+def test_large_mexp_single_float_pinned_by_curand(large_golden, mexp):
+    """[1,2) floats through cuRAND's temper_single (flt_tmp_tbl) at 23209 / 44497."""
+    cases = [c for c in large_golden if c["mexp"] == mexp]
+    with _ctx([c["set"] for c in cases], [c["seed"] for c in cases], 0) as ctx:
+        f = ctx.generate_host(mtgp.F32_12, 32)
+    for i, c in enumerate(cases):
+        assert f[i].tolist() == c["single12_bits"]

@@ -181,3 +181,39 @@ def test_gloo_strong_split_uneven_gather():
     for gid, (p, ck) in enumerate(zip(every, allck)):
         w = oracle_py.MtgpOracle(p, 1).fill(L)
         assert ck == (int(w.astype("uint64").sum()), int(np.bitwise_xor.reduce(w)), L), gid
+
+
+# ---- the single-process multi-GPU batch (C-ABI mtgp_multi, csrc/mtgp_multi.h host logic) ----
+
+def test_multi_host_logic_fake_communicator(tmp_path):
+    """Partition + padded all-gather through a fake ring communicator (tests/cpp/test_multi.cpp)."""
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    exe = tmp_path / "test_multi"
+    subprocess.run(["g++", "-std=c++17", "-O2", "-I", str(root / "include"), "-I",
+                    str(root / "paper_1501_07701_b200/csrc"), str(root / "tests/cpp/test_multi.cpp"), "-o", str(exe)],
+                   check=True, capture_output=True, text=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "ALL OK" in r.stdout, r.stdout + r.stderr
+
+
+def test_shard_range_c_abi_matches_python_split():
+    """mtgp_shard_range (the C-ABI's split) == shard.status_range (bench.py's), and the C-ABI
+    refuses bad arguments; no device needed."""
+    from paper_1501_07701_b200 import mtgp, shard
+    for n in (1, 5, 200, 1024, 1601):
+        for w in range(1, 9):
+            for r in range(w):
+                assert mtgp.shard_range(n, w, r) == shard.status_range(n, r, w)
+    with pytest.raises(mtgp.MtgpInvalidArgument):
+        mtgp.shard_range(10, 2, 2)
+
+
+def test_multi_create_fails_loudly_without_device():
+    import torch
+    from paper_1501_07701_b200 import mtgp, tables
+    if torch.cuda.is_available():
+        pytest.skip("CPU hosts only")
+    with pytest.raises(mtgp.MtgpError):
+        mtgp.MultiGpu(tables.load_curand_11213()[:4], [1] * 4, [0, 1])

@@ -245,3 +245,20 @@ def test_full_ck_compare_reports_mismatch():
     assert fc.compare("c2", 0, hi, sum_mod32=True)["ok"] is True and fc.compare("c2", 0, hi)["ok"] is False
     assert fc.compare("c2", 0, [(0, 0, 3 << 27)] * 2)["ok"] is False
     assert fc.compare("c2", 0, [(0, 0, 99 << 27)] * 2)["ok"] is None
+
+
+def test_large_exponents_pinned_by_curand(large_golden):
+    """MTGP32-23209 / -44497: the restatement equals cuRAND's own init_state / para_rec /
+    temper / temper_single run at N = 726 / 1391 (oracle/curand_pin.cpp --large) -- the
+    independent pin these exponents had no other source for."""
+    assert {c["mexp"] for c in large_golden} == {23209, 44497}
+    for c in large_golden:
+        g = oracle_py.MtgpOracle(c["set"], c["seed"])
+        w0 = g.window()
+        assert [int(w0[0]), int(w0[1]), int(w0[-1])] == c["init_x0_x1_last"]
+        w = g.fill(c["n"])
+        assert w[:32].tolist() == c["u32"]
+        assert (int(w.astype(np.uint64).sum()), int(np.bitwise_xor.reduce(w)), int(w[-1])) == (
+            c["sum64"], c["xor32"], c["last"])
+        f = oracle_py.MtgpOracle(c["set"], c["seed"]).fill(32, kind=1)
+        assert f.tolist() == c["single12_bits"]
