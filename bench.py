@@ -22,6 +22,7 @@ MT19937 through make_word_source()/WordSource::fill) is timed beside it as a sid
 the arm itself for --config mt19937.
 """
 import argparse
+import ctypes as C
 import json
 import os
 import subprocess
@@ -70,10 +71,13 @@ def parse():
                     help="MTGP_OPT_CHECKSUM: 1 sum64 + xor32, 2 sum32 + xor32 (the fixture's sums mod 2^32)")
     ap.add_argument("--min-piece-words", type=int, default=None, help="MTGP_OPT_MIN_PIECE_WORDS (default: library's)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=1, help="end-to-end (host output) steps timed")
+    ap.add_argument("--e2e-words-per-call", type=int, default=1 << 22,
+                    help="words per stream per mtgp_generate call in the e2e leg (reused pinned buffer)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-words-per-thread", type=int, default=1 << 28,
                     help="MT19937 reference (oracle/_ref): words per thread per step")
-    ap.add_argument("--cpu-words-per-stream", type=int, default=1 << 22,
+    ap.add_argument("--cpu-words-per-stream", type=int, default=1 << 26,
                     help="MTGP32 CPU port: words of every stream per step (a bounded sample of the step)")
     ap.add_argument("--as-rank", type=int, default=None,
                     help="single process: generate rank R's shard of a multi-GPU run (its parameter sets / seeds), "
@@ -212,12 +216,18 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def traffic_per_launch(algo_bytes: float):
-    """DRAM read+write bytes of one generation launch, scaled from the committed ncu capture."""
-    f = ROOT / "profiles" / "gen_traffic.json"
+def traffic_per_launch(algo_bytes: float, kver: int, mexp: int):
+    """DRAM read+write bytes of one launch of the timed generation kernel, scaled from that
+    kernel's committed ncu --set full capture (profiles/traffic.json); (None, None) when the
+    kernel has no capture."""
+    f = ROOT / "profiles" / "traffic.json"
     if not f.exists():
-        return None
-    return round(json.loads(f.read_text())["traffic_over_algorithmic"] * algo_bytes)
+        return None, None
+    ks = json.loads(f.read_text())["kernels"]
+    k = ks.get(f"{kver}:{mexp}") or ks.get(str(kver))
+    if k is None:
+        return None, None
+    return round(k["traffic_over_algorithmic"] * algo_bytes), f"{k['source']} ({k['kernel']})"
 
 
 def full_ck():
@@ -501,32 +511,49 @@ def main():
 
     e2e = None
     if not args.no_e2e:
-        # public API, HOST buffers: mtgp_generate(out_is_device=0) into pinned memory; the timed
-        # region contains generation plus the device->host copy of every word. Every rank runs it
-        # at once (each GPU has its own host link); whole-job samples over the slowest rank's time.
-        Le = 1 << 20
+        # public API, HOST buffers, the whole step's volume: a fresh context (mtgp_ctx_create:
+        # parameter table + seeds uploaded, timed separately as the one-off setup), then every
+        # step = L_step words of every stream through mtgp_generate(out_is_device=0) into a
+        # reused page-locked buffer of Le words per stream (the reference's WordSource::fill
+        # pattern), so each timed step holds generation plus the device->host copy of all
+        # S * L_step words. Every rank runs it at once (each GPU has its own host link);
+        # whole-job samples over the slowest rank's time.
+        Le = min(L_step, args.e2e_words_per_call)
         host = torch.empty((S, Le), dtype=torch.int32, pin_memory=True)
         hv = host.numpy().view(np.uint32)
-        ectx = make_ctx(sets, seeds)
-        ectx.set_option(mtgp.OPT_HOST_CHUNK, 1 << 18)
-        ectx.generate_host(kind, Le, out=hv)
-        reps = 5
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        for _ in range(reps):
-            ectx.generate_host(kind, Le, out=hv)
+        ectx = make_ctx(sets, seeds)
+        setup_s = time.perf_counter() - t0
+        ectx.set_option(mtgp.OPT_HOST_CHUNK, 1 << 18)
+        ectx.generate_host(kind, Le, out=hv)  # warm: plan + staging buffers
+        calls_e = L_step // Le
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            for _ in range(calls_e):
+                ectx.generate_host(kind, Le, out=hv)
         el = time.perf_counter() - t0
         ectx.close()
         if world > 1:
-            tt = torch.tensor([el], device=f"cuda:{local}", dtype=torch.float64)
+            tt = torch.tensor([el, setup_s], device=f"cuda:{local}", dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            el = float(tt.item())
-        e2e = {"value": round(world * S * Le * reps / el / 1e9, 4), "unit": "Gsamples/s",
-               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": world * S * Le * 4,
-               "how": f"mtgp_generate(out_is_device=0) of {Le} words x {S} streams into pinned host memory, "
-                      f"{reps} calls on each of {world} GPU(s) at once, max wall clock over ranks"}
+            el, setup_s = float(tt[0].item()), float(tt[1].item())
+        setup_bytes = S * C.sizeof(mtgp.MtParamsC if is_mt else mtgp.MtgpParamsC) + S * 4
+        e2e = {"value": round(world * S * L_step * args.e2e_steps / el / 1e9, 4), "unit": "Gsamples/s",
+               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": world * S * L_step * 4,
+               "steps": args.e2e_steps, "ms_per_step": round(1000 * el / args.e2e_steps, 1),
+               "setup": {"ms": round(1000 * setup_s, 2), "h2d_bytes": world * setup_bytes,
+                         "what": "mtgp_ctx_create: parameter table + seeds uploaded, state windows seeded "
+                                 "(one-off per context, outside the timed steps)"},
+               "how": f"mtgp_generate(out_is_device=0): each step = {calls_e} calls x {Le} words x {S} streams "
+                      f"into one reused page-locked buffer ({S * Le * 4 / 1e9:.2f} GB), the step's full volume "
+                      f"({S * L_step * 4 / 1e9:.1f} GB) copied device->host; {world} GPU(s) at once, max wall "
+                      "clock over ranks. No per-step inputs: the only host->device bytes are the setup's"}
 
+    traffic = traffic_per_launch(bytes_per_launch, kver, mexp)
     if rank == 0:
         line = {
             "metric": "Gsamples/s (uint32 & float) per GPU and at 1/2/4/8 B200; % of HBM write peak",
@@ -554,8 +581,8 @@ def main():
                                           else "rank 0: cuRAND MTGP32-11213 (certified); ranks 1..N-1: synthetic "
                                                "MTGP32-11213 (uncertified period)")},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                         "frac": round(achieved / hbm, 4), "traffic": traffic_per_launch(bytes_per_launch),
-                         "traffic_source": "profiles/gen_traffic.json (ncu dram__bytes_read+write per algorithmic byte)",
+                         "frac": round(achieved / hbm, 4), "traffic": traffic[0],
+                         "traffic_source": traffic[1],
                          "peak_source": hbm_src,
                          "kernel": {5: "mt_gen2_kernel (v5, Engine::mt warp teams, shared-memory rings)",
                                     6: "mt_gen3_kernel (v6, Engine::mt register-resident warp teams)"}.get(

@@ -496,9 +496,21 @@ int mtgp_skip(mtgp_ctx* ctx, uint64_t words) {
     if (words < 4096 || !ctx->planner || !ctx->planner->v2_supported()) {
         // Short skips (and shapes without a planner: mixed Engine::mt statuses): generate into a
         // scratch buffer in chunks; generating is cheaper than a jump for short distances.
+        // The scratch is context-owned and reused: its contents are never read, and every write
+        // to it is ordered on the context stream, so no synchronisation is needed between skips.
         const uint64_t chunk = std::min<uint64_t>(words, 1ull << 20);
-        void* scratch = nullptr;
-        CK(cudaMalloc(&scratch, (size_t)chunk * ctx->n_sets * 4), "cudaMalloc skip scratch");
+        const size_t need = (size_t)chunk * ctx->n_sets * 4;
+        if (ctx->skip_bytes < need) {
+            if (ctx->d_skip) {
+                cudaStreamSynchronize(ctx->stream);
+                cudaFree(ctx->d_skip);
+                ctx->d_skip = nullptr;
+                ctx->skip_bytes = 0;
+            }
+            CK(cudaMalloc(&ctx->d_skip, need), "cudaMalloc skip scratch");
+            ctx->skip_bytes = need;
+        }
+        void* scratch = ctx->d_skip;
         const bool ck = ctx->cksum;
         const int kern = ctx->kernel;
         ctx->cksum = false;
@@ -508,8 +520,6 @@ int mtgp_skip(mtgp_ctx* ctx, uint64_t words) {
             rc = generate_device(ctx, MTGP_U32, scratch, std::min<uint64_t>(chunk, words - done));
         ctx->cksum = ck;
         ctx->kernel = kern;
-        cudaStreamSynchronize(ctx->stream);
-        cudaFree(scratch);
         return rc;
     }
     std::string err;

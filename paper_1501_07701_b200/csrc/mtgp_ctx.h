@@ -51,6 +51,9 @@ struct mtgp_ctx {
     // host-output staging
     void* d_stage = nullptr;
     size_t stage_bytes = 0;
+    // short-skip scratch (mtgp_skip below 4096 words): kept across calls, grown on demand
+    void* d_skip = nullptr;
+    size_t skip_bytes = 0;
     // stat-test scratch (slot 0: saved window, slot 1: chunk + counters), kept across
     // mtgp_stat_run calls, grown on demand, freed with the context
     void* d_scratch[2] = {nullptr, nullptr};
@@ -78,7 +81,7 @@ struct mtgp_ctx {
         if (stream) cudaStreamSynchronize(stream);
         if (copy_stream) cudaStreamSynchronize(copy_stream);
         planner.reset();
-        for (void* p : {(void*)d_params, (void*)d_mt, (void*)d_win, (void*)d_ck, d_stage, d_scratch[0], d_scratch[1]})
+        for (void* p : {(void*)d_params, (void*)d_mt, (void*)d_win, (void*)d_ck, d_stage, d_skip, d_scratch[0], d_scratch[1]})
             if (p) cudaFree(p);
         for (int i = 0; i < 2; ++i) {
             if (ev_gen[i]) cudaEventDestroy(ev_gen[i]);

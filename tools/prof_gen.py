@@ -21,11 +21,12 @@ ap.add_argument("--words", type=int, default=1 << 24)
 ap.add_argument("--calls", type=int, default=3)
 ap.add_argument("--kernel", type=int, default=0)
 ap.add_argument("--no-checksum", action="store_true")
+ap.add_argument("--ck", type=int, default=2, help="MTGP_OPT_CHECKSUM mode (bench default 2)")
 a = ap.parse_args()
 sets = tables.sets_for(a.mexp, a.sets)
 ctx = mtgp.MtgpContext(sets, [1] * a.sets)
 ctx.set_option(mtgp.OPT_KERNEL, a.kernel)
-ctx.set_option(mtgp.OPT_CHECKSUM, 0 if a.no_checksum else 1)
+ctx.set_option(mtgp.OPT_CHECKSUM, 0 if a.no_checksum else a.ck)
 out = torch.empty((a.sets, a.words), dtype=torch.int32, device="cuda")
 for _ in range(a.calls):
     ctx.generate_device(a.kind, out.data_ptr(), a.words)
