@@ -79,6 +79,10 @@ def parse():
                     help="MT19937 reference (oracle/_ref): words per thread per step")
     ap.add_argument("--cpu-words-per-stream", type=int, default=1 << 26,
                     help="MTGP32 CPU port: words of every stream per step (a bounded sample of the step)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="collectives backend under torchrun (nccl; gloo only for --share-device smoke runs)")
+    ap.add_argument("--share-device", action="store_true",
+                    help="map every rank onto the visible GPUs modulo their count (multi-rank smoke run on one GPU)")
     ap.add_argument("--as-rank", type=int, default=None,
                     help="single process: generate rank R's shard of a multi-GPU run (its parameter sets / seeds), "
                          "to time every rank's workload alone on one GPU")
@@ -333,9 +337,19 @@ def main():
     import torch.distributed as dist
     from paper_1501_07701_b200 import mtgp, shard, tables
 
+    # one process per GPU: LOCAL_RANK is the device. --dist-backend gloo (collectives on host
+    # tensors) with --share-device lets a 2-rank smoke run of this multi-rank path on a 1-GPU
+    # box; it is never a scaling measurement (the ranks share one GPU).
+    if args.share_device:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
+    coll_dev = f"cuda:{local}" if args.dist_backend == "nccl" else "cpu"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # nranks / transport lines on stderr
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     mexp, kind, L_step, label = CONFIGS[args.config]
     S = args.sets
     shard_rank, shard_world = rank, world
@@ -395,7 +409,7 @@ def main():
     parity_first = None
     for w in range(args.warmup):
         step()
-        if w == 0 and ck_mode and not is_mt:
+        if w == 0 and ck_mode:
             ctx.sync()
             parity_first = full_ck().compare(args.config, first_set, ctx.checksums(), sum_mod32=ck_mode == 2)
     ctx.sync()
@@ -450,31 +464,32 @@ def main():
     write_peak = out.numel() * 4 / (wp_ms / 1e3) / 1e9
 
     if world > 1:
-        t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
+        t = torch.tensor([ms], device=coll_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         # clocks of the whole job: slowest rank's median / minimum SM clock, union of reasons
         names = [n for n, _ in ClockSampler.REASONS]
         lo = torch.tensor([clk.get("sm_mhz") or 0.0, clk.get("sm_mhz_min") or clk.get("sm_mhz") or 0.0],
-                          device=f"cuda:{local}", dtype=torch.float64)
+                          device=coll_dev, dtype=torch.float64)
         dist.all_reduce(lo, op=dist.ReduceOp.MIN)
-        bits = torch.tensor([float(n in clk.get("reasons", [])) for n in names], device=f"cuda:{local}",
+        bits = torch.tensor([float(n in clk.get("reasons", [])) for n in names], device=coll_dev,
                             dtype=torch.float64)
         dist.all_reduce(bits, op=dist.ReduceOp.MAX)
         clk = dict(clk, sm_mhz=float(lo[0].item()), sm_mhz_min=float(lo[1].item()),
                    reasons=[n for n, b in zip(names, bits.tolist()) if b > 0], ranks=world,
                    note="min over ranks of each rank's median / min SM clock; union of reasons")
     # per-stream checksum gather (NCCL all_gather; the only inter-GPU traffic)
-    allck = shard.gather_checksums(ctx.checksums(), device=f"cuda:{local}")
+    allck = shard.gather_checksums(ctx.checksums(), device=coll_dev)
     gathered_streams = len(allck)
     # full-volume parity, part 2: every word of every stream generated in this run (warm-up and
     # timed steps) through the gathered checksums, against the oracle's cumulative checksums
     parity = None
-    if rank == 0 and ck_mode and not is_mt:
+    if rank == 0 and ck_mode:
         gfirst = first_set if (world == 1 or args.as_rank is not None) else 0
         parity = full_ck().compare(args.config, gfirst, allck, sum_mod32=ck_mode == 2)
         parity["after_first_step"] = parity_first
-        parity["fixture"] = "tests/golden/full_ck.npz (oracle/mtgp32_oracle.c cumulative checksums)"
+        parity["fixture"] = ("tests/golden/mt_full_ck.npz (the reference's own MtWordSource::fill, oracle/_ref)"
+                             if is_mt else "tests/golden/full_ck.npz (oracle/mtgp32_oracle.c cumulative checksums)")
 
     samples_rank = S * L_step * args.steps
     # whole job: every rank's samples (c5: the 1024 sets, however they are split)
@@ -538,7 +553,7 @@ def main():
         el = time.perf_counter() - t0
         ectx.close()
         if world > 1:
-            tt = torch.tensor([el, setup_s], device=f"cuda:{local}", dtype=torch.float64)
+            tt = torch.tensor([el, setup_s], device=coll_dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             el, setup_s = float(tt[0].item()), float(tt[1].item())
         setup_bytes = S * C.sizeof(mtgp.MtParamsC if is_mt else mtgp.MtgpParamsC) + S * 4
@@ -570,6 +585,12 @@ def main():
                        "global_set_ids": ([set_range.start, set_range.stop] if is_c5
                                           else [shard_rank * S, (shard_rank + 1) * S]),
                        "checksums_gathered_streams": gathered_streams,
+                       "collectives": {"backend": args.dist_backend if world > 1 else None, "world": world,
+                                       "hot_path": "none (disjoint set-ID shards)",
+                                       "after_timing": "per-stream checksum all_gather",
+                                       **({"share_device": True, "note": "ranks share one GPU: a smoke run of "
+                                           "the multi-rank path, not a scaling measurement"}
+                                          if args.share_device and world > 1 else {})},
                        "l2": "output 4*S*L/calls bytes per call >> 126 MB L2; no flush needed",
                        "parameter_sets": ("MT19937 (mt19937_params, proj/src/params.cpp:63-77)" if is_mt
                                           else f"global set IDs {set_range.start}..{set_range.stop - 1}: IDs < 200 "

@@ -209,6 +209,8 @@ def ref_lib() -> C.CDLL:
         L.ref_validate.argtypes = [C.c_void_p]
         L.ref_bulk_throughput.argtypes = [C.c_int, C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64)]
         L.ref_bulk_throughput.restype = C.c_double
+        L.ref_cksum_stream.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p, C.c_int]
+        L.ref_cksum_stream.restype = C.c_double
         _ref = L
     return _ref
 
@@ -228,3 +230,15 @@ def ref_bulk_throughput(threads: int, words_per_thread: int, fill_words: int = 1
     x = C.c_uint64()
     secs = ref_lib().ref_bulk_throughput(threads, words_per_thread, fill_words, seed0, C.byref(x))
     return secs, x.value
+
+
+def ref_cksum_stream(seed0: int, n_streams: int, rec_every: int, n_rec: int, threads: int = 8):
+    """Cumulative (sum64, xor32) of MT19937 streams seed0 + s through the reference's own
+    make_word_source + fill (oracle/_ref); arrays [n_streams, n_rec], seconds."""
+    sums = np.zeros((n_streams, n_rec), dtype=np.uint64)
+    xors = np.zeros((n_streams, n_rec), dtype=np.uint32)
+    secs = ref_lib().ref_cksum_stream(seed0, n_streams, rec_every, n_rec, sums.ctypes.data_as(C.c_void_p),
+                                      xors.ctypes.data_as(C.c_void_p), threads)
+    if secs < 0:
+        raise ValueError("rec_every must be a multiple of 2^18")
+    return sums, xors, secs

@@ -114,3 +114,48 @@ double ref_bulk_throughput(int threads, uint64_t words_per_thread, uint32_t fill
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// Full-volume parity fixture for Engine::mt (tests/golden/make_mt_full_ck.py): MT19937 streams
+// seeds seed0 + s, s < n_streams, each produced through the reference's own make_word_source +
+// fill() in 2^18-word calls; after every rec_every words (a multiple of 2^18) the cumulative
+// sum64 (mod 2^64) and xor32 of the stream's words so far are recorded:
+// sums/xors[s * n_rec + k] cover words [0, (k + 1) * rec_every). Threads take whole streams.
+// Returns wall seconds, or -1 if rec_every is not a multiple of the fill size.
+double ref_cksum_stream(uint32_t seed0, uint32_t n_streams, uint64_t rec_every, uint32_t n_rec, uint64_t* sums,
+                        uint32_t* xors, int threads) {
+    constexpr uint64_t kFill = 1u << 18;
+    if (rec_every % kFill) return -1.0;
+    if (threads < 1) threads = 1;
+    std::atomic<uint32_t> next{0};
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) {
+        pool.emplace_back([&] {
+            std::vector<uint32_t> buf(kFill);
+            for (;;) {
+                const uint32_t s = next.fetch_add(1);
+                if (s >= n_streams) break;
+                auto src = make_word_source(mt19937_params(), seed0 + s);
+                uint64_t sum = 0;
+                uint32_t x = 0;
+                for (uint32_t k = 0; k < n_rec; ++k) {
+                    for (uint64_t done = 0; done < rec_every; done += kFill) {
+                        src->fill(std::span<std::uint32_t>(buf.data(), buf.size()));
+                        for (uint32_t w : buf) {
+                            sum += w;
+                            x ^= w;
+                        }
+                    }
+                    sums[(size_t)s * n_rec + k] = sum;
+                    xors[(size_t)s * n_rec + k] = x;
+                }
+            }
+        });
+    }
+    for (auto& th : pool) th.join();
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // extern "C"

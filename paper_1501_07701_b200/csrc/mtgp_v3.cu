@@ -38,6 +38,12 @@ constexpr int kMinCtas3 = 6;
 #ifndef MTGP3_LERP
 #define MTGP3_LERP 0
 #endif
+// Operand select as one LOP3 with a per-lane all-ones / all-zeros mask register instead of
+// SEL on a predicate (bit 0: A stream, bit 1: C stream): the same ALU op count, but the four
+// lane predicates no longer have to be rematerialised by ISETPs on every trip.
+#ifndef MTGP3_MASKSEL
+#define MTGP3_MASKSEL 0
+#endif
 
 namespace {
 
@@ -55,6 +61,7 @@ struct V3Ctx {
     uint32_t srcA0, srcA1, srcC0, srcC1;  // source lanes for carry e = 0 / 1
     bool pA0, pA1, pC0, pC1;              // "take the newer half-step" predicates
     uint32_t mA0, mA1, mC0, mC1;          // the same as 0/1 multipliers (MTGP3_LERP)
+    uint32_t kA0, kA1, kC0, kC1;          // ... and as 0 / ~0 masks (MTGP3_MASKSEL)
     uint32_t neg1;                        // 0xFFFFFFFF, opaque to the compiler
     // bitmap kinds: this stream's bitmap, the piece's first word within the call, the predicate
     uint32_t* bm;
@@ -94,9 +101,10 @@ __device__ __forceinline__ uint32_t conv3(uint32_t o) {
 // Five consecutive operand words for half-step U from the history half-steps
 // h1 = (k=1), h2 = (k=2), h3 = (k=3); residue R; per-carry source lanes / predicates.
 // LERP: the select is lo + m * d with d = hi - lo (dU: the differences of this half-step pair).
-template <int R, int U, bool LERP>
+template <int R, int U, bool LERP, bool MSEL>
 __device__ __forceinline__ void fetch5(uint32_t W[5], const uint4& h1, const uint4& h2, const uint4& h3, const uint4& dU,
-                                       uint32_t src0, uint32_t src1, bool p0, bool p1, uint32_t m0, uint32_t m1) {
+                                       uint32_t src0, uint32_t src1, bool p0, bool p1, uint32_t m0, uint32_t m1,
+                                       uint32_t k0, uint32_t k1) {
 #pragma unroll
     for (int j = 0; j < 5; ++j) {
         const int c = (R + j) & 3;
@@ -106,6 +114,8 @@ __device__ __forceinline__ void fetch5(uint32_t W[5], const uint4& h1, const uin
         uint32_t send;
         if (LERP)
             asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(send) : "r"(comp4(dU, c)), "r"(e ? m1 : m0), "r"(comp4(lo, c)));
+        else if (MSEL)  // (hi & k) | (lo & ~k)
+            asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(send) : "r"(comp4(hi, c)), "r"(comp4(lo, c)), "r"(e ? k1 : k0));
         else
             send = (e ? p1 : p0) ? comp4(hi, c) : comp4(lo, c);
         W[j] = __shfl_sync(FULL, send, e ? src1 : src0);
@@ -137,10 +147,13 @@ __device__ __forceinline__ void step3(const V3Ctx& p, const uint4& h1, const uin
         d0 = diff4(h2, h1, p.neg1);
         d1 = diff4(h3, h2, p.neg1);
     }
-    fetch5<1, 0, kLerpA>(WA[0], h1, h2, h3, d0, p.srcA0, p.srcA1, p.pA0, p.pA1, p.mA0, p.mA1);
-    fetch5<1, 1, kLerpA>(WA[1], h1, h2, h3, d1, p.srcA0, p.srcA1, p.pA0, p.pA1, p.mA0, p.mA1);
-    fetch5<RC, 0, kLerpC>(WC[0], h1, h2, h3, d0, p.srcC0, p.srcC1, p.pC0, p.pC1, p.mC0, p.mC1);
-    fetch5<RC, 1, kLerpC>(WC[1], h1, h2, h3, d1, p.srcC0, p.srcC1, p.pC0, p.pC1, p.mC0, p.mC1);
+    constexpr bool kMselA = MTGP3_MASKSEL & 1, kMselC = MTGP3_MASKSEL & 2;
+    fetch5<1, 0, kLerpA, kMselA>(WA[0], h1, h2, h3, d0, p.srcA0, p.srcA1, p.pA0, p.pA1, p.mA0, p.mA1, p.kA0, p.kA1);
+    fetch5<1, 1, kLerpA, kMselA>(WA[1], h1, h2, h3, d1, p.srcA0, p.srcA1, p.pA0, p.pA1, p.mA0, p.mA1, p.kA0, p.kA1);
+    fetch5<RC, 0, kLerpC, kMselC>(WC[0], h1, h2, h3, d0, p.srcC0, p.srcC1, p.pC0, p.pC1, p.mC0, p.mC1, p.kC0,
+                                  p.kC1);
+    fetch5<RC, 1, kLerpC, kMselC>(WC[1], h1, h2, h3, d1, p.srcC0, p.srcC1, p.pC0, p.pC1, p.mC0, p.mC1, p.kC0,
+                                  p.kC1);
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
         uint32_t r[4], o[4];
@@ -240,6 +253,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, kMinCtas3) gen3_kernel(GenA
     p.pA1 = lane < 9;
     p.mA0 = p.pA0;
     p.mA1 = p.pA1;
+    // all-ones when lane < threshold: an arithmetic shift of (lane - thr), opaque to the
+    // predicate analysis that would turn the LOP3 back into a SEL
+    p.kA0 = (uint32_t)((int32_t)(lane - 8) >> 31);
+    p.kA1 = (uint32_t)((int32_t)(lane - 9) >> 31);
     const TeamWork tw = a.teams[team];
     for (uint32_t pi = tw.first; pi < tw.first + tw.count; ++pi) {
         const Piece pc = a.pieces[pi];
@@ -257,6 +274,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, kMinCtas3) gen3_kernel(GenA
         p.pC1 = lane < thr1;
         p.mC0 = p.pC0;
         p.mC1 = p.pC1;
+        p.kC0 = (uint32_t)((int32_t)(lane - thr0) >> 31);
+        p.kC1 = (uint32_t)((int32_t)(lane - thr1) >> 31);
         p.neg1 = 0u - prm.one;
         uint32_t* optr = reinterpret_cast<uint32_t*>(a.out) + (size_t)pc.set * a.L + pc.offset;
         if (KIND >= kKindBitmapBit0) {

@@ -12,6 +12,8 @@ from typing import Dict, Optional, Sequence, Tuple
 import numpy as np
 
 NPZ = Path(__file__).resolve().parent / "full_ck.npz"
+# Engine::mt (bench.py --config mt19937): made by make_mt_full_ck.py from the reference itself
+MT_NPZ = Path(__file__).resolve().parent / "mt_full_ck.npz"
 
 # config -> (sum array key, xor array key, float index or None, words per record, set-ID offset)
 _LAYOUT = {
@@ -21,19 +23,22 @@ _LAYOUT = {
     "c4-23209": ("c4_23209_sum", "c4_23209_xor", None, 1 << 27),
     "c4-44497": ("c4_44497_sum", "c4_44497_xor", None, 1 << 27),
     "c5": ("c5_sum", "c5_xor", None, 1 << 24),
+    "mt19937": ("mt_sum", "mt_xor", None, 1 << 27),  # stream i = MT19937 seed 5489 + i
 }
 _cache: Dict[str, np.ndarray] = {}
 
 
-def available() -> bool:
-    return NPZ.exists()
+def available(config: str = "c2") -> bool:
+    return (MT_NPZ if config == "mt19937" else NPZ).exists()
 
 
 def _arr(key: str) -> np.ndarray:
     if key not in _cache:
-        with np.load(NPZ) as z:
-            for k in z.files:
-                _cache[k] = z[k]
+        for f in (NPZ, MT_NPZ):
+            if f.exists():
+                with np.load(f) as z:
+                    for k in z.files:
+                        _cache[k] = z[k]
     return _cache[key]
 
 
@@ -47,7 +52,7 @@ def coverage(config: str) -> Tuple[int, int, int]:
 def expected(config: str, first_set: int, n_sets: int, words: int) -> Optional[Tuple[np.ndarray, np.ndarray]]:
     """Oracle (sum64, xor32) of global streams [first_set, first_set + n_sets) after `words`
     words each, or None when the fixture does not reach that far."""
-    if config not in _LAYOUT or not available():
+    if config not in _LAYOUT or not available(config):
         return None
     ks, kx, fi, rec = _LAYOUT[config]
     s, x = _arr(ks), _arr(kx)

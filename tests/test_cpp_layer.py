@@ -50,7 +50,9 @@ def test_cpp_layer_gpu(layer_exe, tmp_path):
     r = subprocess.run([str(layer_exe), str(ROOT / "tests/golden/mtgp32_11213_curand.json"), "--gpu",
                         str(_pyfile(tmp_path))], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
-    # the threading-model cases report their aggregate rate (profiles/r2_threading.txt)
+    # the threading-model cases report their aggregate rate (pytest -s shows it;
+    # profiles/r2/threading.txt)
+    print("\n".join(line for line in r.stdout.splitlines() if "THREADS" in line))
     assert r.stdout.count("every word == oracle: yes") == 2, r.stdout
 
 

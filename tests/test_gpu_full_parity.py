@@ -112,3 +112,24 @@ def test_multi_gpu_batch_c5(torch_cuda, devices, gather):
             r = full_ck.compare("c5", 0, m.checksums())
             assert r["ok"] and r["words_per_stream"] == (k + 1) << 24, r
         del bufs
+
+
+@pytest.mark.skipif(not full_ck.available("mt19937"), reason="mt_full_ck.npz not generated")
+def test_mt19937_every_word_against_the_reference(torch_cuda):
+    """bench.py --config mt19937 (Engine::mt, 200 MT19937 streams, seeds 5489 + i) with the
+    default auto plan (mt_gen3 warp teams, jump-ahead pieces): after every 2^27-word call the
+    cumulative checksums equal those of the reference's own MtWordSource::fill (oracle/_ref,
+    tests/golden/make_mt_full_ck.py) -- 25 bench steps, every word."""
+    torch = torch_cuda
+    n, records, rec = full_ck.coverage("mt19937")
+    out = torch.empty((n, rec), dtype=torch.int32, device="cuda")
+    with mtgp.MtContext([mtgp.mt19937_status()] * n, [5489 + i for i in range(n)]) as ctx:
+        ctx.set_option(mtgp.OPT_CHECKSUM, 1)
+        for k in range(records):
+            ctx.generate_device(mtgp.U32, out.data_ptr(), rec)
+            ctx.sync()
+            r = full_ck.compare("mt19937", 0, ctx.checksums())
+            assert r["ok"], (k, r)
+        pieces, _, kver = ctx.last_plan()
+    assert kver == 6 and pieces > 1000
+    del out

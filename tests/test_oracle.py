@@ -262,3 +262,22 @@ def test_large_exponents_pinned_by_curand(large_golden):
             c["sum64"], c["xor32"], c["last"])
         f = oracle_py.MtgpOracle(c["set"], c["seed"]).fill(32, kind=1)
         assert f.tolist() == c["single12_bits"]
+
+
+def test_mt_full_ck_fixture_matches_restatement():
+    """The Engine::mt fixture (made by the reference's own fill(), oracle/_ref) re-derived with
+    the C restatement of the reference's recurrence (oracle/mt_oracle.c) for the first record of
+    two streams: the fixture, the reference and the restatement agree."""
+    fc = _full_ck()
+    if not fc.available("mt19937"):
+        pytest.skip("mt_full_ck.npz not generated")
+    assert fc.coverage("mt19937") == (200, 50, 1 << 27)
+    for s in (0, 199):
+        g = oracle_py.MtOracle(None, 5489 + s)
+        sm, x = 0, 0
+        for _ in range(8):  # 2^27 words in 2^24-word pieces
+            w = g.fill(1 << 24)
+            sm += int(w.astype(np.uint64).sum())
+            x ^= int(np.bitwise_xor.reduce(w))
+        es, ex = fc.expected("mt19937", s, 1, 1 << 27)
+        assert (sm & 0xFFFFFFFFFFFFFFFF, x) == (int(es[0]), int(ex[0])), s
