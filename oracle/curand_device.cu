@@ -23,6 +23,7 @@
 #include <cinttypes>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -154,14 +155,20 @@ static int cmd_time(uint64_t L, int reps) {
     curandGenerator_t gen;
     CR(curandCreateGenerator(&gen, CURAND_RNG_PSEUDO_MTGP32));
     CR(curandSetPseudoRandomGeneratorSeed(gen, 1));
-    const size_t n = (size_t)kSets * L;
-    CR(curandGenerate(gen, out, n));  // warm
+    // the host API overflows past 2^31 outputs per call (illegal address at 200 x 2^24): the
+    // same volume as chunks of 2^28 outputs into consecutive slices of the buffer
+    const size_t n = (size_t)kSets * L, chunk = std::min<size_t>(n, size_t{1} << 28);
+    auto host_api = [&] {
+        for (size_t done = 0; done < n; done += chunk)
+            CR(curandGenerate(gen, out + done, std::min(chunk, n - done)));
+    };
+    host_api();  // warm
     CK(cudaDeviceSynchronize());
     cudaEvent_t a, b;
     CK(cudaEventCreate(&a));
     CK(cudaEventCreate(&b));
     CK(cudaEventRecord(a));
-    for (int r = 0; r < reps; ++r) CR(curandGenerate(gen, out, n));
+    for (int r = 0; r < reps; ++r) host_api();
     CK(cudaEventRecord(b));
     CK(cudaEventSynchronize(b));
     float ms = 0;

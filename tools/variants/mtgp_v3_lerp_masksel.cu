@@ -1,3 +1,8 @@
+// tools/variants/mtgp_v3_lerp_masksel.cu -- gen3 with the round-2 select experiments (MTGP3_LERP: FMA-pipe
+// select lo + m*(hi-lo); MTGP3_MASKSEL: LOP3 mask select without predicate ISETPs). Both measured
+// no faster (profiles/r2/gen3_lerp_ck_sweep.jsonl, r2/gen3_masksel_sweep.jsonl) and were removed from
+// the product kernel; build with VARIANT_SRCS and tools/sweep_variants.sh by copying over csrc/mtgp_v3.cu.
+// Original header:
 // mtgp_v3.cu -- register-resident MTGP32-11213 generation (no shared memory on the hot path).
 //
 // Same decomposition as v2 (one warp per jump-ahead piece, 256-word steps, lane t owns words
@@ -29,10 +34,21 @@ namespace mtgpb {
 
 
 // Occupancy target: 6 CTAs x 4 warps per SM (80 registers). The pipe-balance variants that
-// measured slower (IMAD.HI shifts, FMA-pipe selects and checksums, LOP3 mask selects, ...) are
-// kept in tools/variants/mtgp_v3_toggles.cu and mtgp_v3_lerp_masksel.cu, their sweeps under
-// profiles/r1_v3_*_sweep.jsonl and profiles/r2/gen3_*_sweep.jsonl.
+// measured slower in round 1 (IMAD.HI shifts, FMA-pipe selects and checksums, ...) are kept in
+// tools/variants/mtgp_v3_toggles.cu, their sweeps under profiles/r1_v3_*_sweep.jsonl.
 constexpr int kMinCtas3 = 6;
+// Operand select of the A (bit 0) / C (bit 1) stream on the FMA pipe: send = lo + m * (hi - lo)
+// with a per-lane 0/1 multiplier m and the differences hi - lo formed once per half-step pair by
+// IMAD (lo * -1 + hi), shared by both streams. One IMAD per fetch instead of one ALU SEL.
+#ifndef MTGP3_LERP
+#define MTGP3_LERP 0
+#endif
+// Operand select as one LOP3 with a per-lane all-ones / all-zeros mask register instead of
+// SEL on a predicate (bit 0: A stream, bit 1: C stream): the same ALU op count, but the four
+// lane predicates no longer have to be rematerialised by ISETPs on every trip.
+#ifndef MTGP3_MASKSEL
+#define MTGP3_MASKSEL 0
+#endif
 
 namespace {
 
@@ -49,6 +65,9 @@ struct V3Ctx {
     uint32_t mask, sh2, mul1, tblr, tmpr;
     uint32_t srcA0, srcA1, srcC0, srcC1;  // source lanes for carry e = 0 / 1
     bool pA0, pA1, pC0, pC1;              // "take the newer half-step" predicates
+    uint32_t mA0, mA1, mC0, mC1;          // the same as 0/1 multipliers (MTGP3_LERP)
+    uint32_t kA0, kA1, kC0, kC1;          // ... and as 0 / ~0 masks (MTGP3_MASKSEL)
+    uint32_t neg1;                        // 0xFFFFFFFF, opaque to the compiler
     // bitmap kinds: this stream's bitmap, the piece's first word within the call, the predicate
     uint32_t* bm;
     unsigned long long poff;
@@ -86,18 +105,37 @@ __device__ __forceinline__ uint32_t conv3(uint32_t o) {
 
 // Five consecutive operand words for half-step U from the history half-steps
 // h1 = (k=1), h2 = (k=2), h3 = (k=3); residue R; per-carry source lanes / predicates.
-template <int R, int U>
-__device__ __forceinline__ void fetch5(uint32_t W[5], const uint4& h1, const uint4& h2, const uint4& h3,
-                                       uint32_t src0, uint32_t src1, bool p0, bool p1) {
+// LERP: the select is lo + m * d with d = hi - lo (dU: the differences of this half-step pair).
+template <int R, int U, bool LERP, bool MSEL>
+__device__ __forceinline__ void fetch5(uint32_t W[5], const uint4& h1, const uint4& h2, const uint4& h3, const uint4& dU,
+                                       uint32_t src0, uint32_t src1, bool p0, bool p1, uint32_t m0, uint32_t m1,
+                                       uint32_t k0, uint32_t k1) {
 #pragma unroll
     for (int j = 0; j < 5; ++j) {
         const int c = (R + j) & 3;
         const int e = (R + j) >> 2;
         const uint4& lo = U == 0 ? h1 : h2;  // k = 1 + U
         const uint4& hi = U == 0 ? h2 : h3;  // k = 2 + U
-        const uint32_t send = (e ? p1 : p0) ? comp4(hi, c) : comp4(lo, c);
+        uint32_t send;
+        if (LERP)
+            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(send) : "r"(comp4(dU, c)), "r"(e ? m1 : m0), "r"(comp4(lo, c)));
+        else if (MSEL)  // (hi & k) | (lo & ~k)
+            asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(send) : "r"(comp4(hi, c)), "r"(comp4(lo, c)), "r"(e ? k1 : k0));
+        else
+            send = (e ? p1 : p0) ? comp4(hi, c) : comp4(lo, c);
         W[j] = __shfl_sync(FULL, send, e ? src1 : src0);
     }
+}
+
+__device__ __forceinline__ uint32_t diff1(uint32_t hi, uint32_t lo, uint32_t neg1) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(lo), "r"(neg1), "r"(hi));
+    return d;
+}
+
+__device__ __forceinline__ uint4 diff4(const uint4& hi, const uint4& lo, uint32_t neg1) {
+    return make_uint4(diff1(hi.x, lo.x, neg1), diff1(hi.y, lo.y, neg1), diff1(hi.z, lo.z, neg1),
+                      diff1(hi.w, lo.w, neg1));
 }
 
 // One 256-word step. Reads history (h1: older step's upper half; h2/h3: newer step's halves),
@@ -108,10 +146,19 @@ __device__ __forceinline__ void step3(const V3Ctx& p, const uint4& h1, const uin
                                       uint4& n1, uint4* sp, uint32_t n, uint32_t len, uint32_t* win_out,
                                       uint32_t win_lo, CkAcc<CKM>& sum, uint32_t& xr) {
     uint32_t WA[2][5], WC[2][5];
-    fetch5<1, 0>(WA[0], h1, h2, h3, p.srcA0, p.srcA1, p.pA0, p.pA1);
-    fetch5<1, 1>(WA[1], h1, h2, h3, p.srcA0, p.srcA1, p.pA0, p.pA1);
-    fetch5<RC, 0>(WC[0], h1, h2, h3, p.srcC0, p.srcC1, p.pC0, p.pC1);
-    fetch5<RC, 1>(WC[1], h1, h2, h3, p.srcC0, p.srcC1, p.pC0, p.pC1);
+    constexpr bool kLerpA = MTGP3_LERP & 1, kLerpC = MTGP3_LERP & 2;
+    uint4 d0 = h1, d1 = h2;
+    if (kLerpA || kLerpC) {
+        d0 = diff4(h2, h1, p.neg1);
+        d1 = diff4(h3, h2, p.neg1);
+    }
+    constexpr bool kMselA = MTGP3_MASKSEL & 1, kMselC = MTGP3_MASKSEL & 2;
+    fetch5<1, 0, kLerpA, kMselA>(WA[0], h1, h2, h3, d0, p.srcA0, p.srcA1, p.pA0, p.pA1, p.mA0, p.mA1, p.kA0, p.kA1);
+    fetch5<1, 1, kLerpA, kMselA>(WA[1], h1, h2, h3, d1, p.srcA0, p.srcA1, p.pA0, p.pA1, p.mA0, p.mA1, p.kA0, p.kA1);
+    fetch5<RC, 0, kLerpC, kMselC>(WC[0], h1, h2, h3, d0, p.srcC0, p.srcC1, p.pC0, p.pC1, p.mC0, p.mC1, p.kC0,
+                                  p.kC1);
+    fetch5<RC, 1, kLerpC, kMselC>(WC[1], h1, h2, h3, d1, p.srcC0, p.srcC1, p.pC0, p.pC1, p.mC0, p.mC1, p.kC0,
+                                  p.kC1);
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
         uint32_t r[4], o[4];
@@ -209,6 +256,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, kMinCtas3) gen3_kernel(GenA
     p.srcA1 = (lane + 9) & 31;
     p.pA0 = lane < 8;
     p.pA1 = lane < 9;
+    p.mA0 = p.pA0;
+    p.mA1 = p.pA1;
+    // all-ones when lane < threshold: an arithmetic shift of (lane - thr), opaque to the
+    // predicate analysis that would turn the LOP3 back into a SEL
+    p.kA0 = (uint32_t)((int32_t)(lane - 8) >> 31);
+    p.kA1 = (uint32_t)((int32_t)(lane - 9) >> 31);
     const TeamWork tw = a.teams[team];
     for (uint32_t pi = tw.first; pi < tw.first + tw.count; ++pi) {
         const Piece pc = a.pieces[pi];
@@ -224,6 +277,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, kMinCtas3) gen3_kernel(GenA
         p.srcC1 = (lane + thr1) & 31;
         p.pC0 = lane < thr0;
         p.pC1 = lane < thr1;
+        p.mC0 = p.pC0;
+        p.mC1 = p.pC1;
+        p.kC0 = (uint32_t)((int32_t)(lane - thr0) >> 31);
+        p.kC1 = (uint32_t)((int32_t)(lane - thr1) >> 31);
+        p.neg1 = 0u - prm.one;
         uint32_t* optr = reinterpret_cast<uint32_t*>(a.out) + (size_t)pc.set * a.L + pc.offset;
         if (KIND >= kKindBitmapBit0) {
             p.bm = reinterpret_cast<uint32_t*>(a.out) + (size_t)pc.set * ((a.L + 31) / 32);
