@@ -70,6 +70,8 @@ def parse():
     ap.add_argument("--checksum-mode", type=int, default=2, choices=[1, 2],
                     help="MTGP_OPT_CHECKSUM: 1 sum64 + xor32, 2 sum32 + xor32 (the fixture's sums mod 2^32)")
     ap.add_argument("--min-piece-words", type=int, default=None, help="MTGP_OPT_MIN_PIECE_WORDS (default: library's)")
+    ap.add_argument("--prejump", type=int, default=None, choices=[0, 1, 2],
+                    help="MTGP_OPT_PREJUMP: speculative next-call jumps, 0 auto (library default), 1 off, 2 on")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1, help="end-to-end (host output) steps timed")
     ap.add_argument("--e2e-words-per-call", type=int, default=1 << 22,
@@ -385,6 +387,8 @@ def main():
     first_set = set_range.start if is_c5 else shard_rank * S
     if args.min_piece_words:
         ctx.set_option(mtgp.OPT_MIN_PIECE_WORDS, args.min_piece_words)
+    if args.prejump is not None:
+        ctx.set_option(mtgp.OPT_PREJUMP, args.prejump)
     ext = torch.cuda.ExternalStream(ctx.stream_handle(), device=torch.device("cuda", local))
     out = torch.empty((S, Lc), dtype=torch.int32, device=f"cuda:{local}")
 
@@ -580,6 +584,7 @@ def main():
             "config": {"workload": label, "sets_per_gpu": S, "seed": 1, "words_per_set_per_step": L_step,
                        "calls_per_step": calls, "kernel": f"v{kver}", "pieces_per_call": pieces,
                        "checksums_fused": not args.no_checksum,
+                       "prejump": {None: "auto", 0: "auto", 1: "off", 2: "on"}[args.prejump],
                        "checksum_mode": {0: "off", 1: "sum64+xor32", 2: "sum32+xor32"}[ck_mode],
                        **({"as_rank": shard_rank, "as_world": shard_world} if args.as_rank is not None else {}),
                        "global_set_ids": ([set_range.start, set_range.stop] if is_c5

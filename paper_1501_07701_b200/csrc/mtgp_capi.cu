@@ -305,6 +305,10 @@ int mtgp_set_option(mtgp_ctx* ctx, int option, int64_t value) {
             if (value < 1) return fail(MTGP_EINVAL, "host chunk must be >= 1");
             ctx->host_chunk = (uint64_t)value;
             return MTGP_OK;
+        case MTGP_OPT_PREJUMP:
+            if (value < 0 || value > 2) return fail(MTGP_EINVAL, "prejump must be 0 (auto), 1 (off) or 2 (on)");
+            ctx->prejump = (int)value;
+            return MTGP_OK;
         case MTGP_OPT_JUMP:
             if (value < 0 || value > 2) return fail(MTGP_EINVAL, "jump must be 0 (auto), 1 (direct) or 2 (split)");
             ctx->jump_mode = (int)value;
@@ -318,9 +322,17 @@ int mtgp_set_option(mtgp_ctx* ctx, int option, int64_t value) {
 
 namespace {
 
+int generate_device_impl(mtgp_ctx* ctx, int kind, void* out, uint64_t L);
+
 // One device-side generation of L words per stream into device memory `out`.
 int generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
     if (L == 0) return MTGP_OK;
+    const int rc = generate_device_impl(ctx, kind, out, L);
+    ++ctx->state_epoch;  // whatever ran (or failed half-way), the next call starts a new epoch
+    return rc;
+}
+
+int generate_device_impl(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
     if (kind >= kKindBitmapBit0 && (ctx->kernel == 1 || !ctx->planner || !ctx->planner->v2_supported() ||
                                     (ctx->engine == 1 && (ctx->kernel == 5 || !ctx->planner->mt3_supported(kind, L, out)))))
         return fail(MTGP_EINVAL, "bitmap output needs the register-resident warp-team kernels");
@@ -380,6 +392,8 @@ int generate_device(mtgp_ctx* ctx, int kind, void* out, uint64_t L) {
         run.timing = ctx->timing ? &ctx->pool : nullptr;
         // Engine::mt contexts: 5 / 6 pick the warp-team kernel, the MTGP kernel numbers mean auto
         run.want_kernel = ctx->engine == 1 ? (ctx->kernel >= 5 ? ctx->kernel : 0) : ctx->kernel;
+        run.prejump = ctx->prejump;
+        run.epoch = ctx->state_epoch;
         std::string err;
         cudaError_t e = ctx->planner->run(run, err);
         if (e != cudaSuccess) return fail(e == cudaErrorMemoryAllocation ? MTGP_ENOMEM : MTGP_ECUDA, "v2 generation: %s (%s)", err.c_str(), cudaGetErrorString(e));
@@ -492,6 +506,7 @@ int mtgp_generate_f32_01oc(mtgp_ctx* ctx, float* out, uint64_t L, int out_is_dev
 int mtgp_skip(mtgp_ctx* ctx, uint64_t words) {
     if (!ctx) return fail(MTGP_EINVAL, "null context");
     if (words == 0) return MTGP_OK;
+    ++ctx->state_epoch;
     CK(cudaSetDevice(ctx->device), "cudaSetDevice");
     if (words < 4096 || !ctx->planner || !ctx->planner->v2_supported()) {
         // Short skips (and shapes without a planner: mixed Engine::mt statuses): generate into a
@@ -563,6 +578,7 @@ int mtgp_state_restore(mtgp_ctx* ctx, const uint32_t* windows, const uint64_t* p
     CK(cudaStreamSynchronize(ctx->stream), "sync");
     if (positions) std::copy(positions, positions + ctx->n_sets, ctx->position.begin());
     if (ctx->planner) ctx->planner->invalidate();
+    ++ctx->state_epoch;
     return MTGP_OK;
 }
 

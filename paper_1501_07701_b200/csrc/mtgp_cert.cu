@@ -66,6 +66,7 @@ int mt_probe(mtgp_ctx* ctx, std::vector<gf2::Poly>& polys) {
     }
     cudaMemcpyAsync(ctx->d_win, d_win, win_bytes, cudaMemcpyDeviceToDevice, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
+    ++ctx->state_epoch;  // the window went back: no speculative windows apply
     ctx->position = pos;
     ctx->cksum = ck;
     cudaFree(d_words);

@@ -41,6 +41,10 @@ struct mtgp_ctx {
     bool ck_sum_mod32 = false;  // a mode-2 call ran since the last reset: sum64 is valid mod 2^32
     int kernel = 0;
     int jump_mode = 0;  // MTGP_OPT_JUMP
+    int prejump = 0;    // MTGP_OPT_PREJUMP
+    // bumped by every change of the stream states (generation, skip, restore, stat passes): the
+    // planner's speculative next-call windows are valid only for the very next state
+    uint64_t state_epoch = 0;
     BitmapPred bm_pred;  // predicate of kKindBitmapRange (ctx_generate_bitmap)
     uint32_t stage_next = 0;  // host output: the staging buffer the next chunk uses (alternates across calls)
     uint32_t max_pieces = 0;

@@ -138,12 +138,42 @@ struct PlannerImpl {
 
     DevBuf d_pieces, d_teams, d_pwin_ptrs, d_pwin, d_q, d_pre, d_rows, d_joboff, d_jobs, d_win_next, d_all_rows,
         d_zbuf, d_leaf;
+    uint64_t plan_id = 0;  // bumped by every plan rebuild
+
+    // Speculative next-call jumps (Planner::run). Call k's prefix x_{t0..} also determines every
+    // window of call k + 1 (x^(offset + L - t0) mod P instead of x^(offset - t0)), so while call
+    // k generates, a side stream computes call k + 1's piece windows into d_pwin_next. Call k + 1
+    // waits for them instead of jumping on the critical path. Worth it when the generator
+    // leaves SM slots free (few-piece plans: small shards, single streams).
+    DevBuf d_q_next, d_pwin_next;
+    uint64_t q_next_plan = ~0ull;  // plan_id the d_q_next polynomials belong to
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_pre = nullptr, ev_spec = nullptr;
+    bool spec_inflight = false;    // ev_spec not yet waited for on the context stream
+    bool spec_ready = false;       // d_pwin_next holds the windows of the call after the last run
+    uint64_t spec_epoch = 0, spec_plan = 0;
+
+    // Order the context stream after an in-flight speculative jump: it reads d_pre, d_q_next,
+    // the job tables and the Karatsuba scratch, which the context stream's next work may rewrite.
+    void join(cudaStream_t st) {
+        if (spec_inflight) {
+            cudaStreamWaitEvent(st, ev_spec, 0);
+            spec_inflight = false;
+        }
+    }
 
     ~PlannerImpl() {
+        if (side) {
+            cudaStreamSynchronize(side);
+            cudaStreamDestroy(side);
+        }
+        if (ev_pre) cudaEventDestroy(ev_pre);
+        if (ev_spec) cudaEventDestroy(ev_spec);
         for (DevBuf* b : {&d_pieces, &d_teams, &d_pwin_ptrs, &d_pwin, &d_q, &d_pre, &d_rows, &d_joboff, &d_jobs,
-                          &d_win_next, &d_all_rows, &d_zbuf, &d_leaf})
+                          &d_win_next, &d_all_rows, &d_zbuf, &d_leaf, &d_q_next, &d_pwin_next})
             b->release();
     }
+    cudaError_t build_next_q(uint64_t L, cudaStream_t st);
     // d = 0 (N <= 384, i.e. 11213) keeps the flat jump when the jumps fill the GPU: the grouped
     // d = 0 leaf path measured 0.66 vs 0.51 ms per C2 call (profiles/r1_jump_sweep.jsonl)
     double jump_k = 0;  // pieces_wanted's G / (r J) for this shape
@@ -234,10 +264,12 @@ void Planner::invalidate() {
     impl_->analyzed = false;
     impl_->jumps_ok = false;
     impl_->plan_valid = false;
+    impl_->spec_ready = false;
 }
 
 cudaError_t Planner::analyze_now(const void* params, const uint32_t* win, cudaStream_t st, std::string& err) {
     if (!impl_->v2) return cudaSuccess;
+    impl_->join(st);
     return impl_->analyze(params, win, st, err);
 }
 
@@ -456,7 +488,47 @@ cudaError_t PlannerImpl::build_plan(uint64_t L, uint32_t T, uint64_t min_piece, 
     plan_T = T;
     plan_want = want;
     plan_valid = true;
+    ++plan_id;
     return cudaGetLastError();
+}
+
+// The current plan's jump polynomials for the NEXT call: x^(offset + L - t0) mod P per job
+// (the same pieces, one call later), uploaded to d_q_next.
+cudaError_t PlannerImpl::build_next_q(uint64_t L, cudaStream_t st) {
+    if (q_next_plan == plan_id) return cudaSuccess;
+    std::vector<uint32_t> hq((size_t)n_q * q_words, 0);
+    std::vector<uint32_t> rows_list(jump_rows);
+    parallel_for(rows_list.size(), [&](size_t r) {
+        const gf2::Modulus& md = *mods[rows_list[r]];
+        gf2::Poly cur;
+        uint64_t cur_off = 0;
+        bool have = false;
+        std::map<uint64_t, gf2::Poly> step_cache;
+        for (uint32_t jj = job_off[r]; jj < job_off[r + 1]; ++jj) {
+            const uint64_t off = pieces[jobs[jj].piece].offset + L - t0;
+            if (!have) {
+                cur = md.x_pow(off);
+                have = true;
+            } else {
+                const uint64_t d = off - cur_off;
+                auto it = step_cache.find(d);
+                if (it == step_cache.end()) it = step_cache.emplace(d, md.x_pow(d)).first;
+                cur = md.mulmod(cur, it->second);
+            }
+            cur_off = off;
+            uint32_t* dst = hq.data() + (size_t)jobs[jj].q * q_words;
+            for (int i = 0; i <= cur.degree(); ++i)
+                if (cur.coeff(i)) dst[i >> 5] |= 1u << (i & 31);
+        }
+    });
+    cudaError_t e;
+    if ((e = d_q_next.ensure(sizeof(uint32_t) * std::max<size_t>(1, hq.size()))) != cudaSuccess) return e;
+    if (!hq.empty() &&
+        (e = cudaMemcpyAsync(d_q_next.p, hq.data(), sizeof(uint32_t) * hq.size(), cudaMemcpyHostToDevice, st)) !=
+            cudaSuccess)
+        return e;
+    q_next_plan = plan_id;
+    return cudaSuccess;
 }
 
 cudaError_t Planner::run(PlanRun& r, std::string& err) {
@@ -465,6 +537,7 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         err = "v2 kernel does not support this parameter shape";
         return cudaSuccess;
     }
+    I.join(r.stream);
     // v3 (register-resident ring) serves MTGP32-11213 when every piece starts 16-byte aligned:
     // 16-byte aligned output, L % 4 == 0 (piece offsets are multiples of 4 by construction)
     const bool reg_ok = !I.mt && r.L % 4 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 15) == 0;
@@ -529,6 +602,16 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         return e;
     if (!err.empty()) return cudaSuccess;
 
+    // Speculative jumps: use the windows the previous call computed for this one when nothing
+    // touched the state in between (epoch) and the plan is the same; speculate for the next call
+    // when the plan has jumps and leaves SM slots free (auto), or always (MTGP_OPT_PREJUMP 2).
+    const bool has_jumps = !I.jump_rows.empty();
+    const bool use_spec = has_jumps && I.spec_ready && r.epoch == I.spec_epoch && I.spec_plan == I.plan_id;
+    I.spec_ready = false;
+    const bool spec_next = has_jumps && r.prejump != 1 && (r.prejump == 2 || 3 * I.teams.size() <= 2 * (size_t)T);
+    if (use_spec) std::swap(I.d_pwin, I.d_pwin_next);  // d_pwin_next's windows are complete (join)
+    r.prejumped = use_spec;
+
     // per-piece start-window pointers: jumped pieces -> d_pwin rows; offset-0 pieces -> current window
     std::vector<const uint32_t*> ptrs(I.pieces.size());
     for (size_t i = 0; i < I.pieces.size(); ++i)
@@ -539,30 +622,58 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         return e;
 
     size_t j0 = 0, j1 = 0, g0 = 0, g1 = 0;
-    if (!I.jump_rows.empty()) {
-        if (r.timing) r.timing->record(r.stream, &j0);
+    JumpArgs ja;
+    ja.pre = I.d_pre.as<uint32_t>();
+    ja.pre_len = I.pre_len;
+    ja.pre_stride = I.prefix_stride();
+    ja.pre_off = I.t0;
+    ja.set_of = I.d_rows.as<uint32_t>();
+    ja.job_off = I.d_joboff.as<uint32_t>();
+    ja.jobs = I.d_jobs.as<JumpJob>();
+    ja.q = I.d_q.as<uint32_t>();
+    ja.q_words = I.q_words;
+    ja.piece_win = I.d_pwin.as<uint32_t>();
+    ja.max_jobs_per_row = I.max_jobs_per_row;
+    ja.n_jobs = (uint32_t)I.jobs.size();
+    if (has_jumps && (!use_spec || spec_next)) {
+        // this call's prefix x_0.. (needed by this call's jumps, or by the next call's speculation)
+        if (r.timing && !use_spec) r.timing->record(r.stream, &j0);
         if ((e = I.prefix(r.params, r.win, I.d_rows.as<uint32_t>(), (uint32_t)I.jump_rows.size(),
                           I.d_pre.as<uint32_t>(), I.prefix_stride(), r.stream)) != cudaSuccess)
             return e;
-        JumpArgs ja;
-        ja.pre = I.d_pre.as<uint32_t>();
-        ja.pre_len = I.pre_len;
-        ja.pre_stride = I.prefix_stride();
-        ja.pre_off = I.t0;
-        ja.set_of = I.d_rows.as<uint32_t>();
-        ja.job_off = I.d_joboff.as<uint32_t>();
-        ja.jobs = I.d_jobs.as<JumpJob>();
-        ja.q = I.d_q.as<uint32_t>();
-        ja.q_words = I.q_words;
-        ja.piece_win = I.d_pwin.as<uint32_t>();
-        ja.max_jobs_per_row = I.max_jobs_per_row;
-        ja.n_jobs = (uint32_t)I.jobs.size();
+        r.launches += 1;
+    }
+    if (has_jumps && !use_spec) {
         if ((e = I.jump(ja, (uint32_t)I.jump_rows.size(), r.stream)) != cudaSuccess) return e;
         if (r.timing) {
             r.timing->record(r.stream, &j1);
             r.timing->jump.push_back({j0, j1});
         }
-        r.launches += 2;
+        r.launches += 1;
+    }
+    if (spec_next) {
+        // the next call's windows from this call's prefix, on the side stream, overlapping this
+        // call's generation (after this call's own jump: they share the Karatsuba scratch)
+        if ((e = I.build_next_q(r.L, r.stream)) != cudaSuccess) return e;
+        if ((e = I.d_pwin_next.ensure(sizeof(uint32_t) * I.N * std::max<size_t>(1, I.pieces.size()))) != cudaSuccess)
+            return e;
+        if (!I.side) {
+            if ((e = cudaStreamCreateWithFlags(&I.side, cudaStreamNonBlocking)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&I.ev_pre, cudaEventDisableTiming)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&I.ev_spec, cudaEventDisableTiming)) != cudaSuccess) return e;
+        }
+        if ((e = cudaEventRecord(I.ev_pre, r.stream)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(I.side, I.ev_pre, 0)) != cudaSuccess) return e;
+        JumpArgs jn = ja;
+        jn.q = I.d_q_next.as<uint32_t>();
+        jn.piece_win = I.d_pwin_next.as<uint32_t>();
+        if ((e = I.jump(jn, (uint32_t)I.jump_rows.size(), I.side)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(I.ev_spec, I.side)) != cudaSuccess) return e;
+        I.spec_inflight = true;
+        I.spec_ready = true;
+        I.spec_epoch = r.epoch + 1;
+        I.spec_plan = I.plan_id;
+        r.launches += 1;
     }
     if (I.mt) {
         MtGenArgs ma;
@@ -618,6 +729,7 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
 cudaError_t Planner::charpoly_sha1(const void* params, uint32_t* win, cudaStream_t st,
                                    std::vector<std::string>& out, std::string& err) {
     PlannerImpl& I = *impl_;
+    I.join(st);
     cudaError_t e;
     if (!I.analyzed && (e = I.analyze(params, win, st, err)) != cudaSuccess) return e;
     out.assign(I.S, std::string());
@@ -635,6 +747,7 @@ cudaError_t Planner::charpoly_sha1(const void* params, uint32_t* win, cudaStream
 cudaError_t Planner::certify(const void* params, uint32_t* win, cudaStream_t st, std::vector<int>& out,
                              std::string& err) {
     PlannerImpl& I = *impl_;
+    I.join(st);
     cudaError_t e;
     if (!I.analyzed && (e = I.analyze(params, win, st, err)) != cudaSuccess) return e;
     out.assign(I.S, 0);
@@ -652,6 +765,8 @@ cudaError_t Planner::skip(const void* params, uint32_t* win, uint64_t words, cud
         err = "skip (jump-ahead) is implemented for mexp 11213, 23209 and 44497 and uniform Engine::mt shapes";
         return cudaSuccess;
     }
+    I.join(st);  // the skip's jump uses the Karatsuba scratch
+    I.spec_ready = false;
     cudaError_t e;
     if (!I.analyzed && (e = I.analyze(params, win, st, err)) != cudaSuccess) return e;
     for (uint32_t s = 0; s < I.S; ++s)

@@ -31,6 +31,12 @@ struct PlanRun {
     EventPool* timing = nullptr;  // non-null: record event pairs around the launches
     int want_kernel = 0;          // 0 auto, 2 force v2, 3 force v3, 4 v4; Engine::mt: 5 mt_gen2, 6 mt_gen3
     int version = 0;              // kernel that ran (2, 3, 4; 5 = Engine::mt warp teams)
+    // Speculative next-call jumps (MTGP_OPT_PREJUMP: 0 auto, 1 off, 2 on). epoch: the context's
+    // state epoch at this call (bumped by every state change); the speculation made by a call
+    // is used by the next one only if it arrives with epoch + 1 and the same plan.
+    int prejump = 0;
+    uint64_t epoch = 0;
+    bool prejumped = false;       // result: this call's piece windows came from the speculation
     // results
     uint64_t launches = 0;        // kernels launched by this call
     uint32_t pieces = 0, warps_per_piece = 0;

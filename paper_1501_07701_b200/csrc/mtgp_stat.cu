@@ -646,6 +646,7 @@ struct StateGuard {
     ~StateGuard() {
         cudaMemcpyAsync(ctx->d_win, win, (size_t)ctx->n_sets * ctx->N * 4, cudaMemcpyDeviceToDevice, ctx->stream);
         cudaStreamSynchronize(ctx->stream);
+        ++ctx->state_epoch;  // the window went back: no speculative windows apply
         ctx->position = pos;
         ctx->cksum = cksum;
     }

@@ -24,6 +24,7 @@ LIB_PATH = _HERE / "libmtgp_b200.so"
 MTGP_OK, MTGP_EINVAL, MTGP_ECUDA, MTGP_ENOMEM, MTGP_ESTATE = 0, 1, 2, 3, 4
 U32, F32_12, F32_01OC, F64_01 = 0, 1, 2, 3
 OPT_CHECKSUM, OPT_KERNEL, OPT_MAX_PIECES, OPT_MIN_PIECE_WORDS, OPT_TIMING, OPT_HOST_CHUNK, OPT_JUMP = 1, 2, 3, 4, 5, 6, 7
+OPT_PREJUMP = 8  # speculative next-call jumps: 0 auto, 1 off, 2 always
 
 # Every symbol include/mtgp_b200.h declares (checked by the CPU test suite).
 EXPORTS = (
