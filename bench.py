@@ -70,6 +70,7 @@ def parse():
     ap.add_argument("--checksum-mode", type=int, default=2, choices=[1, 2],
                     help="MTGP_OPT_CHECKSUM: 1 sum64 + xor32, 2 sum32 + xor32 (the fixture's sums mod 2^32)")
     ap.add_argument("--min-piece-words", type=int, default=None, help="MTGP_OPT_MIN_PIECE_WORDS (default: library's)")
+    ap.add_argument("--max-pieces", type=int, default=None, help="MTGP_OPT_MAX_PIECES (cap on teams/pieces per call)")
     ap.add_argument("--prejump", type=int, default=None, choices=[0, 1, 2],
                     help="MTGP_OPT_PREJUMP: speculative next-call jumps, 0 auto (library default), 1 off, 2 on")
     ap.add_argument("--no-e2e", action="store_true")
@@ -389,6 +390,8 @@ def main():
         ctx.set_option(mtgp.OPT_MIN_PIECE_WORDS, args.min_piece_words)
     if args.prejump is not None:
         ctx.set_option(mtgp.OPT_PREJUMP, args.prejump)
+    if args.max_pieces:
+        ctx.set_option(mtgp.OPT_MAX_PIECES, args.max_pieces)
     ext = torch.cuda.ExternalStream(ctx.stream_handle(), device=torch.device("cuda", local))
     out = torch.empty((S, Lc), dtype=torch.int32, device=f"cuda:{local}")
 

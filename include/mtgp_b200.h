@@ -100,7 +100,7 @@ typedef struct mtgp_ctx mtgp_ctx;
                                    /* windows N > 384 words, direct otherwise), 1 = direct always, */
                                    /* 2 = split (Karatsuba, or q blocks over several warps at d=0) */
 #define MTGP_OPT_PREJUMP 8         /* speculative next-call jumps: 0 = auto (when the call's plan   */
-                                   /* leaves >= 1/3 of the generator's warp slots free), 1 = off,  */
+                                   /* uses <= 1/4 of the generator's warp slots), 1 = off,         */
                                    /* 2 = always. Each call's jump-ahead windows for the NEXT call  */
                                    /* (same length, no state change in between) are computed on a  */
                                    /* side stream while this call generates                         */

@@ -604,11 +604,16 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
 
     // Speculative jumps: use the windows the previous call computed for this one when nothing
     // touched the state in between (epoch) and the plan is the same; speculate for the next call
-    // when the plan has jumps and leaves SM slots free (auto), or always (MTGP_OPT_PREJUMP 2).
+    // when the plan has jumps and its teams fill at most a quarter of the generator's warp slots
+    // (auto), or always (MTGP_OPT_PREJUMP 2). Measured (profiles/r2/): one long-lived stream in
+    // 2^20-word calls 5.3 -> 8.0 G words/s (the jump leaves the critical path and runs on idle
+    // SMs); full-occupancy plans (C2-C5, MT19937) within +-1% (the side-stream jump only fills
+    // the generator's tail, and slows the generator by what it saves); half-occupancy plans
+    // (C5 shards at 4-8 GPUs, 3 of 6 CTAs per SM) 12-20% slower (it competes with the generator).
     const bool has_jumps = !I.jump_rows.empty();
     const bool use_spec = has_jumps && I.spec_ready && r.epoch == I.spec_epoch && I.spec_plan == I.plan_id;
     I.spec_ready = false;
-    const bool spec_next = has_jumps && r.prejump != 1 && (r.prejump == 2 || 3 * I.teams.size() <= 2 * (size_t)T);
+    const bool spec_next = has_jumps && r.prejump != 1 && (r.prejump == 2 || 4 * I.teams.size() <= (size_t)T);
     if (use_spec) std::swap(I.d_pwin, I.d_pwin_next);  // d_pwin_next's windows are complete (join)
     r.prejumped = use_spec;
 
