@@ -32,7 +32,8 @@ static void run(const char* name, const Status& st, std::size_t span, std::size_
 int main() {
     const MtgpStatus mtgp = curand_mtgp32_11213()[0];
     const MtStatus mt = mt19937_status();
-    for (std::size_t chunk : {std::size_t{1} << 20, std::size_t{1} << 22}) {
+    for (std::size_t chunk : {std::size_t{1} << 17, std::size_t{1} << 18, std::size_t{1} << 19, std::size_t{1} << 20,
+                              std::size_t{1} << 22}) {
         for (std::size_t span : {std::size_t{1024}, std::size_t{4096}}) {
             run("mtgp32-11213", mtgp, span, chunk);
             run("mt19937", mt, span, chunk);
