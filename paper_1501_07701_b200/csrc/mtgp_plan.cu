@@ -185,6 +185,7 @@ struct PlannerImpl {
         jump_k = 3.8e-3 * (351.0 * 11213.0) / ((double)N * (double)M * f);
     }
     bool use_kara() const { return kara_ok && ((jump_mode == 0 && kara.depth > 0) || jump_mode == 2); }
+    uint32_t last_jump_launches = 1;  // kernels the last jump() call launched
 
     // words the jump kernels read per row (from x_{t0})
     uint32_t prefix_len() const {
@@ -211,6 +212,8 @@ struct PlannerImpl {
         // warps per jump then (profiles/r1_single_stream.jsonl); keep the flat kernel when the
         // jumps already fill the GPU (C2: 0.51 vs 0.66 ms, profiles/r1_jump_sweep.jsonl).
         const bool split0 = jump_mode == 0 && kara_ok && kara.depth == 0 && kara_groups(kara, a.n_jobs, num_sms) >= 3;
+        // kernels this jump launches: ztrans (d >= 1), qleaf, leaf, combine; or the one flat kernel
+        last_jump_launches = (use_kara() || split0) ? (kara.depth > 0 ? 4u : 3u) : 1u;
         if (use_kara() || split0) {
             KaraPlan k = kara;
             k.groups = kara_groups(k, a.n_jobs, num_sms);
@@ -654,7 +657,7 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
             r.timing->record(r.stream, &j1);
             r.timing->jump.push_back({j0, j1});
         }
-        r.launches += 1;
+        r.launches += I.last_jump_launches;
     }
     if (spec_next) {
         // the next call's windows from this call's prefix, on the side stream, overlapping this
@@ -678,7 +681,7 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         I.spec_ready = true;
         I.spec_epoch = r.epoch + 1;
         I.spec_plan = I.plan_id;
-        r.launches += 1;
+        r.launches += I.last_jump_launches;
     }
     if (I.mt) {
         MtGenArgs ma;
