@@ -423,3 +423,36 @@ def test_large_mexp_single_float_pinned_by_curand(large_golden, mexp):
         f = ctx.generate_host(mtgp.F32_12, 32)
     for i, c in enumerate(cases):
         assert f[i].tolist() == c["single12_bits"]
+
+
+@pytest.mark.parametrize("prejump", [1, 2])
+def test_back_to_back_calls_queued_behind_a_busy_stream(curand_sets, prejump):
+    """ADVICE r1 (plan upload race): calls of different lengths issued back to back without a
+    sync, all queued behind a ~0.5 s spin kernel on the context stream, so every call's plan
+    (and, with prejump 2, every speculative jump) is built and uploaded while the earlier calls
+    have not even started. Each call's words and the end state must still equal the oracle."""
+    import torch
+
+    sets = curand_sets[:16]
+    seeds = list(range(100, 116))
+    lens = [1 << 22, 1 << 18, (1 << 20) + 4 * 12345, 1 << 22, 1 << 16, 1 << 22]
+    with mtgp.MtgpContext(sets, seeds) as ctx:
+        ctx.set_option(mtgp.OPT_MIN_PIECE_WORDS, 1 << 15)  # every call split into jumped pieces
+        ctx.set_option(mtgp.OPT_PREJUMP, prejump)
+        ext = torch.cuda.ExternalStream(ctx.stream_handle())
+        bufs = []
+        with torch.cuda.stream(ext):
+            torch.cuda._sleep(1_000_000_000)
+            for L in lens:
+                b = torch.empty((16, L), dtype=torch.int32, device="cuda")
+                ctx.generate_device(mtgp.U32, b.data_ptr(), L)
+                bufs.append(b)
+        ctx.sync()
+        pos = 0
+        for L, b in zip(lens, bufs):
+            got = b.cpu().numpy().view(np.uint32)
+            want = oracle_py.mtgp_bulk(sets, seeds, L, skip=pos, threads=16)[0]
+            assert np.array_equal(got, want), (prejump, L, pos)
+            pos += L
+        tail = ctx.fill_u32(1024)
+    assert np.array_equal(tail, oracle_py.mtgp_bulk(sets, seeds, 1024, skip=pos, threads=16)[0])
