@@ -37,7 +37,7 @@ int mt_gen2_ctas_per_sm(uint32_t n, int kind, bool cksum);
 // Register-resident warp teams (csrc/mtgp_mt3.cu, kernel version 6): n = 624, every status
 // n - m >= 129 (min_gap), u32 or f64 output, L % 4 == 0, 16-byte aligned output.
 bool mt_gen3_supports(uint32_t n, uint32_t min_gap, int kind);
-cudaError_t launch_mt_gen3(uint32_t n, int kind, bool cksum, const MtGenArgs& a, cudaStream_t st);
-int mt_gen3_ctas_per_sm(uint32_t n, int kind, bool cksum);
+cudaError_t launch_mt_gen3(uint32_t n, int kind, int ck_mode, const MtGenArgs& a, cudaStream_t st);  // ck_mode 0/1/2
+int mt_gen3_ctas_per_sm(uint32_t n, int kind, int ck_mode);
 
 }  // namespace mtgpb

@@ -17,12 +17,20 @@
 //   * the step loop is unrolled by H, so the history shift is register renaming.
 // u32 output; pieces come from the shared planner / jump-ahead (csrc/mtgp_plan.cu), windows in
 // the same n-word window model as every other kernel.
+#include <algorithm>
+#include <type_traits>
+
 #include "mtgp_bitmap.cuh"
 #include "mtgp_mt.cuh"
 #include "mtgp_v2.cuh"
 
 #ifndef MTGP6_MIN_CTAS
 #define MTGP6_MIN_CTAS 5  // 6: 19% more pieces (jumps) for the same cycles
+#endif
+// Planned CTAs per SM: the checksum-mode-2 and unchecked variants fit 6 (80 registers), but the
+// plan keeps 5 so the piece count (jumps) stays that of the 5-CTA layout
+#ifndef MTGP6_MAX_CTAS
+#define MTGP6_MAX_CTAS 5
 #endif
 // Right shifts of the tempering on the FMA pipe as IMAD.HI by 2^(32-k): 0 none, 1 the last
 // (v >> l), 2 both (v >> u too).
@@ -36,6 +44,11 @@
 namespace mtgpb {
 
 namespace {
+
+// Checksum modes (MTGP_OPT_CHECKSUM): 0 none; 1 sum64 + xor32; 2 sum32 + xor32 (the sum mod 2^32
+// in a 32-bit accumulator: one 3-input IADD3 per two words, no carry chain), as in gen3.
+template <int CKM>
+using CkAcc6 = typename std::conditional<CKM == 2, uint32_t, unsigned long long>::type;
 
 constexpr uint32_t kFull6 = 0xffffffffu;
 constexpr uint32_t kHalfWords = 128;
@@ -94,9 +107,9 @@ __device__ __forceinline__ double u32_to_f64_01(uint32_t u) {
 
 // One 128-word step at piece word n; dst = this lane's slot of the step's output (16 bytes for
 // u32, 32 bytes for f64: KIND = MTGP_U32 / MTGP_F64_01).
-template <uint32_t NW, int RC, int AC, int KIND, bool CK, bool TAIL>
+template <uint32_t NW, int RC, int AC, int KIND, int CKM, bool TAIL>
 __device__ __forceinline__ void step6(const M6Ctx& p, const uint4 (&Hs)[S6<NW>::H], uint4& nw, uint4* dst,
-                                      uint32_t n, uint32_t len, uint32_t* win_out, unsigned long long& sum,
+                                      uint32_t n, uint32_t len, uint32_t* win_out, CkAcc6<CKM>& sum,
                                       uint32_t& xr) {
     using S = S6<NW>;
     uint32_t WA[5], WC[4];
@@ -132,7 +145,11 @@ __device__ __forceinline__ void step6(const M6Ctx& p, const uint4 (&Hs)[S6<NW>::
         } else {
             __stcs(dst, make_uint4(o[0], o[1], o[2], o[3]));
         }
-        if (CK) {
+        if constexpr (CKM == 2) {
+            sum = sum + o[0] + o[1];  // 3-input IADD3s, mod 2^32
+            sum = sum + o[2] + o[3];
+            xr ^= o[0] ^ o[1] ^ o[2] ^ o[3];
+        } else if (CKM == 1) {
 #if MTGP6_CK_WIDE
             // 64-bit sum on the FMA pipe: IMAD.WIDE.U32 sum = o * 1 + sum (the 1 is opaque)
 #pragma unroll
@@ -162,9 +179,9 @@ __device__ __forceinline__ void shift1(uint4 (&Hs)[NH], const uint4& nw) {
     Hs[NH - 1] = nw;
 }
 
-template <uint32_t NW, int RC, int AC, int KIND, bool CK>
+template <uint32_t NW, int RC, int AC, int KIND, int CKM>
 __device__ __forceinline__ void run6(const M6Ctx& p, uint4 (&Hs)[S6<NW>::H], uint32_t* optr, uint32_t len,
-                                     uint32_t* win_out, unsigned long long& sum, uint32_t& xr) {
+                                     uint32_t* win_out, CkAcc6<CKM>& sum, uint32_t& xr) {
     using S = S6<NW>;
     const uint32_t steps = (len + kHalfWords - 1) / kHalfWords;
     // A step at n makes sequence words [N + n, N + n + 128): no store predicate and no end
@@ -177,43 +194,43 @@ __device__ __forceinline__ void run6(const M6Ctx& p, uint4 (&Hs)[S6<NW>::H], uin
 #pragma unroll
         for (uint32_t k = 0; k < S::H; ++k) {
             uint4 nw;
-            step6<NW, RC, AC, KIND, CK, false>(p, Hs, nw, dst + 32 * V * k, (m + k) * kHalfWords, len, nullptr, sum,
+            step6<NW, RC, AC, KIND, CKM, false>(p, Hs, nw, dst + 32 * V * k, (m + k) * kHalfWords, len, nullptr, sum,
                                                xr);
             shift1(Hs, nw);
         }
     }
     for (; m < steps; ++m, dst += 32 * V) {
         uint4 nw;
-        step6<NW, RC, AC, KIND, CK, true>(p, Hs, nw, dst, m * kHalfWords, len, win_out, sum, xr);
+        step6<NW, RC, AC, KIND, CKM, true>(p, Hs, nw, dst, m * kHalfWords, len, win_out, sum, xr);
         shift1(Hs, nw);
     }
 }
 
-template <uint32_t NW, int AC, int KIND, bool CK>
+template <uint32_t NW, int AC, int KIND, int CKM>
 __device__ __forceinline__ void run6_rc(int rc, const M6Ctx& p, uint4 (&Hs)[S6<NW>::H], uint32_t* optr,
-                                        uint32_t len, uint32_t* win_out, unsigned long long& sum, uint32_t& xr) {
+                                        uint32_t len, uint32_t* win_out, CkAcc6<CKM>& sum, uint32_t& xr) {
     switch (rc) {
-        case 0: run6<NW, 0, AC, KIND, CK>(p, Hs, optr, len, win_out, sum, xr); break;
-        case 1: run6<NW, 1, AC, KIND, CK>(p, Hs, optr, len, win_out, sum, xr); break;
-        case 2: run6<NW, 2, AC, KIND, CK>(p, Hs, optr, len, win_out, sum, xr); break;
-        default: run6<NW, 3, AC, KIND, CK>(p, Hs, optr, len, win_out, sum, xr); break;
+        case 0: run6<NW, 0, AC, KIND, CKM>(p, Hs, optr, len, win_out, sum, xr); break;
+        case 1: run6<NW, 1, AC, KIND, CKM>(p, Hs, optr, len, win_out, sum, xr); break;
+        case 2: run6<NW, 2, AC, KIND, CKM>(p, Hs, optr, len, win_out, sum, xr); break;
+        default: run6<NW, 3, AC, KIND, CKM>(p, Hs, optr, len, win_out, sum, xr); break;
     }
 }
 
-template <uint32_t NW, int AC, int KIND, bool CK>
+template <uint32_t NW, int AC, int KIND, int CKM>
 __device__ __forceinline__ void run6_ac(int ac, int rc, const M6Ctx& p, uint4 (&Hs)[S6<NW>::H], uint32_t* optr,
-                                        uint32_t len, uint32_t* win_out, unsigned long long& sum, uint32_t& xr) {
+                                        uint32_t len, uint32_t* win_out, CkAcc6<CKM>& sum, uint32_t& xr) {
     if constexpr (AC <= (int)S6<NW>::AC_MAX) {
         if (ac == AC)
-            run6_rc<NW, AC, KIND, CK>(rc, p, Hs, optr, len, win_out, sum, xr);
+            run6_rc<NW, AC, KIND, CKM>(rc, p, Hs, optr, len, win_out, sum, xr);
         else
-            run6_ac<NW, AC + 1, KIND, CK>(ac, rc, p, Hs, optr, len, win_out, sum, xr);
+            run6_ac<NW, AC + 1, KIND, CKM>(ac, rc, p, Hs, optr, len, win_out, sum, xr);
     }
 }
 
 }  // namespace
 
-template <uint32_t NW, int KIND, bool CK>
+template <uint32_t NW, int KIND, int CKM>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, MTGP6_MIN_CTAS) mt_gen3_kernel(MtGenArgs a) {
     using S = S6<NW>;
     const uint32_t warp = threadIdx.x >> 5;
@@ -276,17 +293,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MTGP6_MIN_CTAS) mt_gen3_ker
             win_out = a.win_out + (size_t)pc.set * S::N;
             for (uint32_t j = lane; j + len < S::N; j += 32) win_out[j] = w0[len + j];  // pieces shorter than n
         }
-        unsigned long long sum = 0;
+        CkAcc6<CKM> sum = 0;
         uint32_t xr = 0;
-        run6_ac<NW, 0, KIND, CK>(ac, rc, p, Hs, optr, len, win_out, sum, xr);
-        if (CK) {
+        run6_ac<NW, 0, KIND, CKM>(ac, rc, p, Hs, optr, len, win_out, sum, xr);
+        if (CKM) {
 #pragma unroll
             for (int s = 16; s > 0; s >>= 1) {
                 sum += __shfl_xor_sync(kFull6, sum, s);
                 xr ^= __shfl_xor_sync(kFull6, xr, s);
             }
             if (lane == 0) {
-                atomicAdd(&a.ck[pc.set].sum64, sum);
+                atomicAdd(&a.ck[pc.set].sum64, (unsigned long long)sum);  // mode 2: low half
                 atomicXor(&a.ck[pc.set].xor32, xr);
                 atomicAdd(&a.ck[pc.set].words, (unsigned long long)len);
             }
@@ -300,44 +317,48 @@ bool mt_gen3_supports(uint32_t n, uint32_t min_gap, int kind) {
            n == 624 && min_gap >= 129;
 }
 
-template <int KIND, bool CK>
+template <int KIND, int CKM>
 static int mt3_occ() {
     int c = 0;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, mt_gen3_kernel<624, KIND, CK>, kWarpsPerCta * 32, 0) ==
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, mt_gen3_kernel<624, KIND, CKM>, kWarpsPerCta * 32, 0) ==
                    cudaSuccess
-               ? c
+               ? (KIND >= kKindBitmapBit0 ? c : std::min(c, MTGP6_MAX_CTAS))  // stat passes: as before
                : 0;
 }
 
-cudaError_t launch_mt_gen3(uint32_t n, int kind, bool cksum, const MtGenArgs& a, cudaStream_t st) {
+cudaError_t launch_mt_gen3(uint32_t n, int kind, int ck_mode, const MtGenArgs& a, cudaStream_t st) {
     if (a.n_teams == 0) return cudaSuccess;
     if (n != 624) return cudaErrorInvalidValue;
     const uint32_t grid = (a.n_teams + kWarpsPerCta - 1) / kWarpsPerCta;
     const dim3 block(kWarpsPerCta * 32);
     if (kind == kKindBitmapBit0) {  // no checksums: the words are never output
-        mt_gen3_kernel<624, kKindBitmapBit0, false><<<grid, block, 0, st>>>(a);
+        mt_gen3_kernel<624, kKindBitmapBit0, 0><<<grid, block, 0, st>>>(a);
         return cudaGetLastError();
     }
     if (kind == kKindBitmapRange) {
-        mt_gen3_kernel<624, kKindBitmapRange, false><<<grid, block, 0, st>>>(a);
+        mt_gen3_kernel<624, kKindBitmapRange, 0><<<grid, block, 0, st>>>(a);
         return cudaGetLastError();
     }
-    switch ((kind == MTGP_F64_01 ? 2 : kind == MTGP_U32 ? 0 : 4) + (cksum ? 1 : 0)) {
-        case 0: mt_gen3_kernel<624, MTGP_U32, false><<<grid, block, 0, st>>>(a); break;
-        case 1: mt_gen3_kernel<624, MTGP_U32, true><<<grid, block, 0, st>>>(a); break;
-        case 2: mt_gen3_kernel<624, MTGP_F64_01, false><<<grid, block, 0, st>>>(a); break;
-        case 3: mt_gen3_kernel<624, MTGP_F64_01, true><<<grid, block, 0, st>>>(a); break;
+    switch ((kind == MTGP_F64_01 ? 3 : kind == MTGP_U32 ? 0 : 6) + ck_mode) {
+        case 0: mt_gen3_kernel<624, MTGP_U32, 0><<<grid, block, 0, st>>>(a); break;
+        case 1: mt_gen3_kernel<624, MTGP_U32, 1><<<grid, block, 0, st>>>(a); break;
+        case 2: mt_gen3_kernel<624, MTGP_U32, 2><<<grid, block, 0, st>>>(a); break;
+        case 3: mt_gen3_kernel<624, MTGP_F64_01, 0><<<grid, block, 0, st>>>(a); break;
+        case 4: mt_gen3_kernel<624, MTGP_F64_01, 1><<<grid, block, 0, st>>>(a); break;
+        case 5: mt_gen3_kernel<624, MTGP_F64_01, 2><<<grid, block, 0, st>>>(a); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
 }
 
-int mt_gen3_ctas_per_sm(uint32_t n, int kind, bool cksum) {
+int mt_gen3_ctas_per_sm(uint32_t n, int kind, int ck_mode) {
     if (n != 624) return 0;
-    if (kind == MTGP_U32) return cksum ? mt3_occ<MTGP_U32, true>() : mt3_occ<MTGP_U32, false>();
-    if (kind == MTGP_F64_01) return cksum ? mt3_occ<MTGP_F64_01, true>() : mt3_occ<MTGP_F64_01, false>();
-    if (kind == kKindBitmapBit0) return mt3_occ<kKindBitmapBit0, false>();
-    if (kind == kKindBitmapRange) return mt3_occ<kKindBitmapRange, false>();
+    if (kind == MTGP_U32)
+        return ck_mode == 2 ? mt3_occ<MTGP_U32, 2>() : ck_mode ? mt3_occ<MTGP_U32, 1>() : mt3_occ<MTGP_U32, 0>();
+    if (kind == MTGP_F64_01)
+        return ck_mode == 2 ? mt3_occ<MTGP_F64_01, 2>() : ck_mode ? mt3_occ<MTGP_F64_01, 1>() : mt3_occ<MTGP_F64_01, 0>();
+    if (kind == kKindBitmapBit0) return mt3_occ<kKindBitmapBit0, 0>();
+    if (kind == kKindBitmapRange) return mt3_occ<kKindBitmapRange, 0>();
     return 0;
 }
 

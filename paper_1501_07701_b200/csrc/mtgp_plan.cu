@@ -581,7 +581,7 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
     const bool use_v3 = v3_ok && (r.want_kernel == 3 || (r.want_kernel == 0 && I.M == 11213));
     const bool use_v4 = !use_v3 && v4_ok && (r.want_kernel == 4 || (r.want_kernel == 0 && I.M != 11213));
     const int ck_mode = r.cksum ? (r.ck32 ? 2 : 1) : 0;
-    const int cps = use_mt3  ? mt_gen3_ctas_per_sm(I.N, r.kind, r.cksum)
+    const int cps = use_mt3  ? mt_gen3_ctas_per_sm(I.N, r.kind, ck_mode)
                     : I.mt   ? mt_gen2_ctas_per_sm(I.N, r.kind, r.cksum)
                     : use_v3 ? gen3_ctas_per_sm(r.kind, ck_mode)
                     : use_v4 ? gen4_ctas_per_sm(I.M, r.kind, ck_mode)
@@ -698,7 +698,7 @@ cudaError_t Planner::run(PlanRun& r, std::string& err) {
         ma.pairs = r.L % 2 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 7) == 0;
         ma.pred = r.pred;
         if (r.timing) r.timing->record(r.stream, &g0);
-        e = use_mt3 ? launch_mt_gen3(I.N, r.kind, r.cksum, ma, r.stream)
+        e = use_mt3 ? launch_mt_gen3(I.N, r.kind, ck_mode, ma, r.stream)
                     : launch_mt_gen2(r.kind, r.cksum, ma, r.stream);
         if (e != cudaSuccess) return e;
         r.version = use_mt3 ? 6 : 5;

@@ -115,6 +115,23 @@ def test_multi_gpu_batch_c5(torch_cuda, devices, gather):
 
 
 @pytest.mark.skipif(not full_ck.available("mt19937"), reason="mt_full_ck.npz not generated")
+def test_mt19937_checksum_mode_sum32(torch_cuda):
+    """mt_gen3's 32-bit-sum checksum mode (the bench default) against the reference's fill()."""
+    torch = torch_cuda
+    n, _, rec = full_ck.coverage("mt19937")
+    out = torch.empty((n, rec), dtype=torch.int32, device="cuda")
+    with mtgp.MtContext([mtgp.mt19937_status()] * n, [5489 + i for i in range(n)]) as ctx:
+        ctx.set_option(mtgp.OPT_CHECKSUM, 2)
+        for k in range(6):
+            ctx.generate_device(mtgp.U32, out.data_ptr(), rec)
+            ctx.sync()
+            r = full_ck.compare("mt19937", 0, ctx.checksums(), sum_mod32=True)
+            assert r["ok"], (k, r)
+        assert ctx.last_plan()[2] == 6
+    del out
+
+
+@pytest.mark.skipif(not full_ck.available("mt19937"), reason="mt_full_ck.npz not generated")
 def test_mt19937_every_word_against_the_reference(torch_cuda):
     """bench.py --config mt19937 (Engine::mt, 200 MT19937 streams, seeds 5489 + i) with the
     default auto plan (mt_gen3 warp teams, jump-ahead pieces): after every 2^27-word call the
