@@ -91,41 +91,6 @@ __global__ void jump_qleaf_kernel(const JumpArgs a, const KaraPlan k, uint32_t* 
     }
 }
 
-#ifndef MTGP_LEAF_NIB
-#define MTGP_LEAF_NIB 0
-#endif
-// 4 q bits at a time (MTGP_LEAF_NIB): acc ^= XOR of the z words of the set bits, a 16-way
-// warp-uniform dispatch (ceil(k/2) LOP3 per output for k set bits, 1.25 on average, against
-// 1.5 for two 2-bit steps)
-template <uint32_t MASK>
-__device__ __forceinline__ void nib_apply(uint32_t (&acc)[kJ], const uint32_t* w) {
-#pragma unroll
-    for (int i = 0; i < kJ; ++i) {
-        uint32_t v = acc[i];
-        if (MASK & 1) v ^= w[i];
-        if (MASK & 2) v ^= w[1 + i];
-        if (MASK & 4) v ^= w[2 + i];
-        if (MASK & 8) v ^= w[3 + i];
-        acc[i] = v;
-    }
-}
-// binary decision tree over the nibble's bits, high bit first: 4 uniform branches per nibble
-template <uint32_t PREFIX, int BIT>
-__device__ __forceinline__ void nib_tree(uint32_t pat, uint32_t (&acc)[kJ], const uint32_t* w) {
-    if constexpr (BIT < 0) {
-        if constexpr (PREFIX != 0) nib_apply<PREFIX>(acc, w);
-    } else {
-        if (pat & (1u << BIT))
-            nib_tree<PREFIX | (1u << BIT), BIT - 1>(pat, acc, w);
-        else
-            nib_tree<PREFIX, BIT - 1>(pat, acc, w);
-    }
-}
-template <uint32_t M>
-__device__ __forceinline__ void nib_xor(uint32_t pat, uint32_t (&acc)[kJ], const uint32_t* w) {
-    if (pat) nib_tree<0, 3>(pat, acc, w);
-}
-
 template <bool DIRECT>
 __global__ void __launch_bounds__(kLeafWarps * 32, MTGP_LEAF_MINB) jump_leaf_kernel(const JumpArgs a, const KaraPlan k,
                                                                                   const uint32_t* __restrict__ qleaf,
@@ -182,10 +147,6 @@ __global__ void __launch_bounds__(kLeafWarps * 32, MTGP_LEAF_MINB) jump_leaf_ker
                     w[4 * v + 2] = g.z;
                     w[4 * v + 3] = g.w;
                 }
-#if MTGP_LEAF_NIB
-#pragma unroll
-                for (int bb = 0; bb < 32; bb += 4) nib_xor<0>((qw >> bb) & 15u, acc, w + bb);
-#else
 #pragma unroll
                 for (int bb = 0; bb < 32; bb += 2) {
                     const uint32_t pat = (qw >> bb) & 3u;
@@ -200,7 +161,6 @@ __global__ void __launch_bounds__(kLeafWarps * 32, MTGP_LEAF_MINB) jump_leaf_ker
                         for (int i = 0; i < kJ; ++i) acc[i] ^= w[bb + i] ^ w[bb + 1 + i];
                     }
                 }
-#endif
             }
             if (++iw == kHq) {
                 iw = 0;
