@@ -75,7 +75,7 @@ def parse():
                     help="MTGP_OPT_PREJUMP: speculative next-call jumps, 0 auto (library default), 1 off, 2 on")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1, help="end-to-end (host output) steps timed")
-    ap.add_argument("--e2e-words-per-call", type=int, default=1 << 22,
+    ap.add_argument("--e2e-words-per-call", type=int, default=1 << 20,
                     help="words per stream per mtgp_generate call in the e2e leg (reused pinned buffer)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-words-per-thread", type=int, default=1 << 28,
