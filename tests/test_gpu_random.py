@@ -2,6 +2,7 @@
 host / device outputs, host chunk sizes, output kinds, skips and state save/restore -- every
 word compared with the CPU oracle. Complements the targeted parity tests with combinations
 nobody wrote down."""
+import os
 import random
 
 import numpy as np
@@ -37,7 +38,8 @@ def _conv(u, kind):
     return f
 
 
-@pytest.mark.parametrize("case", range(40))
+# MTGP_RANDOM_CASES widens the sweep for a one-off long run (profiles/r2/random_sweep_long.txt)
+@pytest.mark.parametrize("case", range(int(os.environ.get("MTGP_RANDOM_CASES", "40"))))
 def test_random_request_sequences(case, curand_sets):
     rnd = random.Random(1501 + case)
     engine = rnd.choice(["mtgp11213", "mtgp23209", "mtgp44497", "mt"])
